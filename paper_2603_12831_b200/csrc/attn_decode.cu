@@ -1,0 +1,332 @@
+// K1 + K2: split-K paged flash-decoding over the GPU-resident KV pool.
+//
+// One CTA per (chunk of KV pages of one request, KV head).  KV pages
+// ([64 tokens x head_dim] per head) are staged into shared memory by TMA
+// (cp.async.bulk.tensor, SWIZZLE_128B boxes of 64 x 64) through a 3-stage
+// mbarrier pipeline.  The GQA group of query heads that share the KV head
+// forms the M=16 side of warp-level bf16 MMAs (QK^T and PV); the softmax is
+// online per warp with quad shuffles, and the 4 warps (16 tokens of each
+// page apiece) are merged through shared memory at the end.  Each CTA
+// writes a normalised partial output and its log-sum-exp; decode_combine
+// (K2) LSE-merges the partials of a request before the O projection.
+//
+// This is the work the reference charges as
+// probe_attention(gpu, DECODE, attn_tokens, g) in Engine._run_layer
+// (reference pkg/src/hybridserve/engine.py:939-942; loads accumulate ctx+1
+// per decode at engine.py:675,740).  The kernel is HBM-bound: it reads
+// sum(ctx+1) * 2 * n_kv * head_dim * 2 bytes per layer; the tensor-core
+// instruction used for the tiny GQA tiles is irrelevant to that bound.
+#include <math_constants.h>
+
+#include "hs_common.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+constexpr int kDecStages = 3;
+constexpr int kDecThreads = 128;
+
+int make_kv_map(CUtensorMap* map, const bf16* pool, const KvGeom& g) {
+  const uint64_t rows = static_cast<uint64_t>(g.layers) * g.pages * 2 * g.n_kv * kPageTokens;
+  return make_map_2d_bf16(map, pool, g.head_dim, rows, static_cast<uint64_t>(g.head_dim) * 2, 64,
+                          kPageTokens);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kDecThreads, 2)
+    decode_attn_kernel(const __grid_constant__ CUtensorMap kv_map, KvGeom geom, int layer,
+                       const bf16* __restrict__ q, int q_row_stride, int n_q,
+                       const int* __restrict__ page_table, int pt_stride,
+                       const DecodeChunk* __restrict__ chunks, float* __restrict__ o_part,
+                       float* __restrict__ lse_part, float scale_log2) {
+  constexpr int kBoxBytes = kPageTokens * 128;
+  constexpr int kHalf = (HD / 64) * kBoxBytes;  // K (or V) of one page
+  constexpr int kStageBytes = 2 * kHalf;
+  constexpr int NT = HD / 8;   // output n-tiles
+  constexpr int KS = HD / 16;  // k-steps over head_dim
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kDecStages];
+  __shared__ float sm_m[4][16], sm_l[4][16];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const DecodeChunk ch = chunks[blockIdx.x];
+  const int kvh = blockIdx.y;
+  const int G = n_q / geom.n_kv;
+  const int npages = ch.page_end - ch.page_begin;
+  const int* pt = page_table + static_cast<size_t>(ch.slot) * pt_stride + ch.page_begin;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&kv_map);
+    for (int s = 0; s < kDecStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int i) {
+    const int s = i % kDecStages;
+    const int phys = pt[i];
+    uint8_t* dst = smem + s * kStageBytes;
+    mbar_expect_tx(&full[s], kStageBytes);
+    const int rk = static_cast<int>(kv_row(geom, layer, phys, 0, kvh));
+    const int rv = static_cast<int>(kv_row(geom, layer, phys, 1, kvh));
+#pragma unroll
+    for (int b = 0; b < HD / 64; ++b) {
+      tma_load_2d(dst + b * kBoxBytes, &kv_map, &full[s], b * 64, rk);
+      tma_load_2d(dst + kHalf + b * kBoxBytes, &kv_map, &full[s], b * 64, rv);
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < min(kDecStages, npages); ++i) issue(i);
+  }
+
+  // Q fragments (A operand, rows = query heads of this GQA group)
+  uint32_t qa[KS][4];
+  {
+    const bf16* qrow = q + static_cast<size_t>(ch.row) * q_row_stride;
+    const int h0 = kvh * G + g, h1 = kvh * G + g + 8;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int d0 = ks * 16 + tig * 2;
+      uint32_t z = 0;
+      qa[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + h0 * HD + d0) : z;
+      qa[ks][1] = g + 8 < G ? *reinterpret_cast<const uint32_t*>(qrow + h1 * HD + d0) : z;
+      qa[ks][2] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + h0 * HD + d0 + 8) : z;
+      qa[ks][3] = g + 8 < G ? *reinterpret_cast<const uint32_t*>(qrow + h1 * HD + d0 + 8) : z;
+    }
+  }
+
+  float o[NT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
+  const int tb = warp * 16;  // this warp's 16 tokens inside every page
+
+  for (int i = 0; i < npages; ++i) {
+    const int s = i % kDecStages;
+    mbar_wait(&full[s], (i / kDecStages) & 1);
+    const int tok0 = (ch.page_begin + i) * kPageTokens + tb;
+    if (tok0 < ch.ctx) {  // warp-uniform
+      const uint32_t kbase = smem_u32(smem + s * kStageBytes);
+      const uint32_t vbase = kbase + kHalf;
+      float sc[2][4];
+#pragma unroll
+      for (int n = 0; n < 2; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+      {
+        const int mi = lane >> 3, r = lane & 7;
+        const int row = tb + (mi >> 1) * 8 + r;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(swz_addr(kbase, row, ks * 2 + (mi & 1)), b0, b1, b2, b3);
+          mma_bf16_16816(sc[0], qa[ks], b0, b1);
+          mma_bf16_16816(sc[1], qa[ks], b2, b3);
+        }
+      }
+      // scale, mask, online softmax (rows g and g+8)
+      float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+      for (int n = 0; n < 2; ++n) {
+        const int t = tok0 + n * 8 + tig * 2;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool ok = (t + (e & 1)) < ch.ctx;
+          sc[n][e] = ok ? sc[n][e] * scale_log2 : -CUDART_INF_F;
+        }
+        mx0 = fmaxf(mx0, fmaxf(sc[n][0], sc[n][1]));
+        mx1 = fmaxf(mx1, fmaxf(sc[n][2], sc[n][3]));
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float mu0 = mn0 == -CUDART_INF_F ? 0.f : mn0;
+      const float mu1 = mn1 == -CUDART_INF_F ? 0.f : mn1;
+      const float a0 = exp2f(m0 - mu0), a1 = exp2f(m1 - mu1);
+      m0 = mn0;
+      m1 = mn1;
+      float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+      for (int n = 0; n < 2; ++n) {
+        sc[n][0] = exp2f(sc[n][0] - mu0);
+        sc[n][1] = exp2f(sc[n][1] - mu0);
+        sc[n][2] = exp2f(sc[n][2] - mu1);
+        sc[n][3] = exp2f(sc[n][3] - mu1);
+        rs0 += sc[n][0] + sc[n][1];
+        rs1 += sc[n][2] + sc[n][3];
+      }
+      l0 = l0 * a0 + rs0;
+      l1 = l1 * a1 + rs1;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        o[nt][0] *= a0;
+        o[nt][1] *= a0;
+        o[nt][2] *= a1;
+        o[nt][3] *= a1;
+      }
+      uint32_t pa[4];
+      pa[0] = pack_bf16x2(sc[0][0], sc[0][1]);
+      pa[1] = pack_bf16x2(sc[0][2], sc[0][3]);
+      pa[2] = pack_bf16x2(sc[1][0], sc[1][1]);
+      pa[3] = pack_bf16x2(sc[1][2], sc[1][3]);
+      {
+        const int mi = lane >> 3, r = lane & 7;
+        const int row = tb + (mi & 1) * 8 + r;
+#pragma unroll
+        for (int j = 0; j < NT / 2; ++j) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(swz_addr(vbase, row, 2 * j + (mi >> 1)), b0, b1, b2, b3);
+          mma_bf16_16816(o[2 * j], pa, b0, b1);
+          mma_bf16_16816(o[2 * j + 1], pa, b2, b3);
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with stage s
+    if (threadIdx.x == 0 && i + kDecStages < npages) issue(i + kDecStages);
+  }
+
+  // quad-reduce the row sums
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  if (tig == 0) {
+    sm_m[warp][g] = m0;
+    sm_m[warp][g + 8] = m1;
+    sm_l[warp][g] = l0;
+    sm_l[warp][g + 8] = l1;
+  }
+  __syncthreads();
+  // cross-warp merge: rescale each warp's O to the common max, sum in smem
+  float M0 = -CUDART_INF_F, M1 = -CUDART_INF_F;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    M0 = fmaxf(M0, sm_m[w][g]);
+    M1 = fmaxf(M1, sm_m[w][g + 8]);
+  }
+  const float Mu0 = M0 == -CUDART_INF_F ? 0.f : M0, Mu1 = M1 == -CUDART_INF_F ? 0.f : M1;
+  const float f0 = exp2f(m0 - Mu0), f1 = exp2f(m1 - Mu1);
+  float* so = reinterpret_cast<float*>(smem);  // [4 warps][16 rows][HD]
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int d = nt * 8 + tig * 2;
+    so[(warp * 16 + g) * HD + d] = o[nt][0] * f0;
+    so[(warp * 16 + g) * HD + d + 1] = o[nt][1] * f0;
+    so[(warp * 16 + g + 8) * HD + d] = o[nt][2] * f1;
+    so[(warp * 16 + g + 8) * HD + d + 1] = o[nt][3] * f1;
+  }
+  __syncthreads();
+  const int base = (blockIdx.x * geom.n_kv + kvh) * G;
+  for (int idx = threadIdx.x; idx < G * HD; idx += kDecThreads) {
+    const int r = idx / HD, d = idx % HD;
+    float Mr = -CUDART_INF_F;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) Mr = fmaxf(Mr, sm_m[w][r]);
+    const float Mur = Mr == -CUDART_INF_F ? 0.f : Mr;
+    float L = 0.f, acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      L += sm_l[w][r] * exp2f(sm_m[w][r] - Mur);
+      acc += so[(w * 16 + r) * HD + d];
+    }
+    o_part[static_cast<size_t>(base + r) * HD + d] = L > 0.f ? acc / L : 0.f;
+    if (d == 0)
+      lse_part[base + r] = L > 0.f ? (Mur + log2f(L)) * 0.69314718055994530942f : -CUDART_INF_F;
+  }
+}
+
+// K2: merge the split partials of each (row, query head).  One warp per pair.
+template <int HD>
+__global__ void decode_combine_kernel(const float* __restrict__ o_part,
+                                      const float* __restrict__ lse_part,
+                                      const int* __restrict__ row_chunk_begin, int rows, int n_q,
+                                      int n_kv, bf16* __restrict__ out, int out_row_stride,
+                                      float* __restrict__ lse_out) {
+  const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pair >= rows * n_q) return;
+  const int row = pair / n_q, h = pair % n_q;
+  const int G = n_q / n_kv;
+  const int kvh = h / G, gi = h % G;
+  const int c0 = row_chunk_begin[row], c1 = row_chunk_begin[row + 1];
+  float mx = -CUDART_INF_F;
+  for (int c = c0; c < c1; ++c) mx = fmaxf(mx, lse_part[(c * n_kv + kvh) * G + gi]);
+  const float mu = mx == -CUDART_INF_F ? 0.f : mx;
+  constexpr int PER = HD / 32;
+  float acc[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) acc[j] = 0.f;
+  float wsum = 0.f;
+  for (int c = c0; c < c1; ++c) {
+    const int idx = (c * n_kv + kvh) * G + gi;
+    const float w = __expf(lse_part[idx] - mu);
+    wsum += w;
+    const float* src = o_part + static_cast<size_t>(idx) * HD;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) acc[j] += w * src[lane + 32 * j];
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  bf16* dst = out + static_cast<size_t>(row) * out_row_stride + h * HD;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) dst[lane + 32 * j] = __float2bfloat16(acc[j] * inv);
+  if (lse_out && lane == 0) lse_out[pair] = wsum > 0.f ? mu + logf(wsum) : -CUDART_INF_F;
+}
+
+template <int HD>
+static int launch_decode(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                         int q_row_stride, int n_q, const int* pt, int pt_stride,
+                         const DecodeChunk* chunks, int n_chunks, float* o_part, float* lse_part,
+                         cudaStream_t st) {
+  constexpr int kStageBytes = 2 * (HD / 64) * kPageTokens * 128;
+  constexpr int kSmem = kDecStages * kStageBytes + 1024;
+  static_assert(4 * 16 * HD * 4 <= kDecStages * kStageBytes, "merge scratch must fit");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmem);
+    attr = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
+  dim3 grid(n_chunks, g.n_kv);
+  decode_attn_kernel<HD><<<grid, kDecThreads, kSmem, st>>>(kv_map, g, layer, q, q_row_stride, n_q,
+                                                           pt, pt_stride, chunks, o_part, lse_part,
+                                                           scale_log2);
+  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+}
+
+int decode_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                     int q_row_stride, int n_q, const int* page_table, int pt_stride,
+                     const DecodeChunk* chunks, int n_chunks, float* o_part, float* lse_part,
+                     cudaStream_t st) {
+  if (n_chunks <= 0) return HS_OK;
+  if (n_q % g.n_kv || n_q / g.n_kv > 16) return HS_E_CONFIG;
+  if (g.head_dim == 128)
+    return launch_decode<128>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride,
+                              chunks, n_chunks, o_part, lse_part, st);
+  if (g.head_dim == 64)
+    return launch_decode<64>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride, chunks,
+                             n_chunks, o_part, lse_part, st);
+  return HS_E_CONFIG;
+}
+
+int decode_combine(const float* o_part, const float* lse_part, const int* row_chunk_begin,
+                   int rows, int n_q, int n_kv, int head_dim, bf16* out, int out_row_stride,
+                   float* lse_out, cudaStream_t st) {
+  if (rows <= 0) return HS_OK;
+  const int blocks = (rows * n_q + 3) / 4;
+  if (head_dim == 128)
+    decode_combine_kernel<128><<<blocks, 128, 0, st>>>(o_part, lse_part, row_chunk_begin, rows,
+                                                       n_q, n_kv, out, out_row_stride, lse_out);
+  else if (head_dim == 64)
+    decode_combine_kernel<64><<<blocks, 128, 0, st>>>(o_part, lse_part, row_chunk_begin, rows,
+                                                      n_q, n_kv, out, out_row_stride, lse_out);
+  else
+    return HS_E_CONFIG;
+  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+}
+
+}  // namespace hs

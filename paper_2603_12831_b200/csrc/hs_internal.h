@@ -1,0 +1,82 @@
+// Internal launcher declarations shared by the libhs translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hs.h"
+
+typedef __nv_bfloat16 bf16;
+
+namespace hs {
+
+// ---- TMA maps / GEMM (gemm_tcgen05.cu) ----
+int make_map_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+int make_weight_map(CUtensorMap* map, const bf16* w, int n_out, int k);
+int make_act_map(CUtensorMap* map, const bf16* x, int rows, int k, int ld, int bn);
+int gemm_pick_bn(int tokens);
+int gemm_pick_splits(int n_out, int k, int tokens, int bn, int max_splits);
+int gemm_launch(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,
+                int tokens, int k, int splits, cudaStream_t st);
+
+// ---- KV pool geometry ----
+// pool layout: [layers][pages][2 (K,V)][n_kv][64 tokens][head_dim] bf16
+struct KvGeom {
+  int layers, pages, n_kv, head_dim;
+};
+__host__ __device__ inline int64_t kv_row(const KvGeom& g, int layer, int page, int kv, int head) {
+  return ((((int64_t)layer * g.pages + page) * 2 + kv) * g.n_kv + head) * 64;
+}
+int make_kv_map(CUtensorMap* map, const bf16* pool, const KvGeom& g);
+
+// ---- attention (attn_decode.cu / attn_prefill.cu) ----
+struct DecodeChunk {
+  int row;         // decode row (index into q / output)
+  int slot;        // request slot (page-table row)
+  int page_begin;  // first logical page of this chunk
+  int page_end;    // one past last logical page
+  int ctx;         // valid kv tokens of the request (context + new token)
+};
+int decode_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                     int q_row_stride, int n_q, const int* page_table, int pt_stride,
+                     const DecodeChunk* chunks, int n_chunks, float* o_part, float* lse_part,
+                     cudaStream_t st);
+int decode_combine(const float* o_part, const float* lse_part, const int* row_chunk_begin,
+                   int rows, int n_q, int n_kv, int head_dim, bf16* out, int out_row_stride,
+                   float* lse_out, cudaStream_t st);
+
+struct PrefillTile {
+  int slot;   // request slot
+  int q_row;  // first row of this tile in q / output
+  int pos0;   // absolute position of the tile's first query token
+  int nq;     // query rows in this tile (<= 64)
+};
+int prefill_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                      int q_row_stride, int n_q, const int* page_table, int pt_stride,
+                      const PrefillTile* tiles, int n_tiles, bf16* out, int out_row_stride,
+                      cudaStream_t st);
+
+// ---- elementwise (elementwise.cu) ----
+int embed_gather(const int* tokens, int rows, const bf16* emb, int d, float* h, cudaStream_t st);
+int rmsnorm_rows(const float* h, int rows, int d, const float* w, float eps, bf16* out, int ld_out,
+                 cudaStream_t st);
+int splitk_reduce(const float* part, int splits, int rows, int n, float* out, cudaStream_t st);
+int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
+                      float eps, bf16* out, int ld_out, cudaStream_t st);
+int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv, int head_dim,
+                     const float* rope_cos, const float* rope_sin, const int* row_pos,
+                     const int* row_slot, const int* row_mode, bf16* qbuf, int q_row_stride,
+                     bf16* kv_pool, const KvGeom& g, int layer, const int* page_table,
+                     int pt_stride, bf16* ship, int ship_stride, cudaStream_t st);
+int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld_act,
+             cudaStream_t st);
+int argmax_rows(const float* part, int splits, int rows, int vocab, int* tokens, float* logits_out,
+                cudaStream_t st);
+int lse_merge_rows(const bf16* parts, const float* lse, int n_parts, int rows, int n_q,
+                   int head_dim, int part_stride, int row_stride_parts, bf16* out,
+                   int out_row_stride, cudaStream_t st);
+
+}  // namespace hs
