@@ -114,6 +114,107 @@ int hs_op_lse_merge(const void* parts, const float* lse, int n_parts, int rows, 
                     int head_dim, int part_stride, int row_stride_parts, void* out,
                     int out_row_stride, void* stream);
 
+/* ------------------------------------------------------------ step level
+ * One context per GPU replica.  It owns the weights, the paged KV pool, the
+ * device residual store (ResidualStore, engine.py:133-161), the pinned
+ * piggyback mailboxes (one q|k|v ship row and one result row per request
+ * slot: a chain has at most one item in flight, engine.py:982-1022), the
+ * pinned host KV arena of offloaded requests and the CPU-attention pool.
+ */
+typedef struct hs_ctx hs_ctx;
+
+typedef struct {
+  int d_model, n_layers, n_q, n_kv, head_dim, ffn, vocab;
+  float rope_theta, norm_eps;
+} hs_model_cfg;
+
+typedef struct {
+  int max_rows;          /* batch tokens + piggyback rows entering one layer   */
+  int max_slots;         /* concurrent requests                                 */
+  int kv_pages;          /* 64-token pages in the GPU KV pool                   */
+  int max_pages_per_req; /* page-table width                                    */
+  int max_pos;           /* RoPE table length                                   */
+  int max_chunks;        /* split-K decode-attention work items per layer       */
+  int cpu_threads;       /* CPU attention workers of this replica               */
+  int64_t host_kv_bytes; /* pinned host KV arena (offloaded BE requests)        */
+  int device;
+} hs_rt_cfg;
+
+enum {
+  HS_W_EMBED = 0, HS_W_LM_HEAD = 1, HS_W_FINAL_NORM = 2, HS_W_QKV = 3, HS_W_O = 4,
+  HS_W_GATE_UP = 5, HS_W_DOWN = 6, HS_W_NORM_IN = 7, HS_W_NORM_POST = 8
+};
+
+/* Engine.__init__ (engine.py:251-298) device side. */
+int hs_create(const hs_model_cfg* model, const hs_rt_cfg* rt, hs_ctx** out);
+int hs_destroy(hs_ctx* ctx);
+void* hs_stream(hs_ctx* ctx);
+/* bf16 matrices [out][in] (qkv rows: q heads, k heads, v heads; gate_up
+ * rows: gate then up), fp32 norm vectors.  Layer is 0-based. */
+int hs_set_weight(hs_ctx* ctx, int kind, int layer, const void* host, size_t bytes);
+/* synthetic N(0, std) bf16 weights generated on the device, norms = 1 */
+int hs_init_weights(hs_ctx* ctx, uint64_t seed, float std);
+/* page ids of a request slot (KvManager token accounting, engine.py:194-230) */
+int hs_set_page_table(hs_ctx* ctx, int slot, const int* pages, int n);
+
+/* host KV of offloaded requests (_distribute_offload, engine.py:402-419) */
+int hs_host_kv_reserve(hs_ctx* ctx, int slot, int cap_tokens);
+int hs_host_kv_release(hs_ctx* ctx, int slot);
+int hs_host_kv_ptr(hs_ctx* ctx, int slot, void** host_ptr, int* cap_tokens);
+/* one-shot KV transfer of `tokens` entries (swap-out / swap-in,
+ * engine.py:421-508): GPU pages of the slot <-> its host region */
+int hs_swap_out(hs_ctx* ctx, int slot, int tokens);
+int hs_swap_in(hs_ctx* ctx, int slot, int tokens);
+
+/* Iteration (BatchPlan) descriptor; rows = decodes first, then chunk tokens. */
+typedef struct {
+  int n_rows, n_decode;
+  const int* row_slot;   /* [n_rows] */
+  const int* row_pos;    /* [n_rows] absolute position of the row's token */
+  const int* row_token;  /* [n_rows] token id, or -1 = the slot's last generated token */
+  int n_chunks;
+  const int* chunks;          /* [n_chunks][5] decode split-K work items */
+  const int* row_chunk_begin; /* [n_decode+1] */
+  int n_tiles;
+  const int* tiles;      /* [n_tiles][4] prefill tiles */
+  int n_logit_rows;
+  const int* logit_rows; /* rows producing a token at the last layer */
+} hs_iter_desc;
+
+/* Per-layer piggyback descriptor (_consume_merges + _process_merge,
+ * engine.py:902-1022). */
+typedef struct {
+  int layer;             /* 1-based */
+  int n_carry;           /* QKV(layer)-only rows shipped to the host: layer 1 =
+                            injected fresh tokens, else chains merged at layer-1 */
+  const int* carry_slot;
+  const int* carry_pos;
+  int n_merge;           /* host results merged at this layer (Proj + MLP) */
+  const int* merge_slot;
+  int n_restart;         /* last layer: merged chains continuing with the next
+                            token (embed + QKV(1) + ship) */
+  const int* restart_idx;  /* indices into merge_slot */
+  const int* restart_pos;
+} hs_layer_desc;
+
+int hs_iter_begin(hs_ctx* ctx, const hs_iter_desc* desc);
+/* Engine._run_layer (engine.py:921-950) on the device. */
+int hs_layer(hs_ctx* ctx, const hs_layer_desc* desc);
+/* Waits for the iteration; copies its greedy tokens (logit rows, then the
+ * chains merged at the last layer) and returns their count. */
+int hs_iter_end(hs_ctx* ctx, int* tokens_out, int n);
+/* CPU attention service of n work items (slot, 1-based layer, ctx):
+ * appends each item's new k/v to the host KV and writes the attention
+ * result row into the slot's result mailbox (engine.py:529-560). */
+int hs_cpu_attend(hs_ctx* ctx, const int* slots, const int* layers, const int* ctxs, int n);
+int hs_sync(hs_ctx* ctx);
+
+/* test taps */
+int hs_keep_logits(hs_ctx* ctx, int on);
+int hs_read_logits(hs_ctx* ctx, float* host, int rows);
+int hs_read_ship(hs_ctx* ctx, int slot, void* host, size_t bytes);
+int hs_read_residual(hs_ctx* ctx, int slot, float* host);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -67,7 +67,8 @@ def rmsnorm(h: np.ndarray, w: np.ndarray, eps: float) -> np.ndarray:
 
 def gemm(x: np.ndarray, w: np.ndarray) -> np.ndarray:
     """x [t, k] @ w[n, k]^T with fp64 accumulation -> fp32."""
-    return (x.astype(np.float64) @ w.astype(np.float64).T).astype(np.float32)
+    return (x.astype(np.float64, copy=False) @ w.astype(np.float64, copy=False).T).astype(
+        np.float32)
 
 
 def silu_mul(gate_up: np.ndarray, ffn: int) -> np.ndarray:

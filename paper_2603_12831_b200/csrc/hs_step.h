@@ -1,0 +1,68 @@
+// Internal declarations of the serving-step context (step.cu, cpu_attn.cpp).
+#pragma once
+
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "hs_internal.h"
+
+namespace hs {
+
+int select_tokens(const int* row_token, const int* row_slot, const int* last_token, int rows,
+                  int* tok, cudaStream_t st);
+int gather_rows_f32(const float* src, const int* idx, int rows, int d, float* dst,
+                    cudaStream_t st);
+int scatter_rows_f32(const float* src, const int* idx, int rows, int d, float* dst,
+                     cudaStream_t st);
+int gather_rows_bf16(const bf16* src, int src_stride, const int* idx, int rows, int w, bf16* dst,
+                     int dst_stride, cudaStream_t st);
+int scatter_tokens(const int* tok, const int* slot, int n, int* last_token, cudaStream_t st);
+int kv_swap(bool to_host, bf16* pool, const KvGeom& g, const int* pages, int tokens, bf16* host,
+            int cap, cudaStream_t st);
+
+int set_error(int code, const char* fmt, ...);
+
+// ---------------------------------------------------------------- CPU pool
+// Fixed set of worker threads running parallel_for bodies (the BE
+// CPU-attention service, reference engine.py:529-554; §4 uses an
+// OpenMP pool per GPU).  Workers are pinned to `cpus` when given.
+class ThreadPool {
+ public:
+  explicit ThreadPool(int n, const std::vector<int>& cpus = {});
+  ~ThreadPool();
+  int size() const { return static_cast<int>(workers_.size()) + 1; }
+  // runs body(i) for i in [0, n) on the pool plus the calling thread
+  void parallel_for(int n, const std::function<void(int)>& body);
+
+ private:
+  void loop(int id);
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* body_ = nullptr;
+  int n_ = 0;
+  std::atomic<int> next_{0};
+  int active_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+struct ModelCfg {
+  int d, layers, n_q, n_kv, hd, ffn, vocab;
+  float theta, eps;
+  int qkv_n() const { return (n_q + 2 * n_kv) * hd; }
+};
+
+// Host-side decode attention for one offloaded request and one layer:
+// appends the new token's k/v at position ctx of the request's host KV
+// ([layers][2][n_kv][cap][hd] bf16) and attends q over ctx+1 entries.
+void cpu_attend_head(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int cap, int layer,
+                     int ctx, int h, bf16* out_row, float* lse_out);
+void cpu_attend_one(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int cap, int layer,
+                    int ctx, bf16* out_row, float* lse_out);
+
+}  // namespace hs

@@ -1,0 +1,770 @@
+// The serving-step context: one per GPU replica.
+//
+// Owns the model weights, the paged KV pool, the device residual store, the
+// pinned (mapped) piggyback mailboxes, the pinned host KV arena of offloaded
+// requests and the CPU-attention worker pool, and launches one transformer
+// layer over the concatenated LS+BE rows per hs_layer() call.  This is the
+// real work behind Engine._run_layer (reference
+// pkg/src/hybridserve/engine.py:921-950):
+//
+//   rows [0, B)        batch rows of the iteration plan (decodes, chunk tokens)
+//   rows [B, B+C)      carry rows: QKV(l) of piggyback chains, shipped D2H
+//                      (layer 1: injected fresh tokens, engine.py:995-998;
+//                       l > 1: chains merged at l-1, engine.py:1002-1004)
+//   rows [B, B+M)      merged rows: host attention results entering
+//                      Proj + ResidualAdd + MLP + ResidualAdd at layer l
+//                      (engine.py:999-1001), residual fetched from the store
+//
+// All launches go to one stream; nothing here blocks on the host except
+// hs_iter_end (token readback) and hs_cpu_attend (replay-mode service).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "hs_common.cuh"
+#include "hs_internal.h"
+#include "hs_step.h"
+
+namespace hs {
+
+static const int kBns[5] = {16, 32, 64, 128, 256};
+static int bn_index(int bn) {
+  for (int i = 0; i < 5; ++i)
+    if (kBns[i] == bn) return i;
+  return 4;
+}
+
+struct ActBuf {  // a bf16 activation buffer with one TMA map per token-tile width
+  bf16* p = nullptr;
+  int rows = 0, k = 0;
+  CUtensorMap maps[5];
+};
+
+struct HostRegion {
+  size_t offset = 0;  // bytes into the arena
+  int cap = 0;        // tokens
+  bool used = false;
+};
+
+}  // namespace hs
+
+using namespace hs;
+
+struct hs_ctx {
+  ModelCfg m{};
+  hs_rt_cfg r{};
+  cudaStream_t st = nullptr;
+  KvGeom geom{};
+  // weights
+  bf16 *w_embed = nullptr, *w_lm = nullptr;
+  float* w_final = nullptr;
+  std::vector<bf16*> w_qkv, w_o, w_gu, w_down;
+  std::vector<float*> n_in, n_post;
+  std::vector<CUtensorMap> m_qkv, m_o, m_gu, m_down;
+  CUtensorMap m_lm{};
+  // kv
+  bf16* kv_pool = nullptr;
+  CUtensorMap m_kv{};
+  int* page_table = nullptr;
+  // activations
+  float* h = nullptr;      // residual stream [max_rows][d]
+  float* hr = nullptr;     // restart rows [max_rows][d]
+  ActBuf xn, xn2, attn, act, lin, xr;
+  bf16* qbuf = nullptr;
+  float* part = nullptr;
+  size_t part_floats = 0;
+  float *o_part = nullptr, *lse_part = nullptr;
+  float* resid = nullptr;  // device residual store [max_slots][d]
+  int* last_token = nullptr;
+  int* tok = nullptr;
+  int* tok_out = nullptr;
+  float *rope_cos = nullptr, *rope_sin = nullptr;
+  float* logits = nullptr;  // optional debug copy of the last LM-head logits
+  bool keep_logits = false;
+  // metadata (device) and pinned staging
+  int* dm = nullptr;   // iteration + layer metadata
+  int* hm = nullptr;   // pinned staging (two halves)
+  size_t meta_ints = 0;
+  int stage_half = 0;
+  size_t stage_pos = 0;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  // iteration state
+  int B = 0, D = 0, n_chunks = 0, n_tiles = 0, n_logit = 0, n_tok_out = 0, merges_L = 0;
+  int* tokens_pinned = nullptr;
+  // piggyback mailboxes (pinned, mapped)
+  bf16 *ship_h = nullptr, *ship_d = nullptr, *result_h = nullptr, *result_d = nullptr;
+  // host KV arena (pinned, mapped)
+  bf16 *hkv_h = nullptr, *hkv_d = nullptr;
+  size_t hkv_bytes = 0;
+  std::vector<HostRegion> regions;
+  std::vector<std::pair<size_t, size_t>> free_list;  // (offset, bytes)
+  ThreadPool* pool = nullptr;
+};
+
+namespace {
+
+// ---- metadata offsets (ints) inside dm / staging ----
+struct MetaLayout {
+  size_t row_slot, row_pos, row_token, row_mode, chunks, row_chunk_begin, tiles, logit_rows,
+      logit_slot, merge_slot, restart_slot, restart_pos, restart_token, restart_mode, total;
+};
+
+MetaLayout layout_of(const hs_rt_cfg& r) {
+  MetaLayout L{};
+  size_t o = 0;
+  const size_t R = r.max_rows;
+  L.row_slot = o; o += R;
+  L.row_pos = o; o += R;
+  L.row_token = o; o += R;
+  L.row_mode = o; o += R;
+  L.chunks = o; o += static_cast<size_t>(r.max_chunks) * 5;
+  L.row_chunk_begin = o; o += R + 1;
+  L.tiles = o; o += R * 4;
+  L.logit_rows = o; o += R;
+  L.logit_slot = o; o += R;
+  L.merge_slot = o; o += R;
+  L.restart_slot = o; o += R;
+  L.restart_pos = o; o += R;
+  L.restart_token = o; o += R;
+  L.restart_mode = o; o += R;
+  L.total = o;
+  return L;
+}
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      return set_error(HS_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x,                  \
+                       cudaGetErrorString(e_));                                            \
+  } while (0)
+
+#define RC(x)                                                                              \
+  do {                                                                                     \
+    int rc_ = (x);                                                                         \
+    if (rc_ != HS_OK) {                                                                    \
+      if (rc_ == HS_E_CUDA)                                                                \
+        return set_error(HS_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x,                \
+                         cudaGetErrorString(cudaGetLastError()));                          \
+      return set_error(rc_, "%s:%d %s failed", __FILE__, __LINE__, #x);                    \
+    }                                                                                      \
+  } while (0)
+
+template <typename T>
+int dalloc(T** p, size_t n) {
+  CK(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T)));
+  return HS_OK;
+}
+
+int make_act(ActBuf& a, int rows, int k) {
+  RC(dalloc(&a.p, static_cast<size_t>(rows) * k));
+  a.rows = rows;
+  a.k = k;
+  for (int i = 0; i < 5; ++i)
+    if (make_act_map(&a.maps[i], a.p, rows, k, k, kBns[i]) != HS_OK)
+      return set_error(HS_E_CUDA, "activation map encode failed");
+  return HS_OK;
+}
+
+// GEMM over `tokens` rows of an activation buffer against a cached weight map.
+int gemm(hs_ctx* c, const CUtensorMap& mw, const ActBuf& x, int tokens, int n_out, int k,
+         int* splits_out) {
+  if (tokens <= 0) {
+    *splits_out = 1;
+    return HS_OK;
+  }
+  const int bn = gemm_pick_bn(tokens);
+  const size_t per_split = static_cast<size_t>(tokens) * n_out;
+  const int cap = static_cast<int>(std::min<size_t>(16, c->part_floats / per_split));
+  if (cap < 1) return set_error(HS_E_CAPACITY, "split-K buffer too small for %d x %d", tokens, n_out);
+  const int splits = gemm_pick_splits(n_out, k, tokens, bn, cap);
+  *splits_out = splits;
+  return gemm_launch(mw, x.maps[bn_index(bn)], bn, c->part, n_out, tokens, k, splits, c->st);
+}
+
+int* stage(hs_ctx* c, size_t n) {
+  // pinned staging ring: half per iteration, guarded by the event of the
+  // iteration that last used it
+  const size_t half = c->meta_ints;
+  if (c->stage_pos + n > half) return nullptr;
+  int* p = c->hm + c->stage_half * half + c->stage_pos;
+  c->stage_pos += n;
+  return p;
+}
+
+int upload(hs_ctx* c, size_t dst_off, const int* src, size_t n) {
+  if (n == 0) return HS_OK;
+  int* s = stage(c, n);
+  if (!s) return set_error(HS_E_CAPACITY, "metadata staging overflow");
+  std::memcpy(s, src, n * sizeof(int));
+  CK(cudaMemcpyAsync(c->dm + dst_off, s, n * sizeof(int), cudaMemcpyHostToDevice, c->st));
+  return HS_OK;
+}
+
+int upload_fill(hs_ctx* c, size_t dst_off, int value, size_t n) {
+  if (n == 0) return HS_OK;
+  int* s = stage(c, n);
+  if (!s) return set_error(HS_E_CAPACITY, "metadata staging overflow");
+  for (size_t i = 0; i < n; ++i) s[i] = value;
+  CK(cudaMemcpyAsync(c->dm + dst_off, s, n * sizeof(int), cudaMemcpyHostToDevice, c->st));
+  return HS_OK;
+}
+
+// deterministic N(0, std) weights from a counter hash (splitmix64 + Box-Muller)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_normal_kernel(bf16* w, size_t n, uint64_t seed, float std) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint64_t a = mix64(seed ^ (i * 2 + 0x1234567ull));
+    const uint64_t b = mix64(a ^ 0xA5A5A5A5DEADBEEFull);
+    const float u1 = (static_cast<float>(a >> 40) + 1.0f) * (1.0f / 16777217.0f);
+    const float u2 = static_cast<float>(b >> 40) * (1.0f / 16777216.0f);
+    const float z = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+    w[i] = __float2bfloat16(z * std);
+  }
+}
+
+__global__ void fill_f32_kernel(float* p, size_t n, float v) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+int rope_init(hs_ctx* c) {
+  const int half = c->m.hd / 2;
+  std::vector<float> cs(static_cast<size_t>(c->r.max_pos) * half), sn(cs.size());
+  std::vector<float> inv(half);
+  for (int i = 0; i < half; ++i)
+    inv[i] = static_cast<float>(
+        1.0 / std::pow(static_cast<double>(c->m.theta),
+                       static_cast<double>(static_cast<float>(2 * i) / static_cast<float>(c->m.hd))));
+  for (int p = 0; p < c->r.max_pos; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double a = static_cast<double>(p) * static_cast<double>(inv[i]);
+      cs[static_cast<size_t>(p) * half + i] = static_cast<float>(std::cos(a));
+      sn[static_cast<size_t>(p) * half + i] = static_cast<float>(std::sin(a));
+    }
+  RC(dalloc(&c->rope_cos, cs.size()));
+  RC(dalloc(&c->rope_sin, sn.size()));
+  CK(cudaMemcpy(c->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  return HS_OK;
+}
+
+int build_maps(hs_ctx* c) {
+  const ModelCfg& m = c->m;
+  c->m_qkv.resize(m.layers);
+  c->m_o.resize(m.layers);
+  c->m_gu.resize(m.layers);
+  c->m_down.resize(m.layers);
+  for (int l = 0; l < m.layers; ++l) {
+    if (make_weight_map(&c->m_qkv[l], c->w_qkv[l], m.qkv_n(), m.d) ||
+        make_weight_map(&c->m_o[l], c->w_o[l], m.d, m.n_q * m.hd) ||
+        make_weight_map(&c->m_gu[l], c->w_gu[l], 2 * m.ffn, m.d) ||
+        make_weight_map(&c->m_down[l], c->w_down[l], m.d, m.ffn))
+      return set_error(HS_E_CUDA, "weight map encode failed");
+  }
+  if (make_weight_map(&c->m_lm, c->w_lm, m.vocab, m.d))
+    return set_error(HS_E_CUDA, "lm head map encode failed");
+  return HS_OK;
+}
+
+void free_all(hs_ctx* c) {
+  auto F = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  F(c->w_embed);
+  F(c->w_lm);
+  F(c->w_final);
+  for (auto p : c->w_qkv) F(p);
+  for (auto p : c->w_o) F(p);
+  for (auto p : c->w_gu) F(p);
+  for (auto p : c->w_down) F(p);
+  for (auto p : c->n_in) F(p);
+  for (auto p : c->n_post) F(p);
+  F(c->kv_pool);
+  F(c->page_table);
+  F(c->h);
+  F(c->hr);
+  for (ActBuf* a : {&c->xn, &c->xn2, &c->attn, &c->act, &c->lin, &c->xr}) F(a->p);
+  F(c->qbuf);
+  F(c->part);
+  F(c->o_part);
+  F(c->lse_part);
+  F(c->resid);
+  F(c->last_token);
+  F(c->tok);
+  F(c->tok_out);
+  F(c->rope_cos);
+  F(c->rope_sin);
+  F(c->logits);
+  F(c->dm);
+  if (c->hm) cudaFreeHost(c->hm);
+  if (c->tokens_pinned) cudaFreeHost(c->tokens_pinned);
+  if (c->ship_h) cudaFreeHost(c->ship_h);
+  if (c->result_h) cudaFreeHost(c->result_h);
+  if (c->hkv_h) cudaFreeHost(c->hkv_h);
+  for (auto& e : c->stage_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c->pool;
+}
+
+int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
+  ModelCfg& m = c->m;
+  m = ModelCfg{mc->d_model, mc->n_layers, mc->n_q, mc->n_kv, mc->head_dim, mc->ffn, mc->vocab,
+               mc->rope_theta, mc->norm_eps};
+  c->r = *rc;
+  const hs_rt_cfg& r = c->r;
+  if (m.d % 128 || m.ffn % 128 || m.vocab % 128 || (m.hd != 64 && m.hd != 128) ||
+      m.n_q % m.n_kv || m.n_q / m.n_kv > 16 || (m.n_q * m.hd) % 64 || m.qkv_n() % 128)
+    return set_error(HS_E_CONFIG, "model dims unsupported (d/ffn/vocab %% 128, hd 64|128, G<=16)");
+  if (r.max_rows < 1 || r.max_slots < 1 || r.kv_pages < 1 || r.max_pages_per_req < 1 ||
+      r.max_pos < 1 || r.max_chunks < 1)
+    return set_error(HS_E_CONFIG, "runtime capacities must be >= 1");
+  CK(cudaSetDevice(r.device));
+  CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  // weights
+  const size_t d = m.d;
+  RC(dalloc(&c->w_embed, static_cast<size_t>(m.vocab) * d));
+  RC(dalloc(&c->w_lm, static_cast<size_t>(m.vocab) * d));
+  RC(dalloc(&c->w_final, d));
+  c->w_qkv.assign(m.layers, nullptr);
+  c->w_o.assign(m.layers, nullptr);
+  c->w_gu.assign(m.layers, nullptr);
+  c->w_down.assign(m.layers, nullptr);
+  c->n_in.assign(m.layers, nullptr);
+  c->n_post.assign(m.layers, nullptr);
+  for (int l = 0; l < m.layers; ++l) {
+    RC(dalloc(&c->w_qkv[l], static_cast<size_t>(m.qkv_n()) * d));
+    RC(dalloc(&c->w_o[l], d * m.n_q * m.hd));
+    RC(dalloc(&c->w_gu[l], 2 * static_cast<size_t>(m.ffn) * d));
+    RC(dalloc(&c->w_down[l], d * m.ffn));
+    RC(dalloc(&c->n_in[l], d));
+    RC(dalloc(&c->n_post[l], d));
+  }
+  RC(build_maps(c));
+  // kv pool
+  c->geom = KvGeom{m.layers, r.kv_pages, m.n_kv, m.hd};
+  RC(dalloc(&c->kv_pool, static_cast<size_t>(m.layers) * r.kv_pages * 2 * m.n_kv * kPageTokens *
+                             m.hd));
+  if (make_kv_map(&c->m_kv, c->kv_pool, c->geom)) return set_error(HS_E_CUDA, "kv map failed");
+  RC(dalloc(&c->page_table, static_cast<size_t>(r.max_slots) * r.max_pages_per_req));
+  CK(cudaMemset(c->page_table, 0, static_cast<size_t>(r.max_slots) * r.max_pages_per_req * 4));
+  // activations
+  const size_t R = r.max_rows;
+  RC(dalloc(&c->h, R * d));
+  RC(dalloc(&c->hr, R * d));
+  RC(make_act(c->xn, r.max_rows, m.d));
+  RC(make_act(c->xn2, r.max_rows, m.d));
+  RC(make_act(c->attn, r.max_rows, m.n_q * m.hd));
+  RC(make_act(c->act, r.max_rows, m.ffn));
+  RC(make_act(c->lin, r.max_rows, m.d));
+  RC(make_act(c->xr, r.max_rows, m.d));
+  RC(dalloc(&c->qbuf, R * m.n_q * m.hd));
+  const size_t widest = std::max<size_t>(std::max<size_t>(2 * m.ffn, m.vocab), m.qkv_n());
+  c->part_floats = std::max<size_t>(R * widest, static_cast<size_t>(16) * 64 * widest);
+  RC(dalloc(&c->part, c->part_floats));
+  RC(dalloc(&c->o_part, static_cast<size_t>(r.max_chunks) * m.n_q * m.hd));
+  RC(dalloc(&c->lse_part, static_cast<size_t>(r.max_chunks) * m.n_q));
+  RC(dalloc(&c->resid, static_cast<size_t>(r.max_slots) * d));
+  RC(dalloc(&c->last_token, r.max_slots));
+  CK(cudaMemset(c->last_token, 0, r.max_slots * 4));
+  RC(dalloc(&c->tok, R));
+  RC(dalloc(&c->tok_out, 2 * R));
+  RC(rope_init(c));
+  // metadata
+  c->meta_ints = layout_of(r).total + 16 * R * (m.layers + 2);
+  RC(dalloc(&c->dm, layout_of(r).total));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hm), 2 * c->meta_ints * sizeof(int),
+                   cudaHostAllocDefault));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->tokens_pinned), 2 * R * sizeof(int),
+                   cudaHostAllocDefault));
+  for (auto& e : c->stage_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // piggyback mailboxes: pinned host memory mapped into the device space
+  const size_t ship_elems = static_cast<size_t>(r.max_slots) * m.qkv_n();
+  const size_t res_elems = static_cast<size_t>(r.max_slots) * m.n_q * m.hd;
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->ship_h), ship_elems * 2, cudaHostAllocMapped));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->result_h), res_elems * 2, cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->ship_d), c->ship_h, 0));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->result_d), c->result_h, 0));
+  // host KV arena
+  c->regions.assign(r.max_slots, HostRegion{});
+  if (r.host_kv_bytes > 0) {
+    c->hkv_bytes = static_cast<size_t>(r.host_kv_bytes);
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hkv_h), c->hkv_bytes, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hkv_d), c->hkv_h, 0));
+    c->free_list.push_back({0, c->hkv_bytes});
+  }
+  c->pool = new ThreadPool(std::max(0, r.cpu_threads - 1));
+  CK(cudaStreamSynchronize(c->st));
+  return HS_OK;
+}
+
+int kv_swap_pages(hs_ctx* c, int slot, int tokens, bool to_host) {
+  if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
+  HostRegion& hr = c->regions[slot];
+  if (!hr.used) return set_error(HS_E_INTEGRITY, "slot %d has no host KV region", slot);
+  if (tokens > hr.cap) return set_error(HS_E_CAPACITY, "swap of %d tokens exceeds region", tokens);
+  const int* pages = c->page_table + static_cast<size_t>(slot) * c->r.max_pages_per_req;
+  bf16* host = reinterpret_cast<bf16*>(reinterpret_cast<uint8_t*>(c->hkv_d) + hr.offset);
+  RC(kv_swap(to_host, c->kv_pool, c->geom, pages, tokens, host, hr.cap, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hs_create(const hs_model_cfg* m, const hs_rt_cfg* r, hs_ctx** out) {
+  if (!m || !r || !out) return set_error(HS_E_CONFIG, "null argument");
+  hs_ctx* c = new (std::nothrow) hs_ctx();
+  if (!c) return set_error(HS_E_CAPACITY, "out of host memory");
+  const int rc = create(m, r, c);
+  if (rc != HS_OK) {
+    free_all(c);
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return HS_OK;
+}
+
+int hs_destroy(hs_ctx* c) {
+  if (!c) return HS_OK;
+  cudaStreamSynchronize(c->st);
+  free_all(c);
+  delete c;
+  return HS_OK;
+}
+
+void* hs_stream(hs_ctx* c) { return c ? c->st : nullptr; }
+
+int hs_set_weight(hs_ctx* c, int kind, int layer, const void* host, size_t bytes) {
+  const ModelCfg& m = c->m;
+  const size_t d = m.d;
+  void* dst = nullptr;
+  size_t want = 0;
+  const bool per_layer = kind >= HS_W_QKV;
+  if (per_layer && (layer < 0 || layer >= m.layers))
+    return set_error(HS_E_CONFIG, "layer %d out of range", layer);
+  switch (kind) {
+    case HS_W_EMBED: dst = c->w_embed; want = static_cast<size_t>(m.vocab) * d * 2; break;
+    case HS_W_LM_HEAD: dst = c->w_lm; want = static_cast<size_t>(m.vocab) * d * 2; break;
+    case HS_W_FINAL_NORM: dst = c->w_final; want = d * 4; break;
+    case HS_W_QKV: dst = c->w_qkv[layer]; want = static_cast<size_t>(m.qkv_n()) * d * 2; break;
+    case HS_W_O: dst = c->w_o[layer]; want = d * m.n_q * m.hd * 2; break;
+    case HS_W_GATE_UP: dst = c->w_gu[layer]; want = 2 * static_cast<size_t>(m.ffn) * d * 2; break;
+    case HS_W_DOWN: dst = c->w_down[layer]; want = d * m.ffn * 2; break;
+    case HS_W_NORM_IN: dst = c->n_in[layer]; want = d * 4; break;
+    case HS_W_NORM_POST: dst = c->n_post[layer]; want = d * 4; break;
+    default: return set_error(HS_E_CONFIG, "unknown weight kind %d", kind);
+  }
+  if (bytes != want) return set_error(HS_E_CONFIG, "weight %d: %zu bytes, want %zu", kind, bytes, want);
+  CK(cudaMemcpy(dst, host, bytes, cudaMemcpyHostToDevice));
+  return HS_OK;
+}
+
+int hs_init_weights(hs_ctx* c, uint64_t seed, float std) {
+  const ModelCfg& m = c->m;
+  const size_t d = m.d;
+  uint64_t s = seed * 0x100000001B3ull + 17;
+  auto init = [&](bf16* p, size_t n) {
+    init_normal_kernel<<<148 * 8, 256, 0, c->st>>>(p, n, s, std);
+    s = s * 6364136223846793005ull + 1442695040888963407ull;
+  };
+  auto ones = [&](float* p, size_t n) { fill_f32_kernel<<<64, 256, 0, c->st>>>(p, n, 1.0f); };
+  init(c->w_embed, static_cast<size_t>(m.vocab) * d);
+  init(c->w_lm, static_cast<size_t>(m.vocab) * d);
+  ones(c->w_final, d);
+  for (int l = 0; l < m.layers; ++l) {
+    init(c->w_qkv[l], static_cast<size_t>(m.qkv_n()) * d);
+    init(c->w_o[l], d * m.n_q * m.hd);
+    init(c->w_gu[l], 2 * static_cast<size_t>(m.ffn) * d);
+    init(c->w_down[l], d * m.ffn);
+    ones(c->n_in[l], d);
+    ones(c->n_post[l], d);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->st));
+  return HS_OK;
+}
+
+int hs_set_page_table(hs_ctx* c, int slot, const int* pages, int n) {
+  if (slot < 0 || slot >= c->r.max_slots || n < 0 || n > c->r.max_pages_per_req)
+    return set_error(HS_E_CONFIG, "page table row out of range (slot %d, %d pages)", slot, n);
+  for (int i = 0; i < n; ++i)
+    if (pages[i] < 0 || pages[i] >= c->r.kv_pages)
+      return set_error(HS_E_CONFIG, "page id %d out of range", pages[i]);
+  int* s = stage(c, n);
+  if (!s) return set_error(HS_E_CAPACITY, "metadata staging overflow");
+  std::memcpy(s, pages, n * sizeof(int));
+  CK(cudaMemcpyAsync(c->page_table + static_cast<size_t>(slot) * c->r.max_pages_per_req, s,
+                     n * sizeof(int), cudaMemcpyHostToDevice, c->st));
+  return HS_OK;
+}
+
+int hs_keep_logits(hs_ctx* c, int on) {
+  c->keep_logits = on != 0;
+  if (c->keep_logits && !c->logits)
+    RC(dalloc(&c->logits, static_cast<size_t>(2 * c->r.max_rows) * c->m.vocab));
+  return HS_OK;
+}
+
+int hs_read_logits(hs_ctx* c, float* host, int rows) {
+  if (!c->logits) return set_error(HS_E_CONFIG, "logits not kept (hs_keep_logits)");
+  if (rows > c->n_tok_out) return set_error(HS_E_CONFIG, "only %d logit rows", c->n_tok_out);
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpy(host, c->logits, static_cast<size_t>(rows) * c->m.vocab * 4,
+                cudaMemcpyDeviceToHost));
+  return HS_OK;
+}
+
+int hs_host_kv_reserve(hs_ctx* c, int slot, int cap_tokens) {
+  if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
+  HostRegion& hr = c->regions[slot];
+  if (hr.used) return set_error(HS_E_INTEGRITY, "slot %d already holds a host KV region", slot);
+  const size_t bytes = static_cast<size_t>(cap_tokens) * c->m.layers * 2 * c->m.n_kv * c->m.hd * 2;
+  for (size_t i = 0; i < c->free_list.size(); ++i) {
+    auto& f = c->free_list[i];
+    if (f.second >= bytes) {
+      hr.offset = f.first;
+      hr.cap = cap_tokens;
+      hr.used = true;
+      f.first += bytes;
+      f.second -= bytes;
+      if (f.second == 0) c->free_list.erase(c->free_list.begin() + i);
+      return HS_OK;
+    }
+  }
+  return set_error(HS_E_CAPACITY, "host KV arena exhausted (%zu bytes requested)", bytes);
+}
+
+int hs_host_kv_release(hs_ctx* c, int slot) {
+  if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
+  HostRegion& hr = c->regions[slot];
+  if (!hr.used) return HS_OK;
+  const size_t bytes = static_cast<size_t>(hr.cap) * c->m.layers * 2 * c->m.n_kv * c->m.hd * 2;
+  c->free_list.push_back({hr.offset, bytes});
+  std::sort(c->free_list.begin(), c->free_list.end());
+  std::vector<std::pair<size_t, size_t>> merged;
+  for (auto& f : c->free_list) {
+    if (!merged.empty() && merged.back().first + merged.back().second == f.first)
+      merged.back().second += f.second;
+    else
+      merged.push_back(f);
+  }
+  c->free_list.swap(merged);
+  hr = HostRegion{};
+  return HS_OK;
+}
+
+int hs_host_kv_ptr(hs_ctx* c, int slot, void** host_ptr, int* cap) {
+  if (slot < 0 || slot >= c->r.max_slots || !c->regions[slot].used)
+    return set_error(HS_E_CONFIG, "slot %d has no host KV region", slot);
+  *host_ptr = reinterpret_cast<uint8_t*>(c->hkv_h) + c->regions[slot].offset;
+  *cap = c->regions[slot].cap;
+  return HS_OK;
+}
+
+int hs_swap_out(hs_ctx* c, int slot, int tokens) { return kv_swap_pages(c, slot, tokens, true); }
+int hs_swap_in(hs_ctx* c, int slot, int tokens) { return kv_swap_pages(c, slot, tokens, false); }
+
+int hs_iter_begin(hs_ctx* c, const hs_iter_desc* d) {
+  const hs_rt_cfg& r = c->r;
+  if (d->n_rows < 0 || d->n_rows > r.max_rows || d->n_decode > d->n_rows ||
+      d->n_chunks > r.max_chunks || d->n_logit_rows > d->n_rows || d->n_tiles > r.max_rows)
+    return set_error(HS_E_CAPACITY, "iteration exceeds capacities (rows %d, chunks %d)", d->n_rows,
+                     d->n_chunks);
+  // switch pinned staging halves: everything staged into the current half is
+  // enqueued before this event; the new half may be rewritten once the
+  // copies staged into it last time have executed
+  CK(cudaEventRecord(c->stage_ev[c->stage_half], c->st));
+  c->stage_half ^= 1;
+  CK(cudaEventSynchronize(c->stage_ev[c->stage_half]));
+  c->stage_pos = 0;
+  const MetaLayout L = layout_of(r);
+  c->B = d->n_rows;
+  c->D = d->n_decode;
+  c->n_chunks = d->n_chunks;
+  c->n_tiles = d->n_tiles;
+  c->n_logit = d->n_logit_rows;
+  c->n_tok_out = 0;
+  c->merges_L = 0;
+  RC(upload(c, L.row_slot, d->row_slot, d->n_rows));
+  RC(upload(c, L.row_pos, d->row_pos, d->n_rows));
+  RC(upload(c, L.row_token, d->row_token, d->n_rows));
+  RC(upload_fill(c, L.row_mode, 0, d->n_rows));
+  RC(upload(c, L.chunks, d->chunks, static_cast<size_t>(d->n_chunks) * 5));
+  RC(upload(c, L.row_chunk_begin, d->row_chunk_begin, d->n_chunks ? d->n_decode + 1 : 0));
+  RC(upload(c, L.tiles, d->tiles, static_cast<size_t>(d->n_tiles) * 4));
+  RC(upload(c, L.logit_rows, d->logit_rows, d->n_logit_rows));
+  std::vector<int> lslot(d->n_logit_rows);
+  for (int i = 0; i < d->n_logit_rows; ++i) lslot[i] = d->row_slot[d->logit_rows[i]];
+  RC(upload(c, L.logit_slot, lslot.data(), lslot.size()));
+  return HS_OK;
+}
+
+int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
+  const ModelCfg& m = c->m;
+  const hs_rt_cfg& r = c->r;
+  const MetaLayout L = layout_of(r);
+  const int l = d->layer - 1;  // 0-based
+  const int B = c->B, C = d->n_carry, M = d->n_merge;
+  const bool last = d->layer == m.layers;
+  if (l < 0 || l >= m.layers) return set_error(HS_E_CONFIG, "layer %d out of range", d->layer);
+  if (B + C > r.max_rows || B + M > r.max_rows || d->n_restart > M)
+    return set_error(HS_E_CAPACITY, "layer rows exceed max_rows");
+  int* dm = c->dm;
+  cudaStream_t st = c->st;
+  const int d_ = m.d, nqh = m.n_q * m.hd;
+  int sp = 1;
+  // carry rows: ship meta at [B, B+C)
+  RC(upload(c, L.row_slot + B, d->carry_slot, C));
+  RC(upload(c, L.row_pos + B, d->carry_pos, C));
+  RC(upload_fill(c, L.row_token + B, -1, C));
+  RC(upload_fill(c, L.row_mode + B, 1, C));
+  if (l == 0) {
+    // embed batch rows (+ injected chains: fresh token from last_token)
+    RC(select_tokens(dm + L.row_token, dm + L.row_slot, c->last_token, B + C, c->tok, st));
+    RC(embed_gather(c->tok, B + C, c->w_embed, d_, c->h, st));
+    // residual put for injections (reference _chain_qkv(req, 1), engine.py:997)
+    RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, dm + L.row_slot + B, C, d_, c->resid,
+                        st));
+    RC(rmsnorm_rows(c->h, B + C, d_, c->n_in[0], m.eps, c->xn.p, d_, st));
+  }
+  // QKV over batch + carry rows, RoPE, KV scatter / piggyback ship
+  RC(gemm(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, &sp));
+  RC(qkv_rope_scatter(c->part, sp, B + C, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
+                      dm + L.row_pos, dm + L.row_slot, dm + L.row_mode, c->qbuf, nqh, c->kv_pool,
+                      c->geom, l, c->page_table, r.max_pages_per_req, c->ship_d, m.qkv_n(), st));
+  // attention of batch rows
+  RC(decode_attention(c->m_kv, c->geom, l, c->qbuf, nqh, m.n_q, c->page_table,
+                      r.max_pages_per_req, reinterpret_cast<const DecodeChunk*>(dm + L.chunks),
+                      c->n_chunks, c->o_part, c->lse_part, st));
+  RC(decode_combine(c->o_part, c->lse_part, dm + L.row_chunk_begin, c->n_chunks ? c->D : 0, m.n_q,
+                    m.n_kv, m.hd, c->attn.p, nqh, nullptr, st));
+  RC(prefill_attention(c->m_kv, c->geom, l, c->qbuf, nqh, m.n_q, c->page_table,
+                       r.max_pages_per_req, reinterpret_cast<const PrefillTile*>(dm + L.tiles),
+                       c->n_tiles, c->attn.p, nqh, st));
+  // merged rows: host attention result + stored residual
+  RC(upload(c, L.merge_slot, d->merge_slot, M));
+  RC(gather_rows_bf16(c->result_d, nqh, dm + L.merge_slot, M, nqh,
+                      c->attn.p + static_cast<size_t>(B) * nqh, nqh, st));
+  RC(gather_rows_f32(c->resid, dm + L.merge_slot, M, d_, c->h + static_cast<size_t>(B) * d_, st));
+  const int N = B + M;
+  // Proj + ResidualAdd
+  RC(gemm(c, c->m_o[l], c->attn, N, d_, nqh, &sp));
+  RC(residual_add_norm(c->part, sp, N, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, st));
+  // MLP + ResidualAdd (+ next layer's input norm, or the final norm)
+  RC(gemm(c, c->m_gu[l], c->xn2, N, 2 * m.ffn, d_, &sp));
+  RC(silu_mul(c->part, sp, N, m.ffn, c->act.p, m.ffn, st));
+  RC(gemm(c, c->m_down[l], c->act, N, d_, m.ffn, &sp));
+  RC(residual_add_norm(c->part, sp, N, d_, c->h, last ? c->w_final : c->n_in[l + 1], m.eps,
+                       c->xn.p, d_, st));
+  if (!last) {
+    // residual put for the chains' next layer (engine.py:985)
+    RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, dm + L.merge_slot, M, d_, c->resid,
+                        st));
+    return HS_OK;
+  }
+  // ---- final layer: LM head + greedy token for decode / finishing-prefill
+  // rows and for every chain completing a token (engine.py:1005-1013, 1024-1047)
+  const int NL = c->n_logit + M;
+  RC(gather_rows_bf16(c->xn.p, d_, dm + L.logit_rows, c->n_logit, d_, c->lin.p, d_, st));
+  CK(cudaMemcpyAsync(c->lin.p + static_cast<size_t>(c->n_logit) * d_,
+                     c->xn.p + static_cast<size_t>(B) * d_, static_cast<size_t>(M) * d_ * 2,
+                     cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(dm + L.logit_slot + c->n_logit, dm + L.merge_slot, M * sizeof(int),
+                     cudaMemcpyDeviceToDevice, st));
+  RC(gemm(c, c->m_lm, c->lin, NL, m.vocab, d_, &sp));
+  RC(argmax_rows(c->part, sp, NL, m.vocab, c->tok_out, c->keep_logits ? c->logits : nullptr, st));
+  RC(scatter_tokens(c->tok_out, dm + L.logit_slot, NL, c->last_token, st));
+  c->n_tok_out = NL;
+  c->merges_L = M;
+  // chains continuing with the next token: embed, residual put, QKV(1), ship
+  const int R = d->n_restart;
+  if (R > 0) {
+    std::vector<int> rslot(R);
+    for (int i = 0; i < R; ++i) rslot[i] = d->merge_slot[d->restart_idx[i]];
+    RC(upload(c, L.restart_slot, rslot.data(), R));
+    RC(upload(c, L.restart_pos, d->restart_pos, R));
+    RC(upload_fill(c, L.restart_token, -1, R));
+    RC(upload_fill(c, L.restart_mode, 1, R));
+    RC(select_tokens(dm + L.restart_token, dm + L.restart_slot, c->last_token, R, c->tok, st));
+    RC(embed_gather(c->tok, R, c->w_embed, d_, c->hr, st));
+    RC(scatter_rows_f32(c->hr, dm + L.restart_slot, R, d_, c->resid, st));
+    RC(rmsnorm_rows(c->hr, R, d_, c->n_in[0], m.eps, c->xr.p, d_, st));
+    RC(gemm(c, c->m_qkv[0], c->xr, R, m.qkv_n(), d_, &sp));
+    RC(qkv_rope_scatter(c->part, sp, R, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
+                        dm + L.restart_pos, dm + L.restart_slot, dm + L.restart_mode, c->qbuf, nqh,
+                        c->kv_pool, c->geom, 0, c->page_table, r.max_pages_per_req, c->ship_d,
+                        m.qkv_n(), st));
+  }
+  return HS_OK;
+}
+
+int hs_iter_end(hs_ctx* c, int* tokens_out, int n) {
+  if (n < c->n_tok_out) return set_error(HS_E_CONFIG, "token buffer too small (%d < %d)", n,
+                                         c->n_tok_out);
+  if (c->n_tok_out > 0)
+    CK(cudaMemcpyAsync(c->tokens_pinned, c->tok_out, c->n_tok_out * sizeof(int),
+                       cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->n_tok_out > 0) std::memcpy(tokens_out, c->tokens_pinned, c->n_tok_out * sizeof(int));
+  return c->n_tok_out;
+}
+
+int hs_cpu_attend(hs_ctx* c, const int* slots, const int* layers, const int* ctxs, int n) {
+  CK(cudaStreamSynchronize(c->st));  // the shipped q/k/v rows have landed
+  const ModelCfg& m = c->m;
+  for (int i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= c->r.max_slots || !c->regions[slots[i]].used)
+      return set_error(HS_E_INTEGRITY, "work item for slot %d without host KV", slots[i]);
+    if (ctxs[i] >= c->regions[slots[i]].cap)
+      return set_error(HS_E_CAPACITY, "host KV of slot %d full (ctx %d)", slots[i], ctxs[i]);
+    if (layers[i] < 1 || layers[i] > m.layers)
+      return set_error(HS_E_CONFIG, "work item layer %d out of range", layers[i]);
+  }
+  c->pool->parallel_for(n * m.n_kv, [&](int task) {
+    const int i = task / m.n_kv, h = task % m.n_kv;
+    const int s = slots[i];
+    const HostRegion& hr = c->regions[s];
+    bf16* hkv = reinterpret_cast<bf16*>(reinterpret_cast<uint8_t*>(c->hkv_h) + hr.offset);
+    cpu_attend_head(m, c->ship_h + static_cast<size_t>(s) * m.qkv_n(), hkv, hr.cap,
+                    layers[i] - 1, ctxs[i], h, c->result_h + static_cast<size_t>(s) * m.n_q * m.hd,
+                    nullptr);
+  });
+  return HS_OK;
+}
+
+int hs_sync(hs_ctx* c) {
+  CK(cudaStreamSynchronize(c->st));
+  return HS_OK;
+}
+
+int hs_read_ship(hs_ctx* c, int slot, void* host, size_t bytes) {
+  CK(cudaStreamSynchronize(c->st));
+  if (bytes != static_cast<size_t>(c->m.qkv_n()) * 2) return set_error(HS_E_CONFIG, "size");
+  std::memcpy(host, c->ship_h + static_cast<size_t>(slot) * c->m.qkv_n(), bytes);
+  return HS_OK;
+}
+
+int hs_read_residual(hs_ctx* c, int slot, float* host) {
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpy(host, c->resid + static_cast<size_t>(slot) * c->m.d, c->m.d * 4,
+                cudaMemcpyDeviceToHost));
+  return HS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,472 @@
+"""Host runtime of the B200 step: the libhs context wrapper and `CudaStep`,
+the LayerStep that executes the engine's schedule on the GPU.
+
+`CudaStep` turns the engine's events into libhs calls:
+
+  Engine._start_iteration  -> begin_iteration: rows of the BatchPlan (decodes
+                              first, then chunk tokens), split-K decode work
+                              items, prefill tiles, logit rows   (hs_iter_begin)
+  Engine._run_layer        -> layer: carry / merge / restart rows  (hs_layer)
+  Engine._on_layer_done(L) -> end_iteration: greedy tokens back   (hs_iter_end)
+  Engine._maybe_start_host -> cpu_service: host attention of the work items
+                              (hs_cpu_attend)
+  swap-out / resume / preempt / complete -> page + host-KV management
+
+References: engine.py:879-1047 (iteration), 402-508 (swaps), 512-560 (CPU
+service) of pkg/src/hybridserve.  There is no CPU fallback: without libhs
+and an sm_100 device the constructor raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import zlib
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .engine import (
+    MERGE_CHAIN,
+    MERGE_INJECT,
+    MERGE_TOKEN_END,
+    MERGE_TOKEN_NEXT,
+    LayerStep,
+)
+from .errors import ScenarioError
+from .models import TransformerConfig
+
+PAGE = _lib.PAGE_TOKENS
+_IP = C.POINTER(C.c_int)
+
+
+class HsModelCfg(C.Structure):
+    _fields_ = [("d_model", C.c_int), ("n_layers", C.c_int), ("n_q", C.c_int),
+                ("n_kv", C.c_int), ("head_dim", C.c_int), ("ffn", C.c_int), ("vocab", C.c_int),
+                ("rope_theta", C.c_float), ("norm_eps", C.c_float)]
+
+
+class HsRtCfg(C.Structure):
+    _fields_ = [("max_rows", C.c_int), ("max_slots", C.c_int), ("kv_pages", C.c_int),
+                ("max_pages_per_req", C.c_int), ("max_pos", C.c_int), ("max_chunks", C.c_int),
+                ("cpu_threads", C.c_int), ("host_kv_bytes", C.c_int64), ("device", C.c_int)]
+
+
+class HsIterDesc(C.Structure):
+    _fields_ = [("n_rows", C.c_int), ("n_decode", C.c_int), ("row_slot", _IP),
+                ("row_pos", _IP), ("row_token", _IP), ("n_chunks", C.c_int), ("chunks", _IP),
+                ("row_chunk_begin", _IP), ("n_tiles", C.c_int), ("tiles", _IP),
+                ("n_logit_rows", C.c_int), ("logit_rows", _IP)]
+
+
+class HsLayerDesc(C.Structure):
+    _fields_ = [("layer", C.c_int), ("n_carry", C.c_int), ("carry_slot", _IP),
+                ("carry_pos", _IP), ("n_merge", C.c_int), ("merge_slot", _IP),
+                ("n_restart", C.c_int), ("restart_idx", _IP), ("restart_pos", _IP)]
+
+
+W_EMBED, W_LM_HEAD, W_FINAL_NORM, W_QKV, W_O, W_GATE_UP, W_DOWN, W_NORM_IN, W_NORM_POST = range(9)
+
+_CTX_SIGS = {
+    "hs_create": [C.POINTER(HsModelCfg), C.POINTER(HsRtCfg), C.POINTER(C.c_void_p)],
+    "hs_destroy": [C.c_void_p],
+    "hs_set_weight": [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t],
+    "hs_init_weights": [C.c_void_p, C.c_uint64, C.c_float],
+    "hs_set_page_table": [C.c_void_p, C.c_int, _IP, C.c_int],
+    "hs_host_kv_reserve": [C.c_void_p, C.c_int, C.c_int],
+    "hs_host_kv_release": [C.c_void_p, C.c_int],
+    "hs_host_kv_ptr": [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), _IP],
+    "hs_swap_out": [C.c_void_p, C.c_int, C.c_int],
+    "hs_swap_in": [C.c_void_p, C.c_int, C.c_int],
+    "hs_iter_begin": [C.c_void_p, C.POINTER(HsIterDesc)],
+    "hs_layer": [C.c_void_p, C.POINTER(HsLayerDesc)],
+    "hs_iter_end": [C.c_void_p, _IP, C.c_int],
+    "hs_cpu_attend": [C.c_void_p, _IP, _IP, _IP, C.c_int],
+    "hs_sync": [C.c_void_p],
+    "hs_keep_logits": [C.c_void_p, C.c_int],
+    "hs_read_logits": [C.c_void_p, C.c_void_p, C.c_int],
+    "hs_read_ship": [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t],
+    "hs_read_residual": [C.c_void_p, C.c_int, C.c_void_p],
+}
+_lib._SIGNATURES.update(_CTX_SIGS)
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(_IP)
+
+
+def _i32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int32))
+
+
+@dataclass
+class RuntimeConfig:
+    max_rows: int = 1024
+    max_slots: int = 256
+    kv_pages: int = 1024
+    max_pages_per_req: int = 256
+    max_pos: int = 16384
+    max_chunks: int = 4096
+    cpu_threads: int = 8
+    host_kv_bytes: int = 1 << 30
+    device: int = 0
+
+
+class HsContext:
+    """Owns one libhs context (one GPU replica)."""
+
+    def __init__(self, model: TransformerConfig, rt: RuntimeConfig):
+        lib = _lib.load()
+        for name, argtypes in _CTX_SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = C.c_int
+        lib.hs_stream.argtypes = [C.c_void_p]
+        lib.hs_stream.restype = C.c_void_p
+        _lib.require_device()
+        self.lib = lib
+        self.model = model
+        self.rt = rt
+        mc = HsModelCfg(model.d_model, model.n_layers, model.n_q, model.n_kv, model.head_dim,
+                        model.ffn, model.vocab, model.rope_theta, model.norm_eps)
+        rc = HsRtCfg(rt.max_rows, rt.max_slots, rt.kv_pages, rt.max_pages_per_req, rt.max_pos,
+                     rt.max_chunks, rt.cpu_threads, rt.host_kv_bytes, rt.device)
+        h = C.c_void_p()
+        _lib.check(lib.hs_create(C.byref(mc), C.byref(rc), C.byref(h)), "hs_create")
+        self.h = h
+        self._tok = np.zeros(2 * rt.max_rows, np.int32)
+
+    def close(self) -> None:
+        if self.h:
+            self.lib.hs_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _call(self, name: str, *args) -> int:
+        rc = getattr(self.lib, name)(self.h, *args)
+        if rc < 0 or (rc > 0 and name != "hs_iter_end"):
+            _lib.check(rc, name)
+        return rc
+
+    @property
+    def stream(self) -> int:
+        return self.lib.hs_stream(self.h)
+
+    # weights
+    def set_weight(self, kind: int, layer: int, arr: np.ndarray) -> None:
+        a = np.ascontiguousarray(arr)
+        self._call("hs_set_weight", kind, layer, a.ctypes.data_as(C.c_void_p), a.nbytes)
+
+    def init_weights(self, seed: int, std: float = 0.02) -> None:
+        self._call("hs_init_weights", seed, std)
+
+    def load_weights(self, w: dict) -> None:
+        """w: numpy weights (bf16 bit patterns as uint16 for matrices, fp32
+        norms) in the layout of oracle/weights (embed, lm_head, final_norm,
+        and per-layer lists)."""
+        self.set_weight(W_EMBED, 0, w["embed"])
+        self.set_weight(W_LM_HEAD, 0, w["lm_head"])
+        self.set_weight(W_FINAL_NORM, 0, w["final_norm"])
+        for l in range(self.model.n_layers):
+            self.set_weight(W_QKV, l, w["qkv"][l])
+            self.set_weight(W_O, l, w["o"][l])
+            self.set_weight(W_GATE_UP, l, w["gate_up"][l])
+            self.set_weight(W_DOWN, l, w["down"][l])
+            self.set_weight(W_NORM_IN, l, w["norm_in"][l])
+            self.set_weight(W_NORM_POST, l, w["norm_post"][l])
+
+    def set_page_table(self, slot: int, pages) -> None:
+        p = _i32(pages)
+        self._call("hs_set_page_table", slot, _ip(p), len(p))
+
+    def host_kv_reserve(self, slot: int, cap: int) -> None:
+        self._call("hs_host_kv_reserve", slot, cap)
+
+    def host_kv_release(self, slot: int) -> None:
+        self._call("hs_host_kv_release", slot)
+
+    def swap_out(self, slot: int, tokens: int) -> None:
+        self._call("hs_swap_out", slot, tokens)
+
+    def swap_in(self, slot: int, tokens: int) -> None:
+        self._call("hs_swap_in", slot, tokens)
+
+    def iter_begin(self, rows_slot, rows_pos, rows_tok, n_decode, chunks, chunk_begin, tiles,
+                   logit_rows) -> None:
+        self._keep = [_i32(rows_slot), _i32(rows_pos), _i32(rows_tok),
+                      _i32(chunks).reshape(-1), _i32(chunk_begin), _i32(tiles).reshape(-1),
+                      _i32(logit_rows)]
+        s, p, t, ch, cb, ti, lr = self._keep
+        d = HsIterDesc(len(s), n_decode, _ip(s), _ip(p), _ip(t), len(ch) // 5, _ip(ch), _ip(cb),
+                       len(ti) // 4, _ip(ti), len(lr), _ip(lr))
+        self._call("hs_iter_begin", C.byref(d))
+
+    def layer(self, layer: int, carry_slot, carry_pos, merge_slot, restart_idx, restart_pos):
+        cs, cp, ms, ri, rp = (_i32(carry_slot), _i32(carry_pos), _i32(merge_slot),
+                              _i32(restart_idx), _i32(restart_pos))
+        d = HsLayerDesc(layer, len(cs), _ip(cs), _ip(cp), len(ms), _ip(ms), len(ri), _ip(ri),
+                        _ip(rp))
+        self._call("hs_layer", C.byref(d))
+
+    def iter_end(self) -> np.ndarray:
+        n = self.lib.hs_iter_end(self.h, _ip(self._tok), len(self._tok))
+        if n < 0:
+            _lib.check(-n if n < 0 else n, "hs_iter_end")
+        return self._tok[:n].copy()
+
+    def cpu_attend(self, slots, layers, ctxs) -> None:
+        s, l, c = _i32(slots), _i32(layers), _i32(ctxs)
+        self._call("hs_cpu_attend", _ip(s), _ip(l), _ip(c), len(s))
+
+    def sync(self) -> None:
+        self._call("hs_sync")
+
+    def keep_logits(self, on: bool = True) -> None:
+        self._call("hs_keep_logits", int(on))
+
+    def read_logits(self, rows: int) -> np.ndarray:
+        out = np.zeros((rows, self.model.vocab), np.float32)
+        self._call("hs_read_logits", out.ctypes.data_as(C.c_void_p), rows)
+        return out
+
+
+def prompt_tokens(req_id: str, length: int, vocab: int, seed: int = 0) -> np.ndarray:
+    """Synthetic prompt ids: uniform in [0, vocab) from a per-request seed."""
+    rng = np.random.default_rng((zlib.crc32(req_id.encode()) << 8) ^ seed)
+    return rng.integers(0, vocab, size=length, dtype=np.int64).astype(np.int32)
+
+
+def decode_chunks(ctxs: list[int], n_kv: int, target_ctas: int = 296, max_pages: int = 64):
+    """Split-K work list: each decode row's KV pages cut into chunks so that
+    chunks x KV heads ~ 2 CTAs per SM (148 SMs)."""
+    pages = [(c + PAGE - 1) // PAGE for c in ctxs]
+    total = sum(pages)
+    per = max(1, min(max_pages, -(-total * n_kv // target_ctas))) if total else 1
+    chunks, begin = [], [0]
+    for r, (c, n) in enumerate(zip(ctxs, pages)):
+        for p0 in range(0, n, per):
+            chunks.append((r, -1, p0, min(n, p0 + per), c))
+        begin.append(len(chunks))
+    return chunks, begin
+
+
+class PagePool:
+    """Free list of 64-token KV pages; per-slot page lists."""
+
+    def __init__(self, n_pages: int):
+        self.free = list(range(n_pages - 1, -1, -1))
+        self.owned: dict[int, list[int]] = {}
+
+    def ensure(self, slot: int, tokens: int) -> bool:
+        """Grow the slot's pages to hold `tokens`; True if the list changed."""
+        have = self.owned.setdefault(slot, [])
+        need = (tokens + PAGE - 1) // PAGE
+        if need <= len(have):
+            return False
+        if need - len(have) > len(self.free):
+            raise ScenarioError(f"KV page pool exhausted (slot {slot} needs {need} pages)")
+        while len(have) < need:
+            have.append(self.free.pop())
+        return True
+
+    def release(self, slot: int) -> None:
+        for p in reversed(self.owned.pop(slot, [])):
+            self.free.append(p)
+
+
+class CudaStep(LayerStep):
+    """Executes the engine's schedule on the B200 through libhs."""
+
+    def __init__(self, model: TransformerConfig, rt: Optional[RuntimeConfig] = None,
+                 weights: Optional[dict] = None, weight_seed: int = 0, prompt_seed: int = 0,
+                 keep_logits: bool = False):
+        self.model = model
+        self.rt = rt or RuntimeConfig()
+        self.ctx = HsContext(model, self.rt)
+        if weights is not None:
+            self.ctx.load_weights(weights)
+        else:
+            self.ctx.init_weights(weight_seed)
+        self.keep = keep_logits
+        if keep_logits:
+            self.ctx.keep_logits(True)
+        self.prompt_seed = prompt_seed
+        self.pages = PagePool(self.rt.kv_pages)
+        self.slots: dict[str, int] = {}
+        self.free_slots = list(range(self.rt.max_slots - 1, -1, -1))
+        self.generated: dict[str, list[int]] = {}
+        self.prompts: dict[str, np.ndarray] = {}
+        self._dirty: set[int] = set()
+        self._carry: list[tuple[int, int]] = []
+        self._logit_reqs: list[str] = []
+        self._merge_L: list[str] = []
+        self.last_logits: Optional[np.ndarray] = None
+        self.last_token_reqs: list[str] = []
+        self.last_tokens: Optional[np.ndarray] = None
+        self.iterations = 0
+        self._pending_release: list[str] = []
+
+    # -- bookkeeping --------------------------------------------------------
+
+    def attach(self, engine) -> None:
+        self.engine = engine
+        if engine.layers != self.model.n_layers:
+            raise ScenarioError(
+                f"scenario has {engine.layers} layers but transformer {self.model.name} has "
+                f"{self.model.n_layers}")
+
+    def slot_of(self, rid: str) -> int:
+        s = self.slots.get(rid)
+        if s is None:
+            if not self.free_slots:
+                raise ScenarioError("out of request slots (raise RuntimeConfig.max_slots)")
+            s = self.slots[rid] = self.free_slots.pop()
+        return s
+
+    def tokens_of(self, req) -> np.ndarray:
+        """Prompt ids followed by generated ids (for recompute rebuilds)."""
+        p = self.prompts.get(req.id)
+        if p is None:
+            p = self.prompts[req.id] = prompt_tokens(req.id, req.prompt_len, self.model.vocab,
+                                                     self.prompt_seed)
+        gen = self.generated.get(req.id, [])
+        return np.concatenate([p, np.asarray(gen, np.int32)]) if gen else p
+
+    def _ensure(self, slot: int, tokens: int) -> None:
+        if self.pages.ensure(slot, tokens):
+            self._dirty.add(slot)
+
+    def _flush_pages(self) -> None:
+        for s in sorted(self._dirty):
+            self.ctx.set_page_table(s, self.pages.owned.get(s, []))
+        self._dirty.clear()
+
+    # -- LayerStep ---------------------------------------------------------------
+
+    def begin_iteration(self, plan) -> None:
+        eng = self.engine
+        self._release_pending()
+        slots, pos, toks = [], [], []
+        dec_ctx = []
+        logit_rows = []
+        self._logit_reqs = []
+        for rid in plan.ls_decode + plan.be_decode_gpu:
+            r = eng.requests[rid]
+            s = self.slot_of(rid)
+            self._ensure(s, r.ctx + 1)
+            logit_rows.append(len(slots))
+            self._logit_reqs.append(rid)
+            slots.append(s)
+            pos.append(r.ctx)
+            toks.append(-1)
+            dec_ctx.append(r.ctx + 1)
+        n_dec = len(slots)
+        tiles = []
+        for rid, q in plan.ls_prefill_chunks + plan.be_prefill_chunks:
+            r = eng.requests[rid]
+            s = self.slot_of(rid)
+            done = r.prefill_done
+            self._ensure(s, done + q)
+            seq = self.tokens_of(r)
+            row0 = len(slots)
+            for j in range(0, q, 64):
+                tiles.append((s, row0 + j, done + j, min(64, q - j)))
+            slots += [s] * q
+            pos += list(range(done, done + q))
+            toks += seq[done:done + q].tolist()
+            if done + q >= r.prefill_target and r.rebuild_tokens == 0:
+                logit_rows.append(len(slots) - 1)
+                self._logit_reqs.append(rid)
+        chunks, begin = decode_chunks(dec_ctx, self.model.n_kv)
+        chunks = [(row, slots[row], p0, p1, c) for row, _, p0, p1, c in chunks]
+        self._flush_pages()
+        self.ctx.iter_begin(slots, pos, toks, n_dec, chunks, begin, tiles, logit_rows)
+        self._carry = []
+        self._merge_L = []
+
+    def layer(self, layer: int, merges) -> None:
+        eng = self.engine
+        carry = list(self._carry)
+        merge_slots, merge_ids, restart_idx, restart_pos, next_carry = [], [], [], [], []
+        for item, outcome in merges:
+            r = eng.requests[item.req_id]
+            s = self.slot_of(item.req_id)
+            if outcome == MERGE_INJECT:
+                carry.append((s, r.ctx))
+                continue
+            if outcome == MERGE_CHAIN:
+                next_carry.append((s, r.ctx))
+            elif outcome == MERGE_TOKEN_NEXT:
+                restart_idx.append(len(merge_slots))
+                restart_pos.append(r.ctx)
+            merge_slots.append(s)
+            merge_ids.append(item.req_id)
+        self.ctx.layer(layer, [c[0] for c in carry], [c[1] for c in carry], merge_slots,
+                       restart_idx, restart_pos)
+        self._carry = next_carry
+        if layer == self.model.n_layers:
+            self._merge_L = merge_ids
+
+    def end_iteration(self, plan) -> None:
+        toks = self.ctx.iter_end()
+        reqs = self._logit_reqs + self._merge_L
+        if len(toks) != len(reqs):
+            raise RuntimeError(f"libhs returned {len(toks)} tokens for {len(reqs)} rows")
+        for rid, t in zip(reqs, toks):
+            self.generated.setdefault(rid, []).append(int(t))
+        self.last_token_reqs = reqs
+        self.last_tokens = toks
+        if self.keep and len(reqs):
+            self.last_logits = self.ctx.read_logits(len(reqs))
+        self.iterations += 1
+
+    def cpu_service(self, host_id: int, items) -> None:
+        eng = self.engine
+        self.ctx.cpu_attend([self.slot_of(it.req_id) for it in items], [it.layer for it in items],
+                            [it.ctx_tokens for it in items])
+
+    def swap_out_done(self, req) -> None:
+        s = self.slot_of(req.id)
+        self.ctx.host_kv_reserve(s, req.prompt_len + req.output_len + 1)
+        self.ctx.swap_out(s, req.kv_held)
+        self.pages.release(s)
+        self._dirty.add(s)
+
+    def resumed_on_gpu(self, req) -> None:
+        s = self.slot_of(req.id)
+        self._ensure(s, req.ctx)
+        self._flush_pages()
+        self.ctx.swap_in(s, req.ctx)
+        self.ctx.host_kv_release(s)
+
+    def preempted(self, req) -> None:
+        s = self.slot_of(req.id)
+        self.pages.release(s)
+        self._dirty.add(s)
+
+    def released(self, req) -> None:
+        # a chain can complete inside _run_layer(L) before this layer's rows
+        # (which still read the slot's residual) are launched: free the slot
+        # once the iteration is over
+        self._pending_release.append(req.id)
+
+    def _release_pending(self) -> None:
+        for rid in self._pending_release:
+            s = self.slots.pop(rid, None)
+            if s is None:
+                continue
+            self.pages.release(s)
+            self.ctx.host_kv_release(s)
+            self._dirty.discard(s)
+            self.free_slots.append(s)
+        self._pending_release.clear()
+
+    def finish(self) -> None:
+        self.ctx.sync()
+        self._release_pending()
