@@ -49,6 +49,8 @@ const char* hs_version(void);
 int hs_last_error(char* buf, int cap);
 /* 1 if a CUDA device of compute capability 10.x is visible. */
 int hs_device_ok(void);
+/* number of kernels libhs has launched in this process */
+unsigned long long hs_launch_count(void);
 
 /* -------------------------------------------------------------- op level
  * Single-kernel entry points over caller-owned device buffers.  They are the
@@ -208,6 +210,42 @@ int hs_iter_end(hs_ctx* ctx, int* tokens_out, int n);
  * result row into the slot's result mailbox (engine.py:529-560). */
 int hs_cpu_attend(hs_ctx* ctx, const int* slots, const int* layers, const int* ctxs, int n);
 int hs_sync(hs_ctx* ctx);
+
+/* ------------------------------------------------------------ live mode
+ * Asynchronous counterparts used by the wall-clock engine: the GPU never
+ * waits on the host.  Work items shipped by the last hs_layer() call are
+ * submitted behind a CUDA event; worker threads (pinned to this replica's
+ * cores) service them and append completions to a FIFO (the reference's
+ * output queue, engine.py:181-191,556-560).  Swaps run on a low-priority
+ * copy stream (pack + one 2D DMA); hs_swap_done polls a ticket. */
+int hs_cpu_submit(hs_ctx* ctx, const int* slots, const int* layers, const int* ctxs, int n);
+int hs_cpu_poll(hs_ctx* ctx, int* slots, int* layers, double* t_done, int max);
+int hs_cpu_in_flight(hs_ctx* ctx);
+double hs_cpu_busy_seconds(hs_ctx* ctx);
+double hs_wall_seconds(void);
+int hs_swap_out_async(hs_ctx* ctx, int slot, int tokens, int* ticket);
+int hs_swap_in_async(hs_ctx* ctx, int slot, int tokens, int* ticket);
+/* 1 = done, 0 = in flight */
+int hs_swap_done(hs_ctx* ctx, int ticket);
+/* stream marks for launch pacing, and timing events (CUDA events on the
+ * compute stream; elapsed in ms between two timer ids) */
+int hs_mark(hs_ctx* ctx);
+int hs_wait_mark(hs_ctx* ctx, int id);
+int hs_timer(hs_ctx* ctx);
+int hs_timer_elapsed(hs_ctx* ctx, int a, int b, float* ms);
+/* Per-kernel-class device time and algorithmic work of the launches made
+ * while profiling is on (CUDA events around each launch).  classes:
+ * 0 = Dense GEMMs, 1 = decode attention (K1+K2), 2 = prefill attention.
+ * stats[c] = {launches, milliseconds, bytes, flops}. */
+int hs_profile(hs_ctx* ctx, int on);
+int hs_profile_read(hs_ctx* ctx, double* stats /* [3][4] */, int reset);
+/* Profiler probes on the context's own buffers and layer-0 weights (device
+ * microseconds, median of reps): Dense modules over n rows; decode attention
+ * of g requests with ctx keys each; causal prefill of q new tokens after
+ * `done` tokens of context (the seam of build_dense_table, latency.py:200). */
+int hs_probe_dense(hs_ctx* ctx, int n, int reps, float* us);
+int hs_probe_decode(hs_ctx* ctx, int g, int ctx_len, int reps, float* us);
+int hs_probe_prefill(hs_ctx* ctx, int q, int done, int reps, float* us);
 
 /* test taps */
 int hs_keep_logits(hs_ctx* ctx, int on);

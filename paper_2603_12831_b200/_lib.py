@@ -74,8 +74,16 @@ def load() -> C.CDLL:
     return lib
 
 
+# entry points bound with non-int return types or custom argtypes elsewhere
+_SPECIAL = ["hs_version", "hs_stream", "hs_cpu_busy_seconds", "hs_wall_seconds",
+            "hs_launch_count", "hs_profile", "hs_profile_read", "hs_probe_dense",
+            "hs_probe_decode", "hs_probe_prefill"]
+
+
 def exported_symbols() -> list[str]:
-    return ["hs_version", *_SIGNATURES]
+    from . import runtime  # noqa: F401  (registers the step-level signatures)
+
+    return sorted(set(_SPECIAL) | set(_SIGNATURES))
 
 
 def last_error() -> str:

@@ -295,7 +295,7 @@ static int launch_decode(const CUtensorMap& kv_map, const KvGeom& g, int layer, 
   decode_attn_kernel<HD><<<grid, kDecThreads, kSmem, st>>>(kv_map, g, layer, q, q_row_stride, n_q,
                                                            pt, pt_stride, chunks, o_part, lse_part,
                                                            scale_log2);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 int decode_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
@@ -326,7 +326,7 @@ int decode_combine(const float* o_part, const float* lse_part, const int* row_ch
                                                       n_q, n_kv, out, out_row_stride, lse_out);
   else
     return HS_E_CONFIG;
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 }  // namespace hs

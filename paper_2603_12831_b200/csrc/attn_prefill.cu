@@ -210,7 +210,7 @@ static int launch_prefill(const CUtensorMap& kv_map, const KvGeom& g, int layer,
   prefill_attn_kernel<HD><<<grid, kPreThreads, kSmem, st>>>(
       kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, tiles, out, out_row_stride,
       scale_log2);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 int prefill_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,

@@ -8,6 +8,7 @@
 
 namespace hs {
 thread_local char g_last_error[512] = {0};
+unsigned long long g_launches = 0;
 
 int set_error(int code, const char* fmt, ...) {
   va_list ap;
@@ -43,6 +44,8 @@ int hs_last_error(char* buf, int cap) {
   }
   return n;
 }
+
+unsigned long long hs_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 int hs_device_ok(void) {
   int dev = 0;

@@ -1,0 +1,194 @@
+// Asynchronous CPU-attention service (live mode).
+//
+// The GPU writes a chain's q/k/v row into its pinned mailbox inside hs_layer;
+// hs_cpu_submit records a CUDA event behind those writes and queues one task
+// per (work item, KV head).  Worker threads wait for the event, append the
+// new k/v to the request's host KV, attend over ctx+1 keys and write the
+// result mailbox; when every head of an item is done the item is appended to
+// the completion FIFO that hs_cpu_poll drains.  This is the per-host input
+// queue -> CPU service -> output queue path of the reference
+// (pkg/src/hybridserve/engine.py:181-191, 512-560) with real workers instead
+// of a charged service time; the GPU never waits on it (results are merged
+// only once polled, engine.py:902-919).
+#include <chrono>
+#include <cstring>
+#include <deque>
+
+#include "hs_step.h"
+
+namespace hs {
+
+struct CpuItem {
+  int slot, layer, ctx;
+  int ev;             // index into the event pool
+  int heads_left;
+  double t_submit;
+};
+
+struct CpuTask {
+  int item;  // index into items_
+  int head;
+};
+
+class CpuService {
+ public:
+  CpuService(const ModelCfg& m, int n_threads, int n_events, const std::vector<int>& cpus)
+      : m_(m) {
+    events_.resize(n_events);
+    ev_refs_.assign(n_events, 0);
+    for (auto& e : events_) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    for (int i = 0; i < n_threads; ++i) {
+      threads_.emplace_back([this] { loop(); });
+      if (!cpus.empty()) {
+        cpu_set_t set;
+        CPU_ZERO(&set);
+        CPU_SET(cpus[i % cpus.size()], &set);
+        pthread_setaffinity_np(threads_.back().native_handle(), sizeof(set), &set);
+      }
+    }
+  }
+
+  ~CpuService() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+    for (auto& e : events_) cudaEventDestroy(e);
+  }
+
+  // mailboxes / KV resolution provided by the context
+  std::function<bf16*(int slot)> ship_row, result_row, host_kv;
+  std::function<int(int slot)> host_cap;
+
+  int submit(cudaStream_t st, const int* slots, const int* layers, const int* ctxs, int n) {
+    if (n <= 0) return HS_OK;
+    int ev;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      // find a free event (all of its previous items finished)
+      ev = -1;
+      for (int k = 0; k < static_cast<int>(events_.size()); ++k) {
+        const int e = (next_ev_ + k) % events_.size();
+        if (ev_refs_[e] == 0) {
+          ev = e;
+          break;
+        }
+      }
+      if (ev < 0) return set_error(HS_E_CAPACITY, "cpu service: event pool exhausted");
+      next_ev_ = (ev + 1) % events_.size();
+      ev_refs_[ev] = n;
+    }
+    if (cudaEventRecord(events_[ev], st) != cudaSuccess)
+      return set_error(HS_E_CUDA, "cpu service: event record failed");
+    const double now = wall();
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      for (int i = 0; i < n; ++i) {
+        const int idx = static_cast<int>(items_.size());
+        items_.push_back(CpuItem{slots[i], layers[i], ctxs[i], ev, m_.n_kv, now});
+        for (int h = 0; h < m_.n_kv; ++h) tasks_.push_back(CpuTask{idx, h});
+      }
+      in_flight_ += n;
+    }
+    cv_.notify_all();
+    return HS_OK;
+  }
+
+  int poll(int* slots, int* layers, double* t_done, int max) {
+    std::lock_guard<std::mutex> g(mu_);
+    int k = 0;
+    while (k < max && !done_.empty()) {
+      const auto d = done_.front();
+      done_.pop_front();
+      slots[k] = std::get<0>(d);
+      layers[k] = std::get<1>(d);
+      if (t_done) t_done[k] = std::get<2>(d);
+      ++k;
+    }
+    return k;
+  }
+
+  int in_flight() {
+    std::lock_guard<std::mutex> g(mu_);
+    return in_flight_;
+  }
+
+  double busy_seconds() const { return busy_ns_.load() * 1e-9; }
+
+  static double wall() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      CpuTask t;
+      CpuItem it;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || !tasks_.empty(); });
+        if (stop_) return;
+        t = tasks_.front();
+        tasks_.pop_front();
+        it = items_[t.item];
+      }
+      cudaEventSynchronize(events_[it.ev]);  // the shipped row has landed
+      const auto t0 = std::chrono::steady_clock::now();
+      cpu_attend_head(m_, ship_row(it.slot), host_kv(it.slot), host_cap(it.slot), it.layer - 1,
+                      it.ctx, t.head, result_row(it.slot), nullptr);
+      busy_ns_ += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                      std::chrono::steady_clock::now() - t0)
+                      .count();
+      std::lock_guard<std::mutex> g(mu_);
+      CpuItem& ref = items_[t.item];
+      if (--ref.heads_left == 0) {
+        done_.emplace_back(ref.slot, ref.layer, wall());
+        --ev_refs_[ref.ev];
+        --in_flight_;
+        // compact the item table once everything queued so far is finished
+        if (in_flight_ == 0 && tasks_.empty()) items_.clear();
+      }
+    }
+  }
+
+  ModelCfg m_;
+  std::vector<std::thread> threads_;
+  std::vector<cudaEvent_t> events_;
+  std::vector<int> ev_refs_;
+  int next_ev_ = 0;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<CpuTask> tasks_;
+  std::vector<CpuItem> items_;
+  std::deque<std::tuple<int, int, double>> done_;
+  int in_flight_ = 0;
+  bool stop_ = false;
+  std::atomic<int64_t> busy_ns_{0};
+};
+
+CpuService* make_cpu_service(const ModelCfg& m, int threads, const std::vector<int>& cpus) {
+  return new CpuService(m, threads, 1024, cpus);
+}
+void destroy_cpu_service(CpuService* s) { delete s; }
+void cpu_service_bind(CpuService* s, std::function<bf16*(int)> ship, std::function<bf16*(int)> res,
+                      std::function<bf16*(int)> kv, std::function<int(int)> cap) {
+  s->ship_row = std::move(ship);
+  s->result_row = std::move(res);
+  s->host_kv = std::move(kv);
+  s->host_cap = std::move(cap);
+}
+int cpu_service_submit(CpuService* s, cudaStream_t st, const int* slots, const int* layers,
+                       const int* ctxs, int n) {
+  return s->submit(st, slots, layers, ctxs, n);
+}
+int cpu_service_poll(CpuService* s, int* slots, int* layers, double* t_done, int max) {
+  return s->poll(slots, layers, t_done, max);
+}
+int cpu_service_in_flight(CpuService* s) { return s->in_flight(); }
+double cpu_service_busy(CpuService* s) { return s->busy_seconds(); }
+double wall_seconds() { return CpuService::wall(); }
+
+}  // namespace hs

@@ -37,7 +37,7 @@ __global__ void embed_kernel(const int* __restrict__ tokens, const bf16* __restr
 int embed_gather(const int* tokens, int rows, const bf16* emb, int d, float* h, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
   embed_kernel<<<rows, 256, 0, st>>>(tokens, emb, d, h);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 // ---------------------------------------------------------------- RMSNorm
@@ -57,7 +57,7 @@ int rmsnorm_rows(const float* h, int rows, int d, const float* w, float eps, bf1
                  cudaStream_t st) {
   if (rows <= 0) return HS_OK;
   rmsnorm_kernel<<<rows, 256, 0, st>>>(h, d, w, eps, out, ld_out);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 // ---------------------------------------------------------------- split-K
@@ -76,7 +76,7 @@ int splitk_reduce(const float* part, int splits, int rows, int n, float* out, cu
   if (!total) return HS_OK;
   const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, size_t(148 * 16)));
   splitk_reduce_kernel<<<blocks, 256, 0, st>>>(part, splits, total, out);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 // h += sum_s part[s]; out = rmsnorm(h) * w   (out may be null)
@@ -104,7 +104,7 @@ int residual_add_norm(const float* part, int splits, int rows, int d, float* h, 
                       float eps, bf16* out, int ld_out, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
   residual_add_norm_kernel<<<rows, 256, 0, st>>>(part, splits, rows, d, h, w, eps, out, ld_out);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 // ---------------------------------------------------------------- QKV epilogue
@@ -197,7 +197,7 @@ int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv,
                                                 rope_sin, row_pos, row_slot, row_mode, qbuf,
                                                 q_row_stride, kv_pool, g, layer, page_table,
                                                 pt_stride, ship, ship_stride);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 // ---------------------------------------------------------------- SwiGLU
@@ -225,7 +225,7 @@ int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld
   if (!total) return HS_OK;
   const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, size_t(148 * 16)));
   silu_mul_kernel<<<blocks, 256, 0, st>>>(part, splits, rows, ffn, act, ld_act);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 // ---------------------------------------------------------------- greedy argmax
@@ -277,7 +277,7 @@ int argmax_rows(const float* part, int splits, int rows, int vocab, int* tokens,
                 cudaStream_t st) {
   if (rows <= 0) return HS_OK;
   argmax_kernel<<<rows, 512, 0, st>>>(part, splits, rows, vocab, tokens, logits_out);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 // ---------------------------------------------------------------- LSE merge
@@ -329,7 +329,7 @@ int lse_merge_rows(const bf16* parts, const float* lse, int n_parts, int rows, i
                                                  row_stride_parts, out, out_row_stride);
   else
     return HS_E_CONFIG;
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 }  // namespace hs

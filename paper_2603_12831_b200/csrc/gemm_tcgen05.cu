@@ -203,7 +203,7 @@ static int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, float* out, i
   dim3 grid(n_out / kTileM, (tokens + BN - 1) / BN, splits);
   gemm_bf16_tn_kernel<BN><<<grid, kGemmThreads, C::kSmemBytes, st>>>(mw, mx, out, n_out, tokens,
                                                                     kbps, kb_total);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 int gemm_launch(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,

@@ -12,6 +12,14 @@ typedef __nv_bfloat16 bf16;
 
 namespace hs {
 
+// every kernel launch site returns through launched(): counts the launch
+// (the bench's gpu_launches) and reports a launch error as HS_E_CUDA
+extern unsigned long long g_launches;
+inline int launched() {
+  __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 4;
+}
+
 // ---- TMA maps / GEMM (gemm_tcgen05.cu) ----
 int make_map_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                      uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);

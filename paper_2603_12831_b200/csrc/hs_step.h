@@ -65,4 +65,17 @@ void cpu_attend_head(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int
 void cpu_attend_one(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int cap, int layer,
                     int ctx, bf16* out_row, float* lse_out);
 
+// asynchronous CPU-attention service (cpu_pool.cpp)
+class CpuService;
+CpuService* make_cpu_service(const ModelCfg& m, int threads, const std::vector<int>& cpus);
+void destroy_cpu_service(CpuService* s);
+void cpu_service_bind(CpuService* s, std::function<bf16*(int)> ship, std::function<bf16*(int)> res,
+                      std::function<bf16*(int)> kv, std::function<int(int)> cap);
+int cpu_service_submit(CpuService* s, cudaStream_t st, const int* slots, const int* layers,
+                       const int* ctxs, int n);
+int cpu_service_poll(CpuService* s, int* slots, int* layers, double* t_done, int max);
+int cpu_service_in_flight(CpuService* s);
+double cpu_service_busy(CpuService* s);
+double wall_seconds();
+
 }  // namespace hs

@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <new>
 #include <vector>
 
@@ -102,6 +103,23 @@ struct hs_ctx {
   std::vector<HostRegion> regions;
   std::vector<std::pair<size_t, size_t>> free_list;  // (offset, bytes)
   ThreadPool* pool = nullptr;
+  CpuService* cpu = nullptr;
+  // swaps: copy stream + contiguous staging for pack/unpack around one 2D DMA
+  cudaStream_t copy_st = nullptr;
+  bf16* swap_stage = nullptr;
+  size_t swap_stage_elems = 0;
+  std::map<int, cudaEvent_t> swap_ev;
+  int next_ticket = 1;
+  // marks (pacing) and timing events on the compute stream
+  std::vector<cudaEvent_t> marks, timers;
+  int next_mark = 0, next_timer = 0;
+  // per-kernel-class profiling (class, start, stop, bytes, flops)
+  bool prof_on = false;
+  struct Rec { int cls; cudaEvent_t a, b; double bytes, flops; };
+  std::vector<Rec> prof_pending;
+  std::vector<cudaEvent_t> prof_free;
+  double prof_stats[3][4] = {};
+  double dec_kv_tokens = 0, pre_units = 0, pre_kv_tokens = 0;
 };
 
 namespace {
@@ -169,6 +187,55 @@ int make_act(ActBuf& a, int rows, int k) {
   return HS_OK;
 }
 
+cudaEvent_t prof_event(hs_ctx* c) {
+  if (!c->prof_free.empty()) {
+    cudaEvent_t e = c->prof_free.back();
+    c->prof_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {  // records a start event now and a stop event on destruction
+  hs_ctx* c;
+  int cls;
+  double bytes, flops;
+  cudaEvent_t a = nullptr;
+  ProfScope(hs_ctx* c_, int cls_, double bytes_, double flops_)
+      : c(c_), cls(cls_), bytes(bytes_), flops(flops_) {
+    if (c->prof_on) {
+      a = prof_event(c);
+      cudaEventRecord(a, c->st);
+    }
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEvent_t b = prof_event(c);
+    cudaEventRecord(b, c->st);
+    c->prof_pending.push_back({cls, a, b, bytes, flops});
+  }
+};
+
+int prof_collect(hs_ctx* c) {
+  if (c->prof_pending.empty()) return HS_OK;
+  CK(cudaEventSynchronize(c->prof_pending.back().b));
+  for (auto& r : c->prof_pending) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    double* st = c->prof_stats[r.cls];
+    st[0] += 1;
+    st[1] += ms;
+    st[2] += r.bytes;
+    st[3] += r.flops;
+    c->prof_free.push_back(r.a);
+    c->prof_free.push_back(r.b);
+  }
+  c->prof_pending.clear();
+  return HS_OK;
+}
+
 // GEMM over `tokens` rows of an activation buffer against a cached weight map.
 int gemm(hs_ctx* c, const CUtensorMap& mw, const ActBuf& x, int tokens, int n_out, int k,
          int* splits_out) {
@@ -176,6 +243,9 @@ int gemm(hs_ctx* c, const CUtensorMap& mw, const ActBuf& x, int tokens, int n_ou
     *splits_out = 1;
     return HS_OK;
   }
+  // algorithmic traffic: weights + bf16 activations in + bf16 result out
+  ProfScope ps(c, 0, 2.0 * n_out * k + 2.0 * tokens * k + 2.0 * tokens * n_out,
+               2.0 * tokens * n_out * k);
   const int bn = gemm_pick_bn(tokens);
   const size_t per_split = static_cast<size_t>(tokens) * n_out;
   const int cap = static_cast<int>(std::min<size_t>(16, c->part_floats / per_split));
@@ -315,6 +385,17 @@ void free_all(hs_ctx* c) {
   if (c->hkv_h) cudaFreeHost(c->hkv_h);
   for (auto& e : c->stage_ev)
     if (e) cudaEventDestroy(e);
+  if (c->cpu) destroy_cpu_service(c->cpu);
+  for (auto e : c->marks) cudaEventDestroy(e);
+  for (auto e : c->prof_free) cudaEventDestroy(e);
+  for (auto& r : c->prof_pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->timers) cudaEventDestroy(e);
+  for (auto& kv : c->swap_ev) cudaEventDestroy(kv.second);
+  F(c->swap_stage);
+  if (c->copy_st) cudaStreamDestroy(c->copy_st);
   if (c->st) cudaStreamDestroy(c->st);
   delete c->pool;
 }
@@ -406,7 +487,76 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
     c->free_list.push_back({0, c->hkv_bytes});
   }
   c->pool = new ThreadPool(std::max(0, r.cpu_threads - 1));
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK(cudaStreamCreateWithPriority(&c->copy_st, cudaStreamNonBlocking, lo));
+  c->marks.resize(64);
+  c->timers.resize(256);
+  for (auto& e : c->marks) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : c->timers) CK(cudaEventCreate(&e));
   CK(cudaStreamSynchronize(c->st));
+  return HS_OK;
+}
+
+bf16* host_region(hs_ctx* c, int slot) {
+  return reinterpret_cast<bf16*>(reinterpret_cast<uint8_t*>(c->hkv_h) + c->regions[slot].offset);
+}
+
+int ensure_cpu_service(hs_ctx* c) {
+  if (c->cpu) return HS_OK;
+  if (c->r.cpu_threads <= 0) return set_error(HS_E_CONFIG, "no CPU attention threads configured");
+  c->cpu = make_cpu_service(c->m, c->r.cpu_threads, {});
+  const int qkv = c->m.qkv_n(), nqh = c->m.n_q * c->m.hd;
+  cpu_service_bind(
+      c->cpu, [c, qkv](int s) { return c->ship_h + static_cast<size_t>(s) * qkv; },
+      [c, nqh](int s) { return c->result_h + static_cast<size_t>(s) * nqh; },
+      [c](int s) { return host_region(c, s); }, [c](int s) { return c->regions[s].cap; });
+  return HS_OK;
+}
+
+// Asynchronous one-shot KV transfer on the copy stream:
+//   out: pool pages -> pack (HBM) -> one 2D DMA into the host region
+//   in:  one 2D DMA into staging -> unpack into the slot's (new) pages
+// ordered after everything already queued on the compute stream.
+int swap_async(hs_ctx* c, int slot, int tokens, bool to_host, int* ticket) {
+  if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
+  HostRegion& hr = c->regions[slot];
+  if (!hr.used) return set_error(HS_E_INTEGRITY, "slot %d has no host KV region", slot);
+  if (tokens > hr.cap) return set_error(HS_E_CAPACITY, "swap of %d tokens exceeds region", tokens);
+  const ModelCfg& m = c->m;
+  const size_t rows = static_cast<size_t>(m.layers) * 2 * m.n_kv;
+  const size_t need = rows * tokens * m.hd;
+  if (need > c->swap_stage_elems) {
+    CK(cudaStreamSynchronize(c->copy_st));
+    if (c->swap_stage) CK(cudaFree(c->swap_stage));
+    c->swap_stage = nullptr;
+    RC(dalloc(&c->swap_stage, need));
+    c->swap_stage_elems = need;
+  }
+  cudaEvent_t dep, done;
+  CK(cudaEventCreateWithFlags(&dep, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  CK(cudaEventRecord(dep, c->st));
+  CK(cudaStreamWaitEvent(c->copy_st, dep, 0));
+  CK(cudaEventDestroy(dep));
+  const int* pages = c->page_table + static_cast<size_t>(slot) * c->r.max_pages_per_req;
+  bf16* host = host_region(c, slot);
+  const size_t w = static_cast<size_t>(tokens) * m.hd * 2;
+  const size_t host_pitch = static_cast<size_t>(hr.cap) * m.hd * 2;
+  if (to_host) {
+    RC(kv_swap(true, c->kv_pool, c->geom, pages, tokens, c->swap_stage, tokens, c->copy_st));
+    if (tokens > 0)
+      CK(cudaMemcpy2DAsync(host, host_pitch, c->swap_stage, w, w, rows, cudaMemcpyDeviceToHost,
+                           c->copy_st));
+  } else {
+    if (tokens > 0)
+      CK(cudaMemcpy2DAsync(c->swap_stage, w, host, host_pitch, w, rows, cudaMemcpyHostToDevice,
+                           c->copy_st));
+    RC(kv_swap(false, c->kv_pool, c->geom, pages, tokens, c->swap_stage, tokens, c->copy_st));
+  }
+  CK(cudaEventRecord(done, c->copy_st));
+  *ticket = c->next_ticket++;
+  c->swap_ev[*ticket] = done;
   return HS_OK;
 }
 
@@ -422,6 +572,43 @@ int kv_swap_pages(hs_ctx* c, int slot, int tokens, bool to_host) {
   return HS_OK;
 }
 
+}  // namespace
+
+namespace {
+template <typename F>
+int time_reps(hs_ctx* c, int reps, F&& body, float* us) {
+  std::vector<float> ts;
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  for (int i = 0; i < reps + 2; ++i) {
+    CK(cudaEventRecord(a, c->st));
+    RC(body());
+    CK(cudaEventRecord(b, c->st));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    if (i >= 2) ts.push_back(ms * 1000.f);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  std::sort(ts.begin(), ts.end());
+  *us = ts[ts.size() / 2];
+  return HS_OK;
+}
+
+int probe_pages(hs_ctx* c, int g, int tokens) {
+  const int per = (tokens + kPageTokens - 1) / kPageTokens;
+  if (per > c->r.max_pages_per_req || g > c->r.max_slots)
+    return set_error(HS_E_CAPACITY, "probe exceeds page table");
+  std::vector<int> pt(per);
+  for (int s = 0; s < g; ++s) {
+    for (int i = 0; i < per; ++i) pt[i] = (s * per + i) % c->r.kv_pages;
+    CK(cudaMemcpy(c->page_table + static_cast<size_t>(s) * c->r.max_pages_per_req, pt.data(),
+                  per * 4, cudaMemcpyHostToDevice));
+  }
+  return HS_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -609,6 +796,16 @@ int hs_iter_begin(hs_ctx* c, const hs_iter_desc* d) {
   RC(upload(c, L.row_chunk_begin, d->row_chunk_begin, d->n_chunks ? d->n_decode + 1 : 0));
   RC(upload(c, L.tiles, d->tiles, static_cast<size_t>(d->n_tiles) * 4));
   RC(upload(c, L.logit_rows, d->logit_rows, d->n_logit_rows));
+  c->dec_kv_tokens = 0;
+  for (int r = 0; r < d->n_decode && d->n_chunks; ++r)
+    c->dec_kv_tokens += d->chunks[static_cast<size_t>(d->row_chunk_begin[r]) * 5 + 4];
+  c->pre_units = 0;
+  c->pre_kv_tokens = 0;
+  for (int t = 0; t < d->n_tiles; ++t) {
+    const double pos0 = d->tiles[t * 4 + 2], nq = d->tiles[t * 4 + 3];
+    c->pre_units += nq * pos0 + nq * (nq + 1) / 2;
+    c->pre_kv_tokens += pos0 + nq;
+  }
   std::vector<int> lslot(d->n_logit_rows);
   for (int i = 0; i < d->n_logit_rows; ++i) lslot[i] = d->row_slot[d->logit_rows[i]];
   RC(upload(c, L.logit_slot, lslot.data(), lslot.size()));
@@ -649,14 +846,21 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
                       dm + L.row_pos, dm + L.row_slot, dm + L.row_mode, c->qbuf, nqh, c->kv_pool,
                       c->geom, l, c->page_table, r.max_pages_per_req, c->ship_d, m.qkv_n(), st));
   // attention of batch rows
+  {
+  ProfScope pd(c, 1, c->dec_kv_tokens * 2.0 * m.n_kv * m.hd * 2.0 + 4.0 * c->D * nqh,
+               4.0 * c->dec_kv_tokens * nqh);
   RC(decode_attention(c->m_kv, c->geom, l, c->qbuf, nqh, m.n_q, c->page_table,
                       r.max_pages_per_req, reinterpret_cast<const DecodeChunk*>(dm + L.chunks),
                       c->n_chunks, c->o_part, c->lse_part, st));
   RC(decode_combine(c->o_part, c->lse_part, dm + L.row_chunk_begin, c->n_chunks ? c->D : 0, m.n_q,
                     m.n_kv, m.hd, c->attn.p, nqh, nullptr, st));
+  }
+  {
+  ProfScope pp(c, 2, c->pre_kv_tokens * 2.0 * m.n_kv * m.hd * 2.0, 4.0 * c->pre_units * nqh);
   RC(prefill_attention(c->m_kv, c->geom, l, c->qbuf, nqh, m.n_q, c->page_table,
                        r.max_pages_per_req, reinterpret_cast<const PrefillTile*>(dm + L.tiles),
                        c->n_tiles, c->attn.p, nqh, st));
+  }
   // merged rows: host attention result + stored residual
   RC(upload(c, L.merge_slot, d->merge_slot, M));
   RC(gather_rows_bf16(c->result_d, nqh, dm + L.merge_slot, M, nqh,
@@ -721,6 +925,7 @@ int hs_iter_end(hs_ctx* c, int* tokens_out, int n) {
     CK(cudaMemcpyAsync(c->tokens_pinned, c->tok_out, c->n_tok_out * sizeof(int),
                        cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  RC(prof_collect(c));
   if (c->n_tok_out > 0) std::memcpy(tokens_out, c->tokens_pinned, c->n_tok_out * sizeof(int));
   return c->n_tok_out;
 }
@@ -747,6 +952,150 @@ int hs_cpu_attend(hs_ctx* c, const int* slots, const int* layers, const int* ctx
   });
   return HS_OK;
 }
+
+int hs_mark(hs_ctx* c) {
+  const int id = c->next_mark++;
+  CK(cudaEventRecord(c->marks[id % c->marks.size()], c->st));
+  return id;
+}
+
+int hs_wait_mark(hs_ctx* c, int id) {
+  if (id < 0 || id < c->next_mark - static_cast<int>(c->marks.size())) return HS_OK;
+  CK(cudaEventSynchronize(c->marks[id % c->marks.size()]));
+  return HS_OK;
+}
+
+int hs_timer(hs_ctx* c) {
+  const int id = c->next_timer++;
+  CK(cudaEventRecord(c->timers[id % c->timers.size()], c->st));
+  return id;
+}
+
+int hs_timer_elapsed(hs_ctx* c, int a, int b, float* ms) {
+  const int n = static_cast<int>(c->timers.size());
+  if (a < c->next_timer - n || b < c->next_timer - n)
+    return set_error(HS_E_CONFIG, "timer %d/%d recycled", a, b);
+  CK(cudaEventSynchronize(c->timers[b % n]));
+  CK(cudaEventElapsedTime(ms, c->timers[a % n], c->timers[b % n]));
+  return HS_OK;
+}
+
+int hs_profile(hs_ctx* c, int on) {
+  c->prof_on = on != 0;
+  return HS_OK;
+}
+
+int hs_profile_read(hs_ctx* c, double* stats, int reset) {
+  RC(prof_collect(c));
+  std::memcpy(stats, c->prof_stats, sizeof(c->prof_stats));
+  if (reset) std::memset(c->prof_stats, 0, sizeof(c->prof_stats));
+  return HS_OK;
+}
+
+int hs_probe_dense(hs_ctx* c, int n, int reps, float* us) {
+  const ModelCfg& m = c->m;
+  if (n < 1 || n > c->r.max_rows) return set_error(HS_E_CONFIG, "probe rows out of range");
+  const int d_ = m.d, nqh = m.n_q * m.hd;
+  return time_reps(c, reps, [&]() -> int {
+    int sp;
+    RC(gemm(c, c->m_qkv[0], c->xn, n, m.qkv_n(), d_, &sp));
+    RC(gemm(c, c->m_o[0], c->attn, n, d_, nqh, &sp));
+    RC(residual_add_norm(c->part, sp, n, d_, c->h, c->n_post[0], m.eps, c->xn2.p, d_, c->st));
+    RC(gemm(c, c->m_gu[0], c->xn2, n, 2 * m.ffn, d_, &sp));
+    RC(silu_mul(c->part, sp, n, m.ffn, c->act.p, m.ffn, c->st));
+    RC(gemm(c, c->m_down[0], c->act, n, d_, m.ffn, &sp));
+    RC(residual_add_norm(c->part, sp, n, d_, c->h, c->n_in[0], m.eps, c->xn.p, d_, c->st));
+    return HS_OK;
+  }, us);
+}
+
+int hs_probe_decode(hs_ctx* c, int g, int ctx_len, int reps, float* us) {
+  const ModelCfg& m = c->m;
+  if (g < 1 || g > c->r.max_rows) return set_error(HS_E_CONFIG, "probe rows out of range");
+  RC(probe_pages(c, g, ctx_len));
+  const int per = (ctx_len + kPageTokens - 1) / kPageTokens;
+  const int chunk = std::max(1, std::min(64, (g * per * m.n_kv + 295) / 296));
+  std::vector<int> ch, beg{0};
+  for (int r = 0; r < g; ++r) {
+    for (int p0 = 0; p0 < per; p0 += chunk) {
+      ch.insert(ch.end(), {r, r, p0, std::min(per, p0 + chunk), ctx_len});
+    }
+    beg.push_back(static_cast<int>(ch.size() / 5));
+  }
+  if (static_cast<int>(ch.size() / 5) > c->r.max_chunks)
+    return set_error(HS_E_CAPACITY, "probe exceeds max_chunks");
+  const MetaLayout L = layout_of(c->r);
+  CK(cudaMemcpy(c->dm + L.chunks, ch.data(), ch.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->dm + L.row_chunk_begin, beg.data(), beg.size() * 4, cudaMemcpyHostToDevice));
+  const int nch = static_cast<int>(ch.size() / 5), nqh = m.n_q * m.hd;
+  return time_reps(c, reps, [&]() -> int {
+    RC(decode_attention(c->m_kv, c->geom, 0, c->qbuf, nqh, m.n_q, c->page_table,
+                        c->r.max_pages_per_req,
+                        reinterpret_cast<const DecodeChunk*>(c->dm + L.chunks), nch, c->o_part,
+                        c->lse_part, c->st));
+    RC(decode_combine(c->o_part, c->lse_part, c->dm + L.row_chunk_begin, g, m.n_q, m.n_kv, m.hd,
+                      c->attn.p, nqh, nullptr, c->st));
+    return HS_OK;
+  }, us);
+}
+
+int hs_probe_prefill(hs_ctx* c, int q, int done, int reps, float* us) {
+  const ModelCfg& m = c->m;
+  if (q < 1 || q > c->r.max_rows) return set_error(HS_E_CONFIG, "probe rows out of range");
+  RC(probe_pages(c, 1, done + q));
+  std::vector<int> tiles;
+  for (int j = 0; j < q; j += 64) tiles.insert(tiles.end(), {0, j, done + j, std::min(64, q - j)});
+  const MetaLayout L = layout_of(c->r);
+  CK(cudaMemcpy(c->dm + L.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice));
+  const int nt = static_cast<int>(tiles.size() / 4), nqh = m.n_q * m.hd;
+  return time_reps(c, reps, [&]() -> int {
+    return prefill_attention(c->m_kv, c->geom, 0, c->qbuf, nqh, m.n_q, c->page_table,
+                             c->r.max_pages_per_req,
+                             reinterpret_cast<const PrefillTile*>(c->dm + L.tiles), nt, c->attn.p,
+                             nqh, c->st);
+  }, us);
+}
+
+int hs_swap_out_async(hs_ctx* c, int slot, int tokens, int* ticket) {
+  return swap_async(c, slot, tokens, true, ticket);
+}
+
+int hs_swap_in_async(hs_ctx* c, int slot, int tokens, int* ticket) {
+  return swap_async(c, slot, tokens, false, ticket);
+}
+
+int hs_swap_done(hs_ctx* c, int ticket) {
+  auto it = c->swap_ev.find(ticket);
+  if (it == c->swap_ev.end()) return set_error(HS_E_CONFIG, "unknown swap ticket %d", ticket);
+  const cudaError_t e = cudaEventQuery(it->second);
+  if (e == cudaErrorNotReady) return 0;
+  if (e != cudaSuccess) return set_error(HS_E_CUDA, "swap: %s", cudaGetErrorString(e));
+  cudaEventDestroy(it->second);
+  c->swap_ev.erase(it);
+  return 1;
+}
+
+int hs_cpu_submit(hs_ctx* c, const int* slots, const int* layers, const int* ctxs, int n) {
+  RC(ensure_cpu_service(c));
+  for (int i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= c->r.max_slots || !c->regions[slots[i]].used)
+      return set_error(HS_E_INTEGRITY, "work item for slot %d without host KV", slots[i]);
+    if (ctxs[i] >= c->regions[slots[i]].cap)
+      return set_error(HS_E_CAPACITY, "host KV of slot %d full (ctx %d)", slots[i], ctxs[i]);
+  }
+  return cpu_service_submit(c->cpu, c->st, slots, layers, ctxs, n);
+}
+
+int hs_cpu_poll(hs_ctx* c, int* slots, int* layers, double* t_done, int max) {
+  if (!c->cpu) return 0;
+  return cpu_service_poll(c->cpu, slots, layers, t_done, max);
+}
+
+int hs_cpu_in_flight(hs_ctx* c) { return c->cpu ? cpu_service_in_flight(c->cpu) : 0; }
+
+double hs_cpu_busy_seconds(hs_ctx* c) { return c->cpu ? cpu_service_busy(c->cpu) : 0.0; }
+
+double hs_wall_seconds(void) { return wall_seconds(); }
 
 int hs_sync(hs_ctx* c) {
   CK(cudaStreamSynchronize(c->st));

@@ -87,34 +87,34 @@ int select_tokens(const int* row_token, const int* row_slot, const int* last_tok
   if (rows <= 0) return HS_OK;
   select_tokens_kernel<<<(rows + 127) / 128, 128, 0, st>>>(row_token, row_slot, last_token, rows,
                                                            tok);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 int gather_rows_f32(const float* src, const int* idx, int rows, int d, float* dst,
                     cudaStream_t st) {
   if (rows <= 0) return HS_OK;
   gather_rows_f32_kernel<<<rows, 256, 0, st>>>(src, idx, d, dst);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 int scatter_rows_f32(const float* src, const int* idx, int rows, int d, float* dst,
                      cudaStream_t st) {
   if (rows <= 0) return HS_OK;
   scatter_rows_f32_kernel<<<rows, 256, 0, st>>>(src, idx, d, dst);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 int gather_rows_bf16(const bf16* src, int src_stride, const int* idx, int rows, int w, bf16* dst,
                      int dst_stride, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
   gather_rows_bf16_kernel<<<rows, 128, 0, st>>>(src, src_stride, idx, w, dst, dst_stride);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 int scatter_tokens(const int* tok, const int* slot, int n, int* last_token, cudaStream_t st) {
   if (n <= 0) return HS_OK;
   scatter_tokens_kernel<<<(n + 127) / 128, 128, 0, st>>>(tok, slot, n, last_token);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 int kv_swap(bool to_host, bf16* pool, const KvGeom& g, const int* pages, int tokens, bf16* host,
@@ -125,7 +125,7 @@ int kv_swap(bool to_host, bf16* pool, const KvGeom& g, const int* pages, int tok
     kv_swap_kernel<true><<<grid, 256, 0, st>>>(pool, g, pages, tokens, host, cap);
   else
     kv_swap_kernel<false><<<grid, 256, 0, st>>>(pool, g, pages, tokens, host, cap);
-  return cudaPeekAtLastError() == cudaSuccess ? HS_OK : HS_E_CUDA;
+  return launched();
 }
 
 }  // namespace hs

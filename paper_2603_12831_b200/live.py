@@ -1,0 +1,214 @@
+"""Live serving: the engine on the wall clock with real asynchronous work.
+
+`LiveEngine` keeps every planning rule and state transition of `Engine`
+(and therefore of the reference, pkg/src/hybridserve/engine.py) and changes
+only where time comes from:
+
+* iterations run on the B200 (`LiveCudaStep`); layer l is launched once the
+  GPU is at most one layer behind, so the merges consumed at its start are
+  the results that have *really* arrived (the reference's FIFO head-run
+  semantics, engine.py:902-919, evaluated at launch time);
+* work items are submitted to the CPU-attention pool behind a CUDA event of
+  the layer that shipped their q/k/v, and completions enter the output FIFO
+  in completion order (engine.py:512-560);
+* KV swaps run on the copy stream; a swap-in starts once the request's chain
+  is idle so every token's KV is on the host (engine.py:456-497);
+* token times are CUDA-synchronised wall-clock stamps, so LS TPOT
+  attainment and BE tokens/s are measured, not charged.
+
+The virtual-time call sites are rerouted through `_push`, so the base-class
+code paths are reused unchanged.
+"""
+
+from __future__ import annotations
+
+import time
+from collections import deque
+from typing import Callable, Optional
+
+from .engine import (
+    EV_LAYER_DONE,
+    EV_RESULT,
+    EV_SERVICE_DONE,
+    EV_SWAP_DONE,
+    EV_WORKITEM,
+    Engine,
+)
+from .state import IterationState, ResultItem, SimRequest
+from .workload import build_requests
+
+
+class LiveEngine(Engine):
+    def __init__(self, scenario, models=None, step=None, pace_layers: int = 1):
+        super().__init__(scenario, models=models, step=step)
+        self.t0 = time.perf_counter()
+        self.pace_layers = pace_layers
+        self._unshipped: dict[str, object] = {}   # WorkItems awaiting their ship launch
+        self._submitted: dict[str, object] = {}   # WorkItems in the CPU pool
+        self._swaps: dict[int, tuple[str, str]] = {}
+        self._swapin_wait: set[str] = set()
+        self._chain_token_marks: list[tuple[SimRequest, int]] = []
+        self._dirty = True
+        self.iteration_log: list[dict] = []
+
+    def clock(self) -> float:
+        return time.perf_counter() - self.t0
+
+    # -- rerouted virtual-time actions -----------------------------------------
+
+    def _push(self, t: float, kind: str, payload) -> None:
+        if kind == EV_WORKITEM:
+            self._unshipped[payload.req_id] = payload
+        elif kind == EV_SWAP_DONE:
+            rid, direction = payload
+            req = self.requests[rid]
+            if direction == "out":
+                self._swaps[self.step.swap_out_async(req)] = (rid, "out")
+            else:
+                self._swapin_wait.add(rid)
+        elif kind in (EV_LAYER_DONE, EV_SERVICE_DONE, EV_RESULT):
+            raise AssertionError(f"{kind} is not scheduled in live mode")
+        else:
+            super()._push(t, kind, payload)
+
+    def _emit_token(self, req: SimRequest, t: float) -> None:
+        super()._emit_token(req, t)
+        if self._iter is not None:
+            # chain token completed inside the iteration: stamp at its end
+            self._chain_token_marks.append((req, len(req.token_times) - 1))
+
+    # -- async completions ---------------------------------------------------------
+
+    def _poll_async(self) -> None:
+        now = self.clock()
+        for rid, layer in self.step.cpu_poll():
+            item = self._submitted.pop(rid)
+            self.now = now
+            if self.opts.record_traces:
+                self.traces.setdefault(rid, []).append((layer, "Attn", "CPU"))
+            self._on_result(ResultItem(rid, layer, now, item.enq_seq))
+            self._dirty = True
+        for ticket in [t for t in self._swaps if self.step.swap_done(t)]:
+            rid, direction = self._swaps.pop(ticket)
+            self.now = now
+            req = self.requests[rid]
+            if direction == "out":
+                self._finish_swap_out(req)
+            else:
+                self._finish_swap_in(req)
+            self._dirty = True
+        for rid in list(self._swapin_wait):
+            req = self.requests[rid]
+            if req.phase == "done" or req.swap_state != "in_transfer":
+                self._swapin_wait.discard(rid)
+                continue
+            if req.chain_state in ("none", "inject"):
+                self._swapin_wait.discard(rid)
+                self._swaps[self.step.swap_in_async(req)] = (rid, "in")
+
+    def _submit_shipped(self, req_ids) -> None:
+        items = [self._unshipped.pop(rid) for rid in req_ids]
+        if not items:
+            return
+        self.step.cpu_submit(items)
+        for it in items:
+            self._submitted[it.req_id] = it
+            self.queues.input_enq += 1
+            self.queues.input_deq += 1
+            self._log("workitem_enq", request=it.req_id, layer=it.layer, host=0)
+
+    # -- iterations -------------------------------------------------------------------
+
+    def _live_iteration(self, plan) -> bool:
+        cap = self._merge_cap(plan.loads)
+        has_work = (plan.ls_decode or plan.ls_prefill_chunks or plan.be_prefill_chunks
+                    or plan.be_decode_gpu
+                    or (cap > 0 and (self.queues.output or self.pending_injections)))
+        if not has_work:
+            return False
+        self.gpu_busy = True
+        self.counters["iterations"] += 1
+        it = IterationState(plan=plan, merge_cap=cap, start=self.now, layer=1, merges_total=0,
+                            merge_layers={})
+        self._iter = it
+        self._chain_token_marks = []
+        self.step.begin_iteration(plan)
+        for layer in range(1, self.layers + 1):
+            it.layer = layer
+            self.step.pace(self.pace_layers)
+            self._poll_async()
+            self.now = start = self.clock()
+            merged = self._consume_merges(layer, cap)
+            if merged:
+                it.merges_total += len(merged)
+                it.merge_layers[layer] = len(merged)
+                self.counters["merges"] += len(merged)
+            outcomes = [(item, self._process_merge(item, layer, start, start))
+                        for item in merged]
+            self._submit_shipped(self.step.layer(layer, outcomes))
+            if self.opts.record_layer_times:
+                self.layer_start_log.append((it.start, layer, start))
+        self.step.end_iteration(plan)
+        self.now = end = self.clock()
+        chain_tokens = len(self._chain_token_marks)
+        for req, idx in self._chain_token_marks:
+            req.token_times[idx] = end
+            if req.first_token_time is not None and idx == 0:
+                req.first_token_time = end
+            if req.completion is not None:
+                req.completion = end
+        self._chain_token_marks = []
+        rec = {"start": it.start, "end": end, "decodes": len(plan.ls_decode) +
+               len(plan.be_decode_gpu), "ls_decodes": len(plan.ls_decode),
+               "be_gpu_decodes": len(plan.be_decode_gpu),
+               "chunk_tokens": sum(q for _, q in plan.ls_prefill_chunks + plan.be_prefill_chunks),
+               "merges": it.merges_total, "batch_tokens": plan.loads.batch_tokens,
+               "chain_tokens": chain_tokens, "device_ms": self.step.last_device_ms}
+        self.iteration_log.append(rec)
+        self._log("iteration", **{k: v for k, v in rec.items() if k != "device_ms"})
+        self._iter = None
+        self.gpu_busy = False
+        self._commit_iteration(plan)
+        self._dirty = True
+        return True
+
+    # -- main loop ------------------------------------------------------------------------
+
+    def admit_specs(self, specs) -> deque:
+        q = deque()
+        for spec in specs:
+            req = SimRequest(spec)
+            self.requests[req.id] = req
+            q.append(req)
+        return q
+
+    def run_live(self, max_iterations: Optional[int] = None, horizon_s: Optional[float] = None,
+                 on_iteration: Optional[Callable[[int], None]] = None,
+                 arrivals: Optional[deque] = None, idle_exit: bool = True) -> int:
+        """Serve until `max_iterations`, the horizon, or (idle_exit) no work
+        is left.  Returns the number of iterations run."""
+        if arrivals is None:
+            arrivals = self.admit_specs(build_requests(self.scenario.workload,
+                                                       horizon_s or self.scenario.horizon_s))
+        n = 0
+        horizon = horizon_s if horizon_s is not None else float("inf")
+        while True:
+            self.now = self.clock()
+            if self.now > horizon or (max_iterations is not None and n >= max_iterations):
+                break
+            while arrivals and arrivals[0].arrival <= self.now:
+                self._on_arrival(arrivals.popleft())
+                self._dirty = True
+            self._poll_async()
+            if self._dirty and self._runnable():
+                self._dirty = False
+                if self._live_iteration(self._plan()):
+                    n += 1
+                    if on_iteration:
+                        on_iteration(n)
+                    continue
+            if idle_exit and not arrivals and not self._submitted and not self._swaps \
+                    and not self._swapin_wait and not self._runnable():
+                break
+            time.sleep(2e-5)
+        return n

@@ -88,7 +88,19 @@ _CTX_SIGS = {
     "hs_read_logits": [C.c_void_p, C.c_void_p, C.c_int],
     "hs_read_ship": [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t],
     "hs_read_residual": [C.c_void_p, C.c_int, C.c_void_p],
+    "hs_cpu_submit": [C.c_void_p, _IP, _IP, _IP, C.c_int],
+    "hs_cpu_poll": [C.c_void_p, _IP, _IP, C.c_void_p, C.c_int],
+    "hs_cpu_in_flight": [C.c_void_p],
+    "hs_swap_out_async": [C.c_void_p, C.c_int, C.c_int, _IP],
+    "hs_swap_in_async": [C.c_void_p, C.c_int, C.c_int, _IP],
+    "hs_swap_done": [C.c_void_p, C.c_int],
+    "hs_mark": [C.c_void_p],
+    "hs_wait_mark": [C.c_void_p, C.c_int],
+    "hs_timer": [C.c_void_p],
+    "hs_timer_elapsed": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)],
 }
+_NONNEG_RETURNS = {"hs_iter_end", "hs_cpu_poll", "hs_cpu_in_flight", "hs_swap_done", "hs_mark",
+                   "hs_timer"}
 _lib._SIGNATURES.update(_CTX_SIGS)
 
 
@@ -124,6 +136,16 @@ class HsContext:
             fn.restype = C.c_int
         lib.hs_stream.argtypes = [C.c_void_p]
         lib.hs_stream.restype = C.c_void_p
+        lib.hs_cpu_busy_seconds.argtypes = [C.c_void_p]
+        lib.hs_cpu_busy_seconds.restype = C.c_double
+        lib.hs_wall_seconds.argtypes = []
+        lib.hs_wall_seconds.restype = C.c_double
+        lib.hs_launch_count.argtypes = []
+        lib.hs_launch_count.restype = C.c_ulonglong
+        lib.hs_profile.argtypes = [C.c_void_p, C.c_int]
+        lib.hs_profile.restype = C.c_int
+        lib.hs_profile_read.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int]
+        lib.hs_profile_read.restype = C.c_int
         _lib.require_device()
         self.lib = lib
         self.model = model
@@ -150,8 +172,10 @@ class HsContext:
 
     def _call(self, name: str, *args) -> int:
         rc = getattr(self.lib, name)(self.h, *args)
-        if rc < 0 or (rc > 0 and name != "hs_iter_end"):
-            _lib.check(rc, name)
+        if rc > 0 and name in _NONNEG_RETURNS:
+            return rc
+        if rc != 0:
+            _lib.check(rc if rc > 0 else -rc, name)
         return rc
 
     @property
@@ -226,6 +250,42 @@ class HsContext:
 
     def sync(self) -> None:
         self._call("hs_sync")
+
+    # live mode
+    def cpu_submit(self, slots, layers, ctxs) -> None:
+        s, l, c = _i32(slots), _i32(layers), _i32(ctxs)
+        self._call("hs_cpu_submit", _ip(s), _ip(l), _ip(c), len(s))
+
+    def cpu_poll(self, max_items: int = 4096):
+        s = np.zeros(max_items, np.int32)
+        l = np.zeros(max_items, np.int32)
+        n = self._call("hs_cpu_poll", _ip(s), _ip(l), None, max_items)
+        return s[:n], l[:n]
+
+    def cpu_busy_seconds(self) -> float:
+        return self.lib.hs_cpu_busy_seconds(self.h)
+
+    def swap_async(self, slot: int, tokens: int, out: bool) -> int:
+        t = C.c_int(0)
+        self._call("hs_swap_out_async" if out else "hs_swap_in_async", slot, tokens, C.byref(t))
+        return t.value
+
+    def swap_done(self, ticket: int) -> bool:
+        return self._call("hs_swap_done", ticket) == 1
+
+    def mark(self) -> int:
+        return self._call("hs_mark")
+
+    def wait_mark(self, mark_id: int) -> None:
+        self._call("hs_wait_mark", mark_id)
+
+    def timer(self) -> int:
+        return self._call("hs_timer")
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_float(0)
+        self._call("hs_timer_elapsed", a, b, C.byref(ms))
+        return ms.value
 
     def keep_logits(self, on: bool = True) -> None:
         self._call("hs_keep_logits", int(on))
@@ -311,6 +371,9 @@ class CudaStep(LayerStep):
         self.last_tokens: Optional[np.ndarray] = None
         self.iterations = 0
         self._pending_release: list[str] = []
+        # host<->device bytes moved by the step (metadata, tokens, piggyback rows)
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
 
     # -- bookkeeping --------------------------------------------------------
 
@@ -385,6 +448,9 @@ class CudaStep(LayerStep):
                 self._logit_reqs.append(rid)
         chunks, begin = decode_chunks(dec_ctx, self.model.n_kv)
         chunks = [(row, slots[row], p0, p1, c) for row, _, p0, p1, c in chunks]
+        self.h2d_bytes += 4 * (4 * len(slots) + 5 * len(chunks) + len(begin) + 4 * len(tiles)
+                               + 2 * len(logit_rows))
+        self.h2d_bytes += 4 * sum(len(self.pages.owned.get(s_, [])) for s_ in self._dirty)
         self._flush_pages()
         self.ctx.iter_begin(slots, pos, toks, n_dec, chunks, begin, tiles, logit_rows)
         self._carry = []
@@ -398,10 +464,10 @@ class CudaStep(LayerStep):
             r = eng.requests[item.req_id]
             s = self.slot_of(item.req_id)
             if outcome == MERGE_INJECT:
-                carry.append((s, r.ctx))
+                carry.append((s, r.ctx, item.req_id))
                 continue
             if outcome == MERGE_CHAIN:
-                next_carry.append((s, r.ctx))
+                next_carry.append((s, r.ctx, item.req_id))
             elif outcome == MERGE_TOKEN_NEXT:
                 restart_idx.append(len(merge_slots))
                 restart_pos.append(r.ctx)
@@ -409,15 +475,22 @@ class CudaStep(LayerStep):
             merge_ids.append(item.req_id)
         self.ctx.layer(layer, [c[0] for c in carry], [c[1] for c in carry], merge_slots,
                        restart_idx, restart_pos)
+        shipped = [c[2] for c in carry] + [merge_ids[i] for i in restart_idx]
+        m = self.model
+        self.h2d_bytes += 4 * (4 * len(carry) + len(merge_slots) + 4 * len(restart_idx))
+        self.h2d_bytes += len(merge_slots) * m.result_bytes       # host result rows (PCIe reads)
+        self.d2h_bytes += len(shipped) * m.ship_bytes             # q|k|v rows (PCIe writes)
         self._carry = next_carry
         if layer == self.model.n_layers:
             self._merge_L = merge_ids
+        return shipped
 
     def end_iteration(self, plan) -> None:
         toks = self.ctx.iter_end()
         reqs = self._logit_reqs + self._merge_L
         if len(toks) != len(reqs):
             raise RuntimeError(f"libhs returned {len(toks)} tokens for {len(reqs)} rows")
+        self.d2h_bytes += 4 * len(toks)
         for rid, t in zip(reqs, toks):
             self.generated.setdefault(rid, []).append(int(t))
         self.last_token_reqs = reqs
@@ -470,3 +543,73 @@ class CudaStep(LayerStep):
     def finish(self) -> None:
         self.ctx.sync()
         self._release_pending()
+
+
+class LiveCudaStep(CudaStep):
+    """CudaStep for LiveEngine: asynchronous CPU service and swaps, launch
+    pacing and per-iteration device timing (CUDA events)."""
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        self._marks: list[int] = []
+        self._t_begin = -1
+        self.last_device_ms = 0.0
+        self.device_ms_total = 0.0
+        self.swap_out_tickets: dict[int, str] = {}
+
+    def begin_iteration(self, plan) -> None:
+        super().begin_iteration(plan)
+        self._t_begin = self.ctx.timer()
+        self._marks = []
+
+    def layer(self, layer: int, merges):
+        shipped = super().layer(layer, merges)
+        self._marks.append(self.ctx.mark())
+        return shipped
+
+    def pace(self, lag: int) -> None:
+        """Block until at most `lag` launched layers are still queued."""
+        if len(self._marks) > lag:
+            self.ctx.wait_mark(self._marks[-lag - 1])
+
+    def end_iteration(self, plan) -> None:
+        t_end = self.ctx.timer()
+        super().end_iteration(plan)
+        self.last_device_ms = self.ctx.elapsed_ms(self._t_begin, t_end)
+        self.device_ms_total += self.last_device_ms
+
+    def cpu_submit(self, items) -> None:
+        self.ctx.cpu_submit([self.slot_of(it.req_id) for it in items],
+                            [it.layer for it in items], [it.ctx_tokens for it in items])
+
+    def cpu_poll(self):
+        slots, layers = self.ctx.cpu_poll()
+        if not len(slots):
+            return []
+        by_slot = {s: rid for rid, s in self.slots.items()}
+        return [(by_slot[int(s)], int(l)) for s, l in zip(slots, layers)]
+
+    def swap_out_async(self, req) -> int:
+        s = self.slot_of(req.id)
+        self.ctx.host_kv_reserve(s, req.prompt_len + req.output_len + 1)
+        return self.ctx.swap_async(s, req.kv_held, out=True)
+
+    def swap_in_async(self, req) -> int:
+        s = self.slot_of(req.id)
+        self._ensure(s, req.ctx)
+        self._flush_pages()
+        return self.ctx.swap_async(s, req.ctx, out=False)
+
+    def swap_done(self, ticket: int) -> bool:
+        return self.ctx.swap_done(ticket)
+
+    def swap_out_done(self, req) -> None:
+        s = self.slot_of(req.id)
+        self.pages.release(s)
+        self._dirty.add(s)
+
+    def resumed_on_gpu(self, req) -> None:
+        self.ctx.host_kv_release(self.slot_of(req.id))
+
+    def cpu_service(self, host_id: int, items) -> None:
+        raise AssertionError("live mode submits work items asynchronously")
