@@ -154,6 +154,33 @@ def prepopulate_be(engine, step, n: int, seed: int) -> list:
     return out
 
 
+def prepopulate_ls(engine, step, n: int, seed: int) -> list:
+    """LS requests already decoding on the GPU (synthetic KV pages): a
+    steady-state batch that does not depend on wall-clock arrivals (used for
+    profiler captures, where kernels are serialised)."""
+    from paper_2603_12831_b200.state import SimRequest
+    from paper_2603_12831_b200.workload import RequestSpec, ServiceClass, sharegpt_like
+
+    pairs = sharegpt_like().pairs
+    out = []
+    for i in range(n):
+        p, o = pairs[(seed * 31 + i) % len(pairs)]
+        r = SimRequest(RequestSpec(f"LS-P{i:04d}", ServiceClass.LS, p, max(o, 400), 0.0))
+        engine.requests[r.id] = r
+        r.admitted = True
+        r.phase = "decode"
+        r.prefill_done = p
+        r.tokens_out = 1
+        r.token_times = [0.0]
+        r.first_token_time = 0.0
+        r.kv_place = "gpu"
+        r.kv_held = r.ctx
+        engine.kv.alloc_gpu(r.kv_held)
+        step._ensure(step.slot_of(r.id), r.ctx)
+        out.append(r)
+    return out
+
+
 def window_metrics(engine, t0: float, t1: float) -> dict:
     from paper_2603_12831_b200.workload import ServiceClass
 
@@ -313,6 +340,8 @@ def run_ours(args) -> None:
         models = profiler.load(models_path)
     engine = LiveEngine(scenario, models=models, step=step)
     prepopulate_be(engine, step, args.be_chains, args.seed + rank)
+    if args.ls_decodes:
+        prepopulate_ls(engine, step, args.ls_decodes, args.seed + rank)
     from paper_2603_12831_b200.workload import build_requests
 
     arrivals = engine.admit_specs(build_requests(scenario.workload, 600.0))
@@ -442,6 +471,7 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ls-rate", type=float, default=8.0)
     ap.add_argument("--be-chains", type=int, default=32)
+    ap.add_argument("--ls-decodes", type=int, default=0)
     ap.add_argument("--gpu-kv-tokens", type=int, default=24576)
     ap.add_argument("--max-piggyback", type=int, default=64)
     ap.add_argument("--piggyback-reserve-us", type=float, default=100.0)

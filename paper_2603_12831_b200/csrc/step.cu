@@ -491,7 +491,7 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   CK(cudaStreamCreateWithPriority(&c->copy_st, cudaStreamNonBlocking, lo));
   c->marks.resize(64);
-  c->timers.resize(256);
+  c->timers.resize(8192);
   for (auto& e : c->marks) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : c->timers) CK(cudaEventCreate(&e));
   CK(cudaStreamSynchronize(c->st));
