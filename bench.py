@@ -353,7 +353,7 @@ def run_ours(args) -> None:
         dist.barrier()
     launches0 = step.ctx.lib.hs_launch_count()
     step.ctx.lib.hs_profile(step.ctx.h, 1)
-    prof = (C_double * 12)()
+    prof = (C_double * 16)()
     step.ctx.lib.hs_profile_read(step.ctx.h, prof, 1)
     h2d0, d2h0 = step.h2d_bytes, step.d2h_bytes
     with ClockSampler(local) as clocks:
@@ -372,7 +372,7 @@ def run_ours(args) -> None:
     iters = engine.iteration_log[it0:]
     m = window_metrics(engine, w0, w1)
     wall_s = w1 - w0
-    stats = np.array(list(prof), dtype=np.float64).reshape(3, 4)
+    stats = np.array(list(prof), dtype=np.float64).reshape(4, 4)
     tot = np.array([m["be_tokens"], m["ls_tokens"], device_s, wall_s, stats[0, 1], stats[0, 2],
                     stats[0, 0], stats[0, 3], launches], dtype=np.float64)
     if dist:
@@ -432,6 +432,11 @@ def run_ours(args) -> None:
         "slo_met": m["tpot_attainment"] >= 0.99,
         "merges": n_merges, "avg_batch_tokens": avg_rows,
         "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters) if iters else None,
+        "device_breakdown_ms": {"total": device_s * 1e3, "layers": stats[3, 1],
+                                "gemm": stats[0, 1], "decode_attn": stats[1, 1],
+                                "prefill_attn": stats[2, 1],
+                                "other_kernels": stats[3, 1] - stats[0, 1] - stats[1, 1] - stats[2, 1],
+                                "between_layers": device_s * 1e3 - stats[3, 1]},
         "roofline": roof,
         "e2e": {"value": e2e_val, "unit": UNIT,
                 "h2d_bytes_per_step": (step.h2d_bytes - h2d0) / max(args.steps, 1),

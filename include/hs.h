@@ -63,6 +63,12 @@ unsigned long long hs_launch_count(void);
  * n_out % 128 == 0, k % 64 == 0.  *splits_used <= max_splits. */
 int hs_op_gemm_bf16(const void* x, int tokens, int ldx, const void* w, int n_out, int k,
                     float* out_partial, int max_splits, int* splits_used, void* stream);
+/* Same product with the weights pre-tiled [n/128][k/64][128][64] (each
+ * 16 KB TMA box contiguous in HBM); hs_op_relayout_blocked converts. */
+int hs_op_relayout_blocked(const void* w, void* w_blocked, int n, int k, void* stream);
+int hs_op_gemm_bf16_blocked(const void* x, int tokens, int ldx, const void* w_blocked, int n_out,
+                            int k, float* out_partial, int max_splits, int* splits_used,
+                            void* stream);
 /* out[t][n] = sum_s part[s][t][n] */
 int hs_op_splitk_reduce(const float* part, int splits, int rows, int n, float* out,
                         void* stream);
@@ -235,10 +241,11 @@ int hs_timer(hs_ctx* ctx);
 int hs_timer_elapsed(hs_ctx* ctx, int a, int b, float* ms);
 /* Per-kernel-class device time and algorithmic work of the launches made
  * while profiling is on (CUDA events around each launch).  classes:
- * 0 = Dense GEMMs, 1 = decode attention (K1+K2), 2 = prefill attention.
+ * 0 = Dense GEMMs, 1 = decode attention (K1+K2), 2 = prefill attention,
+ * 3 = whole hs_layer spans (device time from a layer's first to last kernel).
  * stats[c] = {launches, milliseconds, bytes, flops}. */
 int hs_profile(hs_ctx* ctx, int on);
-int hs_profile_read(hs_ctx* ctx, double* stats /* [3][4] */, int reset);
+int hs_profile_read(hs_ctx* ctx, double* stats /* [4][4] */, int reset);
 /* Profiler probes on the context's own buffers and layer-0 weights (device
  * microseconds, median of reps): Dense modules over n rows; decode attention
  * of g requests with ctx keys each; causal prefill of q new tokens after

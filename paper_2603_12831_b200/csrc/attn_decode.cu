@@ -246,6 +246,7 @@ __global__ void decode_combine_kernel(const float* __restrict__ o_part,
                                       const int* __restrict__ row_chunk_begin, int rows, int n_q,
                                       int n_kv, bf16* __restrict__ out, int out_row_stride,
                                       float* __restrict__ lse_out) {
+  pdl_trigger();
   const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (pair >= rows * n_q) return;

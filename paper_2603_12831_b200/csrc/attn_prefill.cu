@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(kPreThreads)
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[kPreStages];
 
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
   const PrefillTile tile = tiles[blockIdx.x];

@@ -71,14 +71,42 @@ int hs_op_gemm_bf16(const void* x, int tokens, int ldx, const void* w, int n_out
     return HS_OK;
   }
   const int bn = gemm_pick_bn(tokens);
-  const int splits = gemm_pick_splits(n_out, k, tokens, bn, max_splits);
   CUtensorMap mw, mx;
   if (make_weight_map(&mw, static_cast<const bf16*>(w), n_out, k) != HS_OK ||
       make_act_map(&mx, static_cast<const bf16*>(x), tokens, k, ldx, bn) != HS_OK)
     return set_error(HS_E_CUDA, "gemm: cuTensorMapEncodeTiled failed");
-  if (splits_used) *splits_used = splits;
-  return cuda_status(gemm_launch(mw, mx, bn, out_partial, n_out, tokens, k, splits, S(stream)),
-                     "gemm");
+  int planes = 1;
+  const int rc = gemm_launch(mw, mx, bn, out_partial, n_out, tokens, k, max_splits, S(stream),
+                             &planes);
+  if (splits_used) *splits_used = planes;
+  return cuda_status(rc, "gemm");
+}
+
+int hs_op_relayout_blocked(const void* w, void* w_blocked, int n, int k, void* stream) {
+  return cuda_status(relayout_blocked(static_cast<const bf16*>(w), static_cast<bf16*>(w_blocked),
+                                      n, k, S(stream)),
+                     "relayout_blocked");
+}
+
+int hs_op_gemm_bf16_blocked(const void* x, int tokens, int ldx, const void* w_blocked, int n_out,
+                            int k, float* out_partial, int max_splits, int* splits_used,
+                            void* stream) {
+  if (tokens < 0 || n_out % 128 || k % 64 || ldx < k || max_splits < 1)
+    return set_error(HS_E_CONFIG, "gemm: bad shape tokens=%d n=%d k=%d", tokens, n_out, k);
+  if (tokens == 0) {
+    if (splits_used) *splits_used = 1;
+    return HS_OK;
+  }
+  const int bn = gemm_pick_bn(tokens);
+  CUtensorMap mw, mx;
+  if (make_weight_map_blocked(&mw, static_cast<const bf16*>(w_blocked), n_out, k) != HS_OK ||
+      make_act_map(&mx, static_cast<const bf16*>(x), tokens, k, ldx, bn) != HS_OK)
+    return set_error(HS_E_CUDA, "gemm: cuTensorMapEncodeTiled failed");
+  int planes = 1;
+  const int rc = gemm_launch(mw, mx, bn, out_partial, n_out, tokens, k, max_splits, S(stream),
+                             &planes, true);
+  if (splits_used) *splits_used = planes;
+  return cuda_status(rc, "gemm_blocked");
 }
 
 int hs_op_splitk_reduce(const float* part, int splits, int rows, int n, float* out,

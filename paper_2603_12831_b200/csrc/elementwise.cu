@@ -8,10 +8,49 @@
 
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "hs_common.cuh"
 #include "hs_internal.h"
 
+namespace cg = cooperative_groups;
+
 namespace hs {
+
+constexpr int kMaxSplits = 16;
+
+// Sum of `splits` fp32 split-K planes at p (plane stride in floats): all
+// loads are issued before the first add so the latency is paid once.
+__device__ __forceinline__ float4 sum_planes4(const float* __restrict__ p, size_t plane,
+                                              int splits) {
+  float4 v[kMaxSplits];
+#pragma unroll
+  for (int k = 0; k < kMaxSplits; ++k)
+    if (k < splits) v[k] = __ldg(reinterpret_cast<const float4*>(p + k * plane));
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < kMaxSplits; ++k)
+    if (k < splits) {
+      a.x += v[k].x;
+      a.y += v[k].y;
+      a.z += v[k].z;
+      a.w += v[k].w;
+    }
+  return a;
+}
+
+__device__ __forceinline__ float sum_planes1(const float* __restrict__ p, size_t plane,
+                                             int splits) {
+  float v[kMaxSplits];
+#pragma unroll
+  for (int k = 0; k < kMaxSplits; ++k)
+    if (k < splits) v[k] = __ldg(p + k * plane);
+  float a = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxSplits; ++k)
+    if (k < splits) a += v[k];
+  return a;
+}
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
@@ -41,23 +80,13 @@ int embed_gather(const int* tokens, int rows, const bf16* emb, int d, float* h, 
 }
 
 // ---------------------------------------------------------------- RMSNorm
-__global__ void rmsnorm_kernel(const float* __restrict__ h, int d, const float* __restrict__ w,
-                               float eps, bf16* __restrict__ out, int ld_out) {
-  __shared__ float red[32];
-  const int r = blockIdx.x;
-  const float* x = h + static_cast<size_t>(r) * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += x[i] * x[i];
-  const float inv = rsqrtf(block_sum(ss, red) / d + eps);
-  bf16* o = out + static_cast<size_t>(r) * ld_out;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = __float2bfloat16(x[i] * inv * w[i]);
-}
+// (the residual_add_norm cluster kernel with no partials to add; defined below)
+int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
+                      float eps, bf16* out, int ld_out, cudaStream_t st);
 
 int rmsnorm_rows(const float* h, int rows, int d, const float* w, float eps, bf16* out, int ld_out,
                  cudaStream_t st) {
-  if (rows <= 0) return HS_OK;
-  rmsnorm_kernel<<<rows, 256, 0, st>>>(h, d, w, eps, out, ld_out);
-  return launched();
+  return residual_add_norm(nullptr, 0, rows, d, const_cast<float*>(h), w, eps, out, ld_out, st);
 }
 
 // ---------------------------------------------------------------- split-K
@@ -80,30 +109,66 @@ int splitk_reduce(const float* part, int splits, int rows, int n, float* out, cu
 }
 
 // h += sum_s part[s]; out = rmsnorm(h) * w   (out may be null)
-__global__ void residual_add_norm_kernel(const float* __restrict__ part, int splits, int rows,
-                                         int d, float* __restrict__ h, const float* __restrict__ w,
-                                         float eps, bf16* __restrict__ out, int ld_out) {
+// One 8-CTA thread-block cluster per row: each CTA owns d/8 columns, the
+// row's sum of squares is reduced through distributed shared memory, so a
+// handful of rows still spreads over 8x as many SMs.
+constexpr int kNormCluster = 8;
+
+__global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
+    residual_add_norm_kernel(const float* __restrict__ part, int splits, int rows, int d,
+                             float* __restrict__ h, const float* __restrict__ w, float eps,
+                             bf16* __restrict__ out, int ld_out) {
   __shared__ float red[32];
-  const int r = blockIdx.x;
-  float* x = h + static_cast<size_t>(r) * d;
+  __shared__ float ssq_cta;
+  pdl_trigger();
+  cg::cluster_group cluster = cg::this_cluster();
+  const int r = blockIdx.y;
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int cols = d / kNormCluster;  // multiple of 4
+  const int c0 = rank * cols;
+  float* x = h + static_cast<size_t>(r) * d + c0;
   const size_t plane = static_cast<size_t>(rows) * d;
+  const float* pp = part + static_cast<size_t>(r) * d + c0;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float v = x[i];
-    for (int k = 0; k < splits; ++k) v += part[k * plane + static_cast<size_t>(r) * d + i];
-    x[i] = v;
-    ss += v * v;
+  for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<float4*>(x + i);
+    if (splits > 0) {
+      const float4 a = sum_planes4(pp + i, plane, splits);
+      v.x += a.x;
+      v.y += a.y;
+      v.z += a.z;
+      v.w += a.w;
+      *reinterpret_cast<float4*>(x + i) = v;
+    }
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   if (!out) return;
-  const float inv = rsqrtf(block_sum(ss, red) / d + eps);
-  bf16* o = out + static_cast<size_t>(r) * ld_out;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = __float2bfloat16(x[i] * inv * w[i]);
+  ss = block_sum(ss, red);
+  if (threadIdx.x == 0) ssq_cta = ss;
+  cluster.sync();
+  float total = 0.f;
+#pragma unroll
+  for (int k = 0; k < kNormCluster; ++k) total += *cluster.map_shared_rank(&ssq_cta, k);
+  cluster.sync();  // keep every CTA's smem alive until all ranks have read it
+  const float inv = rsqrtf(total / d + eps);
+  bf16* o = out + static_cast<size_t>(r) * ld_out + c0;
+  const float* wp = w + c0;
+  for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    const float4 g = *reinterpret_cast<const float4*>(wp + i);
+    uint2 pk;
+    pk.x = pack_bf16x2(v.x * inv * g.x, v.y * inv * g.y);
+    pk.y = pack_bf16x2(v.z * inv * g.z, v.w * inv * g.w);
+    *reinterpret_cast<uint2*>(o + i) = pk;
+  }
 }
 
 int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
                       float eps, bf16* out, int ld_out, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  residual_add_norm_kernel<<<rows, 256, 0, st>>>(part, splits, rows, d, h, w, eps, out, ld_out);
+  if (d % (4 * kNormCluster) || splits > kMaxSplits) return HS_E_CONFIG;
+  dim3 grid(kNormCluster, rows);
+  residual_add_norm_kernel<<<grid, 256, 0, st>>>(part, splits, rows, d, h, w, eps, out, ld_out);
   return launched();
 }
 
@@ -116,6 +181,8 @@ int residual_add_norm(const float* part, int splits, int rows, int d, float* h, 
 //           Piggybacking, reference engine.py:982-989 _chain_qkv)
 //   mode 2: q -> qbuf row, k/v -> ship slot (GPU attention of a row whose KV
 //           lives on the host is not used; reserved)
+// grid (rows, n_q + 2 n_kv): one block per (row, head), hd/2 threads; q and k
+// heads are rotated, v heads copied.
 __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int splits, int rows,
                                         int n_q, int n_kv, int hd,
                                         const float* __restrict__ rope_cos,
@@ -126,65 +193,38 @@ __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int spli
                                         int q_row_stride, bf16* __restrict__ kv_pool, KvGeom geom,
                                         int layer, const int* __restrict__ page_table,
                                         int pt_stride, bf16* __restrict__ ship, int ship_stride) {
-  const int r = blockIdx.x;
+  const int r = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
+  const int half = hd / 2;
   const int n_tot = (n_q + 2 * n_kv) * hd;
   const size_t plane = static_cast<size_t>(rows) * n_tot;
-  const float* src = part + static_cast<size_t>(r) * n_tot;
+  const int base = head * hd;
+  const float* src = part + static_cast<size_t>(r) * n_tot + base;
   const int pos = row_pos[r], slot = row_slot[r], mode = row_mode[r];
-  const int half = hd / 2;
-  const float* cs = rope_cos + static_cast<size_t>(pos) * half;
-  const float* sn = rope_sin + static_cast<size_t>(pos) * half;
-  bf16* kpage = nullptr;
-  bf16* vpage = nullptr;
-  if (mode == 0) {
+  const float x1 = sum_planes1(src + i, plane, splits);
+  const float x2 = sum_planes1(src + i + half, plane, splits);
+  bf16 y1, y2;
+  if (head < n_q + n_kv) {  // rotate q and k heads
+    const float c = rope_cos[static_cast<size_t>(pos) * half + i];
+    const float s = rope_sin[static_cast<size_t>(pos) * half + i];
+    y1 = __float2bfloat16(x1 * c - x2 * s);
+    y2 = __float2bfloat16(x2 * c + x1 * s);
+  } else {
+    y1 = __float2bfloat16(x1);
+    y2 = __float2bfloat16(x2);
+  }
+  bf16* dst;
+  if (mode == 1) {
+    dst = ship + static_cast<size_t>(slot) * ship_stride + base;
+  } else if (head < n_q) {
+    dst = qbuf + static_cast<size_t>(r) * q_row_stride + base;
+  } else {
+    const int kv = head < n_q + n_kv ? 0 : 1;
+    const int kh = head - n_q - kv * n_kv;
     const int phys = page_table[static_cast<size_t>(slot) * pt_stride + pos / kPageTokens];
-    const int t = pos % kPageTokens;
-    kpage = kv_pool + (kv_row(geom, layer, phys, 0, 0) + t) * hd;
-    vpage = kv_pool + (kv_row(geom, layer, phys, 1, 0) + t) * hd;
+    dst = kv_pool + (kv_row(geom, layer, phys, kv, kh) + pos % kPageTokens) * hd;
   }
-  bf16* shp = mode == 1 ? ship + static_cast<size_t>(slot) * ship_stride : nullptr;
-  // rotated pairs: q heads then k heads
-  const int n_pairs = (n_q + n_kv) * half;
-  for (int p = threadIdx.x; p < n_pairs; p += blockDim.x) {
-    const int head = p / half, i = p % half;
-    const int base = head * hd;
-    float x1 = 0.f, x2 = 0.f;
-    for (int k = 0; k < splits; ++k) {
-      x1 += src[k * plane + base + i];
-      x2 += src[k * plane + base + i + half];
-    }
-    const float c = cs[i], s = sn[i];
-    const bf16 y1 = __float2bfloat16(x1 * c - x2 * s);
-    const bf16 y2 = __float2bfloat16(x2 * c + x1 * s);
-    if (mode == 1) {
-      shp[base + i] = y1;
-      shp[base + i + half] = y2;
-    } else if (head < n_q) {
-      bf16* qd = qbuf + static_cast<size_t>(r) * q_row_stride + base;
-      qd[i] = y1;
-      qd[i + half] = y2;
-    } else {
-      // kv page row for head kh: rows of one (page, kv, head) block are
-      // contiguous; heads are 64 rows apart
-      const int kh = head - n_q;
-      bf16* kd = kpage + static_cast<size_t>(kh) * kPageTokens * hd;
-      kd[i] = y1;
-      kd[i + half] = y2;
-    }
-  }
-  // v heads (no rotation)
-  const int vbase = (n_q + n_kv) * hd;
-  for (int e = threadIdx.x; e < n_kv * hd; e += blockDim.x) {
-    float x = 0.f;
-    for (int k = 0; k < splits; ++k) x += src[k * plane + vbase + e];
-    const bf16 y = __float2bfloat16(x);
-    if (mode == 1) {
-      shp[vbase + e] = y;
-    } else {
-      const int kh = e / hd, i = e % hd;
-      vpage[static_cast<size_t>(kh) * kPageTokens * hd + i] = y;
-    }
-  }
+  dst[i] = y1;
+  dst[i + half] = y2;
 }
 
 int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv, int head_dim,
@@ -193,27 +233,26 @@ int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv,
                      bf16* kv_pool, const KvGeom& g, int layer, const int* page_table,
                      int pt_stride, bf16* ship, int ship_stride, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  qkv_rope_scatter_kernel<<<rows, 256, 0, st>>>(part, splits, rows, n_q, n_kv, head_dim, rope_cos,
-                                                rope_sin, row_pos, row_slot, row_mode, qbuf,
-                                                q_row_stride, kv_pool, g, layer, page_table,
-                                                pt_stride, ship, ship_stride);
+  if (splits > kMaxSplits) return HS_E_CONFIG;
+  dim3 grid(rows, n_q + 2 * n_kv);
+  qkv_rope_scatter_kernel<<<grid, head_dim / 2, 0, st>>>(
+      part, splits, rows, n_q, n_kv, head_dim, rope_cos, rope_sin, row_pos, row_slot, row_mode,
+      qbuf, q_row_stride, kv_pool, g, layer, page_table, pt_stride, ship, ship_stride);
   return launched();
 }
 
 // ---------------------------------------------------------------- SwiGLU
 __global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int rows, int ffn,
                                 bf16* __restrict__ act, int ld_act) {
+  pdl_trigger();
   const size_t plane = static_cast<size_t>(rows) * 2 * ffn;
   const size_t total = static_cast<size_t>(rows) * ffn;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t r = idx / ffn, i = idx % ffn;
     const float* src = part + r * 2 * ffn;
-    float gt = 0.f, up = 0.f;
-    for (int k = 0; k < splits; ++k) {
-      gt += src[k * plane + i];
-      up += src[k * plane + ffn + i];
-    }
+    const float gt = sum_planes1(src + i, plane, splits);
+    const float up = sum_planes1(src + ffn + i, plane, splits);
     const float s = gt / (1.f + __expf(-gt));
     act[r * ld_act + i] = __float2bfloat16(s * up);
   }
@@ -229,33 +268,41 @@ int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld
 }
 
 // ---------------------------------------------------------------- greedy argmax
-__global__ void argmax_kernel(const float* __restrict__ part, int splits, int rows, int vocab,
-                              int* __restrict__ tokens, float* __restrict__ logits_out) {
+// One 8-CTA cluster per row; each CTA scans a vocab slice, the cluster picks
+// the best (value, lowest index) through distributed shared memory.
+constexpr int kArgCluster = 8;
+
+__device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
+  if (v > bv || (v == bv && i < bi)) {
+    bv = v;
+    bi = i;
+  }
+}
+
+__global__ void __cluster_dims__(kArgCluster, 1, 1) __launch_bounds__(512)
+    argmax_kernel(const float* __restrict__ part, int splits, int rows, int vocab,
+                  int* __restrict__ tokens, float* __restrict__ logits_out) {
   __shared__ float sv[32];
   __shared__ int si[32];
-  const int r = blockIdx.x;
+  __shared__ float cta_v;
+  __shared__ int cta_i;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int r = blockIdx.y;
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int per = (vocab + kArgCluster - 1) / kArgCluster;
+  const int lo = rank * per, hi = min(vocab, lo + per);
   const size_t plane = static_cast<size_t>(rows) * vocab;
   const float* src = part + static_cast<size_t>(r) * vocab;
   float best = -CUDART_INF_F;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
-    float v = 0.f;
-    for (int k = 0; k < splits; ++k) v += src[k * plane + i];
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const float v = sum_planes1(src + i, plane, splits);
     if (logits_out) logits_out[static_cast<size_t>(r) * vocab + i] = v;
-    if (v > best || (v == best && i < bi)) {
-      best = v;
-      bi = i;
-    }
+    better(best, bi, v, i);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > best || (ov == best && oi < bi)) {
-      best = ov;
-      bi = oi;
-    }
-  }
+  for (int o = 16; o > 0; o >>= 1)
+    better(best, bi, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, bi, o));
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) {
     sv[w] = best;
@@ -263,20 +310,27 @@ __global__ void argmax_kernel(const float* __restrict__ part, int splits, int ro
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int nw = blockDim.x >> 5;
-    for (int i = 1; i < nw; ++i)
-      if (sv[i] > best || (sv[i] == best && si[i] < bi)) {
-        best = sv[i];
-        bi = si[i];
-      }
-    tokens[r] = bi;
+    for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) better(best, bi, sv[k], si[k]);
+    cta_v = best;
+    cta_i = bi;
   }
+  cluster.sync();
+  if (rank == 0 && threadIdx.x == 0) {
+    float v = cta_v;
+    int idx = cta_i;
+    for (int k = 1; k < kArgCluster; ++k)
+      better(v, idx, *cluster.map_shared_rank(&cta_v, k), *cluster.map_shared_rank(&cta_i, k));
+    tokens[r] = idx;
+  }
+  cluster.sync();
 }
 
 int argmax_rows(const float* part, int splits, int rows, int vocab, int* tokens, float* logits_out,
                 cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  argmax_kernel<<<rows, 512, 0, st>>>(part, splits, rows, vocab, tokens, logits_out);
+  if (splits > kMaxSplits) return HS_E_CONFIG;
+  dim3 grid(kArgCluster, rows);
+  argmax_kernel<<<grid, 512, 0, st>>>(part, splits, rows, vocab, tokens, logits_out);
   return launched();
 }
 

@@ -27,8 +27,14 @@ int make_weight_map(CUtensorMap* map, const bf16* w, int n_out, int k);
 int make_act_map(CUtensorMap* map, const bf16* x, int rows, int k, int ld, int bn);
 int gemm_pick_bn(int tokens);
 int gemm_pick_splits(int n_out, int k, int tokens, int bn, int max_splits);
+// Persistent stream-K GEMM; writes `*planes` (<= max_planes) fp32 partial
+// planes [planes][tokens][n_out] whose sum is the product.
 int gemm_launch(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,
-                int tokens, int k, int splits, cudaStream_t st);
+                int tokens, int k, int max_planes, cudaStream_t st, int* planes,
+                bool blocked = false);
+// weights pre-tiled [n/128][k/64][128][64] (see gemm_tcgen05.cu)
+int relayout_blocked(const bf16* src, bf16* dst, int n, int k, cudaStream_t st);
+int make_weight_map_blocked(CUtensorMap* map, const bf16* w, int n_out, int k);
 
 // ---- KV pool geometry ----
 // pool layout: [layers][pages][2 (K,V)][n_kv][64 tokens][head_dim] bf16

@@ -118,7 +118,7 @@ struct hs_ctx {
   struct Rec { int cls; cudaEvent_t a, b; double bytes, flops; };
   std::vector<Rec> prof_pending;
   std::vector<cudaEvent_t> prof_free;
-  double prof_stats[3][4] = {};
+  double prof_stats[4][4] = {};
   double dec_kv_tokens = 0, pre_units = 0, pre_kv_tokens = 0;
 };
 
@@ -250,9 +250,8 @@ int gemm(hs_ctx* c, const CUtensorMap& mw, const ActBuf& x, int tokens, int n_ou
   const size_t per_split = static_cast<size_t>(tokens) * n_out;
   const int cap = static_cast<int>(std::min<size_t>(16, c->part_floats / per_split));
   if (cap < 1) return set_error(HS_E_CAPACITY, "split-K buffer too small for %d x %d", tokens, n_out);
-  const int splits = gemm_pick_splits(n_out, k, tokens, bn, cap);
-  *splits_out = splits;
-  return gemm_launch(mw, x.maps[bn_index(bn)], bn, c->part, n_out, tokens, k, splits, c->st);
+  return gemm_launch(mw, x.maps[bn_index(bn)], bn, c->part, n_out, tokens, k, cap, c->st,
+                     splits_out);
 }
 
 int* stage(hs_ctx* c, size_t n) {
@@ -826,6 +825,7 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   cudaStream_t st = c->st;
   const int d_ = m.d, nqh = m.n_q * m.hd;
   int sp = 1;
+  ProfScope whole(c, 3, 0.0, 0.0);  // the layer's span on the device
   // carry rows: ship meta at [B, B+C)
   RC(upload(c, L.row_slot + B, d->carry_slot, C));
   RC(upload(c, L.row_pos + B, d->carry_pos, C));

@@ -42,6 +42,7 @@ __global__ void scatter_rows_f32_kernel(const float* __restrict__ src, const int
 __global__ void gather_rows_bf16_kernel(const bf16* __restrict__ src, int src_stride,
                                         const int* __restrict__ idx, int w, bf16* __restrict__ dst,
                                         int dst_stride) {
+  pdl_trigger();
   const int r = blockIdx.x;
   const int4* s = reinterpret_cast<const int4*>(src + static_cast<size_t>(idx[r]) * src_stride);
   int4* o = reinterpret_cast<int4*>(dst + static_cast<size_t>(r) * dst_stride);

@@ -262,3 +262,26 @@ def test_norms_embed_silu_argmax_merge(cuda):
     for r in range(rows):
         ref = O.lse_merge(parts[r].reshape(n_parts, n_q, hd), lse[r])
         assert _rel(got[r], ref) < 1.5e-2
+
+
+@pytest.mark.parametrize("tokens,n,k", [(1, 128, 64), (16, 6144, 4096), (77, 384, 512),
+                                        (300, 256, 1024)])
+def test_gemm_tcgen05_blocked_weights(cuda, tokens, n, k):
+    """Same GEMM with weights pre-tiled [n/128][k/64][128][64] (4-D TMA map)."""
+    import torch
+    from paper_2603_12831_b200 import _lib
+
+    rng = np.random.default_rng(tokens + n)
+    x = _bf16_np(rng, (tokens, k))
+    w = _bf16_np(rng, (n, k), 0.05)
+    xd, wd = _t(x, cuda, torch.bfloat16), _t(w, cuda, torch.bfloat16)
+    wb = torch.empty_like(wd)
+    _lib.call("hs_op_relayout_blocked", _p(wd), _p(wb), n, k, None)
+    part = torch.zeros(16 * tokens * n, dtype=torch.float32, device=cuda)
+    out = torch.zeros(tokens * n, dtype=torch.float32, device=cuda)
+    used = C.c_int(0)
+    _lib.call("hs_op_gemm_bf16_blocked", _p(xd), tokens, k, _p(wb), n, k, _p(part), 16,
+              C.byref(used), None)
+    _lib.call("hs_op_splitk_reduce", _p(part), used.value, tokens, n, _p(out), None)
+    torch.cuda.synchronize()
+    assert _rel(out.cpu().numpy().reshape(tokens, n), O.gemm(x, w)) < 1e-4

@@ -53,6 +53,8 @@ def main():
     toks = [1, 16, 64, 256] if quick else [1, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
     for name, (n, k) in shapes.items():
         w = (torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)
+        wb = torch.empty_like(w)
+        _lib.call("hs_op_relayout_blocked", p(w), p(wb), n, k, stream)
         for t in toks:
             x = torch.randn(t, k, device=dev).to(torch.bfloat16)
             part = torch.empty(16 * t * n, dtype=torch.float32, device=dev)
@@ -63,10 +65,18 @@ def main():
                           stream)
 
             sec = timed(run, flush=flush)
+
+            def run_b():
+                _lib.call("hs_op_gemm_bf16_blocked", p(x), t, k, p(wb), n, k, p(part), 16,
+                          C.byref(used), stream)
+
+            sec_b = timed(run_b, flush=flush)
             flops = 2.0 * t * n * k
             bytes_ = 2.0 * n * k + 2.0 * t * k + 4.0 * used.value * t * n
             print(json.dumps({"kernel": "gemm", "shape": name, "tokens": t, "splits": used.value,
-                              "us": sec * 1e6, "tflops": flops / sec / 1e12,
+                              "us": sec * 1e6, "us_blocked": sec_b * 1e6,
+                              "gbs_blocked": (2.0 * n * k + 2.0 * t * k) / sec_b / 1e9,
+                              "tflops": flops / sec / 1e12,
                               "gbs": bytes_ / sec / 1e9,
                               "hbm_frac": bytes_ / sec / 1e9 / PEAKS["hbm_gbs"],
                               "tensor_frac": flops / sec / 1e12 / PEAKS["bf16_tflops"]}),
