@@ -338,7 +338,7 @@ def run_ours(args) -> None:
             profiler.save(models, out, {"config": args.config, "how": "hs_probe_* on B200"})
     else:
         models = profiler.load(models_path)
-    engine = LiveEngine(scenario, models=models, step=step)
+    engine = LiveEngine(scenario, models=models, step=step, pace_layers=args.pace)
     prepopulate_be(engine, step, args.be_chains, args.seed + rank)
     if args.ls_decodes:
         prepopulate_ls(engine, step, args.ls_decodes, args.seed + rank)
@@ -347,8 +347,10 @@ def run_ours(args) -> None:
     arrivals = engine.admit_specs(build_requests(scenario.workload, 600.0))
     setup_s = time.perf_counter() - t_setup
     engine.t0 = time.perf_counter()
+    step.set_anchor(engine.clock())
     engine.run_live(max_iterations=args.warmup, arrivals=arrivals, idle_exit=False)
     step.ctx.sync()
+    engine.drain()
     if dist:
         dist.barrier()
     launches0 = step.ctx.lib.hs_launch_count()
@@ -359,19 +361,24 @@ def run_ours(args) -> None:
     with ClockSampler(local) as clocks:
         step.ctx.sync()
         tm0 = step.ctx.timer()
-        w0 = engine.clock()
+        w0 = host_w0 = engine.clock()
         it0 = len(engine.iteration_log)
         engine.run_live(max_iterations=args.steps, arrivals=arrivals, idle_exit=False)
         tm1 = step.ctx.timer()
         step.ctx.sync()
-        w1 = engine.clock()
+        engine.drain()
+        w1 = host_w1 = engine.clock()
     device_s = step.ctx.elapsed_ms(tm0, tm1) / 1e3
     launches = step.ctx.lib.hs_launch_count() - launches0
     step.ctx.lib.hs_profile_read(step.ctx.h, prof, 1)
     step.ctx.lib.hs_profile(step.ctx.h, 0)
     iters = engine.iteration_log[it0:]
+    # the window in engine time: from the completion of the last warm-up
+    # iteration to the completion of the last timed one
+    w0 = engine.iteration_log[it0 - 1]["end"] if it0 > 0 else w0
+    w1 = iters[-1]["end"] if iters else w1
     m = window_metrics(engine, w0, w1)
-    wall_s = w1 - w0
+    wall_s = host_w1 - host_w0
     stats = np.array(list(prof), dtype=np.float64).reshape(4, 4)
     tot = np.array([m["be_tokens"], m["ls_tokens"], device_s, wall_s, stats[0, 1], stats[0, 2],
                     stats[0, 0], stats[0, 3], launches], dtype=np.float64)
@@ -431,7 +438,8 @@ def run_ours(args) -> None:
         "ls_tokens": int(tot[1]), "be_tokens": int(tot[0]), "ls_gaps": m["ls_gaps"],
         "slo_met": m["tpot_attainment"] >= 0.99,
         "merges": n_merges, "avg_batch_tokens": avg_rows,
-        "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters) if iters else None,
+        "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters
+                                              if i.get("device_ms")) if iters else None,
         "device_breakdown_ms": {"total": device_s * 1e3, "layers": stats[3, 1],
                                 "gemm": stats[0, 1], "decode_attn": stats[1, 1],
                                 "prefill_attn": stats[2, 1],
@@ -481,6 +489,7 @@ def main() -> None:
     ap.add_argument("--max-piggyback", type=int, default=64)
     ap.add_argument("--piggyback-reserve-us", type=float, default=100.0)
     ap.add_argument("--max-rows", type=int, default=4096)
+    ap.add_argument("--pace", type=int, default=2, help="layers the host may run ahead")
     ap.add_argument("--calibrate", action="store_true")
     ap.add_argument("--calibrate-out", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")

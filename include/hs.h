@@ -233,6 +233,14 @@ int hs_swap_out_async(hs_ctx* ctx, int slot, int tokens, int* ticket);
 int hs_swap_in_async(hs_ctx* ctx, int slot, int tokens, int* ticket);
 /* 1 = done, 0 = in flight */
 int hs_swap_done(hs_ctx* ctx, int ticket);
+/* Pipelined iterations: hs_iter_end_async queues the token readback and an
+ * event and returns at once (the host plans the next iteration while this
+ * one runs); hs_iter_poll returns 1 with the tokens and the completion time
+ * in ms after the last hs_anchor() once the iteration has finished. */
+int hs_anchor(hs_ctx* ctx);
+int hs_iter_end_async(hs_ctx* ctx, int* ticket);
+int hs_iter_poll(hs_ctx* ctx, int ticket, int* tokens_out, int n, double* done_ms);
+int hs_iter_ntokens(hs_ctx* ctx, int ticket);
 /* stream marks for launch pacing, and timing events (CUDA events on the
  * compute stream; elapsed in ms between two timer ids) */
 int hs_mark(hs_ctx* ctx);

@@ -39,6 +39,8 @@ __global__ void __launch_bounds__(kDecThreads, 2)
                        const int* __restrict__ page_table, int pt_stride,
                        const DecodeChunk* __restrict__ chunks, float* __restrict__ o_part,
                        float* __restrict__ lse_part, float scale_log2) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   constexpr int kBoxBytes = kPageTokens * 128;
   constexpr int kHalf = (HD / 64) * kBoxBytes;  // K (or V) of one page
   constexpr int kStageBytes = 2 * kHalf;
@@ -246,6 +248,7 @@ __global__ void decode_combine_kernel(const float* __restrict__ o_part,
                                       const int* __restrict__ row_chunk_begin, int rows, int n_q,
                                       int n_kv, bf16* __restrict__ out, int out_row_stride,
                                       float* __restrict__ lse_out) {
+  pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -293,10 +296,9 @@ static int launch_decode(const CUtensorMap& kv_map, const KvGeom& g, int layer, 
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
   dim3 grid(n_chunks, g.n_kv);
-  decode_attn_kernel<HD><<<grid, kDecThreads, kSmem, st>>>(kv_map, g, layer, q, q_row_stride, n_q,
+  return launch_pdl(decode_attn_kernel<HD>, dim3(grid), dim3(kDecThreads), kSmem, st, kv_map, g, layer, q, q_row_stride, n_q,
                                                            pt, pt_stride, chunks, o_part, lse_part,
                                                            scale_log2);
-  return launched();
 }
 
 int decode_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
@@ -320,14 +322,12 @@ int decode_combine(const float* o_part, const float* lse_part, const int* row_ch
   if (rows <= 0) return HS_OK;
   const int blocks = (rows * n_q + 3) / 4;
   if (head_dim == 128)
-    decode_combine_kernel<128><<<blocks, 128, 0, st>>>(o_part, lse_part, row_chunk_begin, rows,
-                                                       n_q, n_kv, out, out_row_stride, lse_out);
-  else if (head_dim == 64)
-    decode_combine_kernel<64><<<blocks, 128, 0, st>>>(o_part, lse_part, row_chunk_begin, rows,
-                                                      n_q, n_kv, out, out_row_stride, lse_out);
-  else
-    return HS_E_CONFIG;
-  return launched();
+    return launch_pdl(decode_combine_kernel<128>, dim3(blocks), dim3(128), 0, st, o_part,
+                      lse_part, row_chunk_begin, rows, n_q, n_kv, out, out_row_stride, lse_out);
+  if (head_dim == 64)
+    return launch_pdl(decode_combine_kernel<64>, dim3(blocks), dim3(128), 0, st, o_part, lse_part,
+                      row_chunk_begin, rows, n_q, n_kv, out, out_row_stride, lse_out);
+  return HS_E_CONFIG;
 }
 
 }  // namespace hs

@@ -28,6 +28,8 @@ __global__ void __launch_bounds__(kPreThreads)
                         const int* __restrict__ page_table, int pt_stride,
                         const PrefillTile* __restrict__ tiles, bf16* __restrict__ out,
                         int out_row_stride, float scale_log2) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   constexpr int kBoxBytes = kPageTokens * 128;
   constexpr int kHalf = (HD / 64) * kBoxBytes;
   constexpr int kStageBytes = 2 * kHalf;
@@ -39,7 +41,6 @@ __global__ void __launch_bounds__(kPreThreads)
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[kPreStages];
 
-  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
   const PrefillTile tile = tiles[blockIdx.x];
@@ -208,10 +209,8 @@ static int launch_prefill(const CUtensorMap& kv_map, const KvGeom& g, int layer,
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
   dim3 grid(n_tiles, n_q);
-  prefill_attn_kernel<HD><<<grid, kPreThreads, kSmem, st>>>(
-      kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, tiles, out, out_row_stride,
+  return launch_pdl(prefill_attn_kernel<HD>, dim3(grid), dim3(kPreThreads), kSmem, st, kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, tiles, out, out_row_stride,
       scale_log2);
-  return launched();
 }
 
 int prefill_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,

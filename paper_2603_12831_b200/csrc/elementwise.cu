@@ -67,6 +67,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // ---------------------------------------------------------------- embedding
 __global__ void embed_kernel(const int* __restrict__ tokens, const bf16* __restrict__ emb, int d,
                              float* __restrict__ h) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   const int r = blockIdx.x;
   const bf16* src = emb + static_cast<size_t>(tokens[r]) * d;
   float* dst = h + static_cast<size_t>(r) * d;
@@ -75,8 +77,7 @@ __global__ void embed_kernel(const int* __restrict__ tokens, const bf16* __restr
 
 int embed_gather(const int* tokens, int rows, const bf16* emb, int d, float* h, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  embed_kernel<<<rows, 256, 0, st>>>(tokens, emb, d, h);
-  return launched();
+  return launch_pdl(embed_kernel, dim3(rows), dim3(256), 0, st, tokens, emb, d, h);
 }
 
 // ---------------------------------------------------------------- RMSNorm
@@ -92,6 +93,8 @@ int rmsnorm_rows(const float* h, int rows, int d, const float* w, float eps, bf1
 // ---------------------------------------------------------------- split-K
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, size_t total,
                                      float* __restrict__ out) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     float s = 0.f;
@@ -104,8 +107,7 @@ int splitk_reduce(const float* part, int splits, int rows, int n, float* out, cu
   const size_t total = static_cast<size_t>(rows) * n;
   if (!total) return HS_OK;
   const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, size_t(148 * 16)));
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(part, splits, total, out);
-  return launched();
+  return launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, part, splits, total, out);
 }
 
 // h += sum_s part[s]; out = rmsnorm(h) * w   (out may be null)
@@ -118,9 +120,10 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
     residual_add_norm_kernel(const float* __restrict__ part, int splits, int rows, int d,
                              float* __restrict__ h, const float* __restrict__ w, float eps,
                              bf16* __restrict__ out, int ld_out) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   __shared__ float red[32];
   __shared__ float ssq_cta;
-  pdl_trigger();
   cg::cluster_group cluster = cg::this_cluster();
   const int r = blockIdx.y;
   const int rank = static_cast<int>(cluster.block_rank());
@@ -168,8 +171,7 @@ int residual_add_norm(const float* part, int splits, int rows, int d, float* h, 
   if (rows <= 0) return HS_OK;
   if (d % (4 * kNormCluster) || splits > kMaxSplits) return HS_E_CONFIG;
   dim3 grid(kNormCluster, rows);
-  residual_add_norm_kernel<<<grid, 256, 0, st>>>(part, splits, rows, d, h, w, eps, out, ld_out);
-  return launched();
+  return launch_pdl(residual_add_norm_kernel, dim3(grid), dim3(256), 0, st, part, splits, rows, d, h, w, eps, out, ld_out);
 }
 
 // ---------------------------------------------------------------- QKV epilogue
@@ -193,6 +195,8 @@ __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int spli
                                         int q_row_stride, bf16* __restrict__ kv_pool, KvGeom geom,
                                         int layer, const int* __restrict__ page_table,
                                         int pt_stride, bf16* __restrict__ ship, int ship_stride) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   const int r = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
   const int half = hd / 2;
   const int n_tot = (n_q + 2 * n_kv) * hd;
@@ -235,15 +239,14 @@ int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv,
   if (rows <= 0) return HS_OK;
   if (splits > kMaxSplits) return HS_E_CONFIG;
   dim3 grid(rows, n_q + 2 * n_kv);
-  qkv_rope_scatter_kernel<<<grid, head_dim / 2, 0, st>>>(
-      part, splits, rows, n_q, n_kv, head_dim, rope_cos, rope_sin, row_pos, row_slot, row_mode,
+  return launch_pdl(qkv_rope_scatter_kernel, dim3(grid), dim3(head_dim / 2), 0, st, part, splits, rows, n_q, n_kv, head_dim, rope_cos, rope_sin, row_pos, row_slot, row_mode,
       qbuf, q_row_stride, kv_pool, g, layer, page_table, pt_stride, ship, ship_stride);
-  return launched();
 }
 
 // ---------------------------------------------------------------- SwiGLU
 __global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int rows, int ffn,
                                 bf16* __restrict__ act, int ld_act) {
+  pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const size_t plane = static_cast<size_t>(rows) * 2 * ffn;
   const size_t total = static_cast<size_t>(rows) * ffn;
@@ -263,8 +266,7 @@ int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld
   const size_t total = static_cast<size_t>(rows) * ffn;
   if (!total) return HS_OK;
   const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, size_t(148 * 16)));
-  silu_mul_kernel<<<blocks, 256, 0, st>>>(part, splits, rows, ffn, act, ld_act);
-  return launched();
+  return launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, st, part, splits, rows, ffn, act, ld_act);
 }
 
 // ---------------------------------------------------------------- greedy argmax
@@ -282,6 +284,8 @@ __device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
 __global__ void __cluster_dims__(kArgCluster, 1, 1) __launch_bounds__(512)
     argmax_kernel(const float* __restrict__ part, int splits, int rows, int vocab,
                   int* __restrict__ tokens, float* __restrict__ logits_out) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   __shared__ float sv[32];
   __shared__ int si[32];
   __shared__ float cta_v;
@@ -330,8 +334,7 @@ int argmax_rows(const float* part, int splits, int rows, int vocab, int* tokens,
   if (rows <= 0) return HS_OK;
   if (splits > kMaxSplits) return HS_E_CONFIG;
   dim3 grid(kArgCluster, rows);
-  argmax_kernel<<<grid, 512, 0, st>>>(part, splits, rows, vocab, tokens, logits_out);
-  return launched();
+  return launch_pdl(argmax_kernel, dim3(grid), dim3(512), 0, st, part, splits, rows, vocab, tokens, logits_out);
 }
 
 // ---------------------------------------------------------------- LSE merge
@@ -344,6 +347,8 @@ __global__ void lse_merge_kernel(const bf16* __restrict__ parts, const float* __
                                  int n_parts, int rows, int n_q, int part_stride,
                                  int row_stride_parts, bf16* __restrict__ out,
                                  int out_row_stride) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (pair >= rows * n_q) return;
@@ -376,14 +381,12 @@ int lse_merge_rows(const bf16* parts, const float* lse, int n_parts, int rows, i
   if (rows <= 0) return HS_OK;
   const int blocks = (rows * n_q + 3) / 4;
   if (head_dim == 128)
-    lse_merge_kernel<128><<<blocks, 128, 0, st>>>(parts, lse, n_parts, rows, n_q, part_stride,
-                                                  row_stride_parts, out, out_row_stride);
-  else if (head_dim == 64)
-    lse_merge_kernel<64><<<blocks, 128, 0, st>>>(parts, lse, n_parts, rows, n_q, part_stride,
-                                                 row_stride_parts, out, out_row_stride);
-  else
-    return HS_E_CONFIG;
-  return launched();
+    return launch_pdl(lse_merge_kernel<128>, dim3(blocks), dim3(128), 0, st, parts, lse, n_parts,
+                      rows, n_q, part_stride, row_stride_parts, out, out_row_stride);
+  if (head_dim == 64)
+    return launch_pdl(lse_merge_kernel<64>, dim3(blocks), dim3(128), 0, st, parts, lse, n_parts,
+                      rows, n_q, part_stride, row_stride_parts, out, out_row_stride);
+  return HS_E_CONFIG;
 }
 
 }  // namespace hs

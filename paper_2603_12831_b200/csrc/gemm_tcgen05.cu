@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();  // dependents may be scheduled; they wait for our completion
 
   if (warp == 0) {
     if (lane == 0) {

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/hs.h"
 
 typedef __nv_bfloat16 bf16;
@@ -18,6 +20,27 @@ extern unsigned long long g_launches;
 inline int launched() {
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 4;
+}
+
+// Launch with programmatic stream serialization: the kernel may be scheduled
+// while its predecessor drains; every libhs kernel begins with
+// griddepcontrol.wait (pdl_wait) before touching dependent memory and
+// triggers its own dependents right away.
+template <typename... KArgs, typename... Args>
+inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  return launched();
 }
 
 // ---- TMA maps / GEMM (gemm_tcgen05.cu) ----

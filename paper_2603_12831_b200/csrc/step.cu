@@ -110,6 +110,13 @@ struct hs_ctx {
   size_t swap_stage_elems = 0;
   std::map<int, cudaEvent_t> swap_ev;
   int next_ticket = 1;
+  // asynchronous iteration completion: ring of pinned token buffers + events
+  static constexpr int kIterRing = 8;
+  int* tok_ring = nullptr;  // pinned [kIterRing][2*max_rows]
+  cudaEvent_t iter_ev[kIterRing] = {};
+  int iter_n[kIterRing] = {};
+  int next_iter = 0;
+  cudaEvent_t anchor = nullptr;
   // marks (pacing) and timing events on the compute stream
   std::vector<cudaEvent_t> marks, timers;
   int next_mark = 0, next_timer = 0;
@@ -386,6 +393,10 @@ void free_all(hs_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->cpu) destroy_cpu_service(c->cpu);
   for (auto e : c->marks) cudaEventDestroy(e);
+  for (auto e : c->iter_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->anchor) cudaEventDestroy(c->anchor);
+  if (c->tok_ring) cudaFreeHost(c->tok_ring);
   for (auto e : c->prof_free) cudaEventDestroy(e);
   for (auto& r : c->prof_pending) {
     cudaEventDestroy(r.a);
@@ -489,6 +500,10 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
   int lo = 0, hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   CK(cudaStreamCreateWithPriority(&c->copy_st, cudaStreamNonBlocking, lo));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->tok_ring),
+                   sizeof(int) * hs_ctx::kIterRing * 2 * r.max_rows, cudaHostAllocDefault));
+  for (auto& e : c->iter_ev) CK(cudaEventCreate(&e));
+  CK(cudaEventCreate(&c->anchor));
   c->marks.resize(64);
   c->timers.resize(8192);
   for (auto& e : c->marks) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -928,6 +943,51 @@ int hs_iter_end(hs_ctx* c, int* tokens_out, int n) {
   RC(prof_collect(c));
   if (c->n_tok_out > 0) std::memcpy(tokens_out, c->tokens_pinned, c->n_tok_out * sizeof(int));
   return c->n_tok_out;
+}
+
+int hs_anchor(hs_ctx* c) {
+  CK(cudaEventRecord(c->anchor, c->st));
+  CK(cudaEventSynchronize(c->anchor));
+  return HS_OK;
+}
+
+int hs_iter_end_async(hs_ctx* c, int* ticket) {
+  const int id = c->next_iter;
+  const int slot = id % hs_ctx::kIterRing;
+  if (id >= hs_ctx::kIterRing) {  // the ring slot must have been consumed
+    const cudaError_t e = cudaEventQuery(c->iter_ev[slot]);
+    if (e == cudaErrorNotReady) CK(cudaEventSynchronize(c->iter_ev[slot]));
+  }
+  int* dst = c->tok_ring + static_cast<size_t>(slot) * 2 * c->r.max_rows;
+  if (c->n_tok_out > 0)
+    CK(cudaMemcpyAsync(dst, c->tok_out, c->n_tok_out * sizeof(int), cudaMemcpyDeviceToHost,
+                       c->st));
+  CK(cudaEventRecord(c->iter_ev[slot], c->st));
+  c->iter_n[slot] = c->n_tok_out;
+  *ticket = id;
+  c->next_iter = id + 1;
+  return HS_OK;
+}
+
+// 1 = done (tokens copied, *done_ms = completion time after the anchor), 0 = running
+int hs_iter_poll(hs_ctx* c, int ticket, int* tokens_out, int n, double* done_ms) {
+  if (ticket < c->next_iter - hs_ctx::kIterRing || ticket >= c->next_iter)
+    return set_error(HS_E_CONFIG, "iteration ticket %d out of window", ticket);
+  const int slot = ticket % hs_ctx::kIterRing;
+  const cudaError_t e = cudaEventQuery(c->iter_ev[slot]);
+  if (e == cudaErrorNotReady) return 0;
+  if (e != cudaSuccess) return set_error(HS_E_CUDA, "iteration: %s", cudaGetErrorString(e));
+  if (n < c->iter_n[slot]) return set_error(HS_E_CONFIG, "token buffer too small");
+  std::memcpy(tokens_out, c->tok_ring + static_cast<size_t>(slot) * 2 * c->r.max_rows,
+              c->iter_n[slot] * sizeof(int));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->anchor, c->iter_ev[slot]));
+  *done_ms = ms;
+  return 1;
+}
+
+int hs_iter_ntokens(hs_ctx* c, int ticket) {
+  return c->iter_n[ticket % hs_ctx::kIterRing];
 }
 
 int hs_cpu_attend(hs_ctx* c, const int* slots, const int* layers, const int* ctxs, int n) {

@@ -14,6 +14,8 @@ __global__ void select_tokens_kernel(const int* __restrict__ row_token,
                                      const int* __restrict__ row_slot,
                                      const int* __restrict__ last_token, int rows,
                                      int* __restrict__ tok) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const int t = row_token[r];
@@ -23,6 +25,8 @@ __global__ void select_tokens_kernel(const int* __restrict__ row_token,
 // dst[r] = src[idx[r]]  (fp32 rows of width d)
 __global__ void gather_rows_f32_kernel(const float* __restrict__ src, const int* __restrict__ idx,
                                        int d, float* __restrict__ dst) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   const int r = blockIdx.x;
   const float4* s = reinterpret_cast<const float4*>(src + static_cast<size_t>(idx[r]) * d);
   float4* o = reinterpret_cast<float4*>(dst + static_cast<size_t>(r) * d);
@@ -32,6 +36,8 @@ __global__ void gather_rows_f32_kernel(const float* __restrict__ src, const int*
 // dst[idx[r]] = src[r]
 __global__ void scatter_rows_f32_kernel(const float* __restrict__ src, const int* __restrict__ idx,
                                         int d, float* __restrict__ dst) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   const int r = blockIdx.x;
   const float4* s = reinterpret_cast<const float4*>(src + static_cast<size_t>(r) * d);
   float4* o = reinterpret_cast<float4*>(dst + static_cast<size_t>(idx[r]) * d);
@@ -42,6 +48,7 @@ __global__ void scatter_rows_f32_kernel(const float* __restrict__ src, const int
 __global__ void gather_rows_bf16_kernel(const bf16* __restrict__ src, int src_stride,
                                         const int* __restrict__ idx, int w, bf16* __restrict__ dst,
                                         int dst_stride) {
+  pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const int r = blockIdx.x;
   const int4* s = reinterpret_cast<const int4*>(src + static_cast<size_t>(idx[r]) * src_stride);
@@ -51,6 +58,8 @@ __global__ void gather_rows_bf16_kernel(const bf16* __restrict__ src, int src_st
 
 __global__ void scatter_tokens_kernel(const int* __restrict__ tok, const int* __restrict__ slot,
                                       int n, int* __restrict__ last_token) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) last_token[slot[i]] = tok[i];
 }
@@ -61,6 +70,8 @@ __global__ void scatter_tokens_kernel(const int* __restrict__ tok, const int* __
 template <bool kToHost>
 __global__ void kv_swap_kernel(bf16* __restrict__ pool, KvGeom g, const int* __restrict__ pages,
                                int tokens, bf16* __restrict__ host, int cap) {
+  pdl_wait();  // dependent data of the previous kernel is visible
+  pdl_trigger();
   // grid.x = layers*2*n_kv, grid.y = token tiles of 64
   const int lkh = blockIdx.x;
   const int h = lkh % g.n_kv;
@@ -86,36 +97,31 @@ __global__ void kv_swap_kernel(bf16* __restrict__ pool, KvGeom g, const int* __r
 int select_tokens(const int* row_token, const int* row_slot, const int* last_token, int rows,
                   int* tok, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  select_tokens_kernel<<<(rows + 127) / 128, 128, 0, st>>>(row_token, row_slot, last_token, rows,
+  return launch_pdl(select_tokens_kernel, dim3((rows + 127) / 128), dim3(128), 0, st, row_token, row_slot, last_token, rows,
                                                            tok);
-  return launched();
 }
 
 int gather_rows_f32(const float* src, const int* idx, int rows, int d, float* dst,
                     cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  gather_rows_f32_kernel<<<rows, 256, 0, st>>>(src, idx, d, dst);
-  return launched();
+  return launch_pdl(gather_rows_f32_kernel, dim3(rows), dim3(256), 0, st, src, idx, d, dst);
 }
 
 int scatter_rows_f32(const float* src, const int* idx, int rows, int d, float* dst,
                      cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  scatter_rows_f32_kernel<<<rows, 256, 0, st>>>(src, idx, d, dst);
-  return launched();
+  return launch_pdl(scatter_rows_f32_kernel, dim3(rows), dim3(256), 0, st, src, idx, d, dst);
 }
 
 int gather_rows_bf16(const bf16* src, int src_stride, const int* idx, int rows, int w, bf16* dst,
                      int dst_stride, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  gather_rows_bf16_kernel<<<rows, 128, 0, st>>>(src, src_stride, idx, w, dst, dst_stride);
-  return launched();
+  return launch_pdl(gather_rows_bf16_kernel, dim3(rows), dim3(128), 0, st, src, src_stride, idx, w, dst, dst_stride);
 }
 
 int scatter_tokens(const int* tok, const int* slot, int n, int* last_token, cudaStream_t st) {
   if (n <= 0) return HS_OK;
-  scatter_tokens_kernel<<<(n + 127) / 128, 128, 0, st>>>(tok, slot, n, last_token);
-  return launched();
+  return launch_pdl(scatter_tokens_kernel, dim3((n + 127) / 128), dim3(128), 0, st, tok, slot, n, last_token);
 }
 
 int kv_swap(bool to_host, bf16* pool, const KvGeom& g, const int* pages, int tokens, bf16* host,
@@ -123,10 +129,10 @@ int kv_swap(bool to_host, bf16* pool, const KvGeom& g, const int* pages, int tok
   if (tokens <= 0) return HS_OK;
   dim3 grid(g.layers * 2 * g.n_kv, (tokens + kPageTokens - 1) / kPageTokens);
   if (to_host)
-    kv_swap_kernel<true><<<grid, 256, 0, st>>>(pool, g, pages, tokens, host, cap);
-  else
-    kv_swap_kernel<false><<<grid, 256, 0, st>>>(pool, g, pages, tokens, host, cap);
-  return launched();
+    return launch_pdl(kv_swap_kernel<true>, grid, dim3(256), 0, st, pool, g, pages, tokens, host,
+                      cap);
+  return launch_pdl(kv_swap_kernel<false>, grid, dim3(256), 0, st, pool, g, pages, tokens, host,
+                    cap);
 }
 
 }  // namespace hs

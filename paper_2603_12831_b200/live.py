@@ -47,9 +47,10 @@ class LiveEngine(Engine):
         self._submitted: dict[str, object] = {}   # WorkItems in the CPU pool
         self._swaps: dict[int, tuple[str, str]] = {}
         self._swapin_wait: set[str] = set()
-        self._chain_token_marks: list[tuple[SimRequest, int]] = []
+        self._collect: Optional[list] = None  # tokens emitted by the iteration being launched
         self._dirty = True
         self.iteration_log: list[dict] = []
+        self._last_done = None
 
     def clock(self) -> float:
         return time.perf_counter() - self.t0
@@ -73,9 +74,14 @@ class LiveEngine(Engine):
 
     def _emit_token(self, req: SimRequest, t: float) -> None:
         super()._emit_token(req, t)
-        if self._iter is not None:
-            # chain token completed inside the iteration: stamp at its end
-            self._chain_token_marks.append((req, len(req.token_times) - 1))
+        if self._collect is not None:
+            # stamped with the iteration's device completion time once known
+            self._collect.append((req, len(req.token_times) - 1))
+
+    def _complete(self, req: SimRequest, t: float) -> None:
+        super()._complete(req, t)
+        if self._collect is not None:
+            self._collect.append((req, -1))
 
     # -- async completions ---------------------------------------------------------
 
@@ -131,7 +137,7 @@ class LiveEngine(Engine):
         it = IterationState(plan=plan, merge_cap=cap, start=self.now, layer=1, merges_total=0,
                             merge_layers={})
         self._iter = it
-        self._chain_token_marks = []
+        self._collect = []
         self.step.begin_iteration(plan)
         for layer in range(1, self.layers + 1):
             it.layer = layer
@@ -148,29 +154,38 @@ class LiveEngine(Engine):
             self._submit_shipped(self.step.layer(layer, outcomes))
             if self.opts.record_layer_times:
                 self.layer_start_log.append((it.start, layer, start))
-        self.step.end_iteration(plan)
-        self.now = end = self.clock()
-        chain_tokens = len(self._chain_token_marks)
-        for req, idx in self._chain_token_marks:
-            req.token_times[idx] = end
-            if req.first_token_time is not None and idx == 0:
-                req.first_token_time = end
-            if req.completion is not None:
-                req.completion = end
-        self._chain_token_marks = []
-        rec = {"start": it.start, "end": end, "decodes": len(plan.ls_decode) +
-               len(plan.be_decode_gpu), "ls_decodes": len(plan.ls_decode),
-               "be_gpu_decodes": len(plan.be_decode_gpu),
+        # Pipelined: queue the token readback and commit now; the host plans
+        # the next iteration while this one runs.  Token times are patched to
+        # the iteration's device completion time when it is polled.
+        rec = {"start": it.start, "decodes": len(plan.ls_decode) + len(plan.be_decode_gpu),
+               "ls_decodes": len(plan.ls_decode), "be_gpu_decodes": len(plan.be_decode_gpu),
                "chunk_tokens": sum(q for _, q in plan.ls_prefill_chunks + plan.be_prefill_chunks),
                "merges": it.merges_total, "batch_tokens": plan.loads.batch_tokens,
-               "chain_tokens": chain_tokens, "device_ms": self.step.last_device_ms}
-        self.iteration_log.append(rec)
-        self._log("iteration", **{k: v for k, v in rec.items() if k != "device_ms"})
+               "marks": self._collect}
+        self.step.end_iteration(plan, payload=rec)
         self._iter = None
         self.gpu_busy = False
+        self.now = self.clock()
         self._commit_iteration(plan)
+        self._collect = None
+        rec["chain_tokens"] = sum(1 for r, i in rec["marks"] if i >= 0 and r.cls.value == "BE")
+        self.iteration_log.append(rec)
         self._dirty = True
+        self._resolve_iterations()
         return True
+
+    def _resolve_iterations(self, block: bool = False) -> None:
+        for rec, t_done, _ in self.step.poll_iterations(block=block):
+            for req, idx in rec.pop("marks"):
+                if idx < 0:
+                    req.completion = t_done
+                    continue
+                req.token_times[idx] = t_done
+                if idx == 0:
+                    req.first_token_time = t_done
+            rec["end"] = t_done
+            rec["device_ms"] = (t_done - self._last_done) * 1e3 if self._last_done else None
+            self._last_done = t_done
 
     # -- main loop ------------------------------------------------------------------------
 
@@ -187,6 +202,8 @@ class LiveEngine(Engine):
                  arrivals: Optional[deque] = None, idle_exit: bool = True) -> int:
         """Serve until `max_iterations`, the horizon, or (idle_exit) no work
         is left.  Returns the number of iterations run."""
+        if self.step.anchor_wall == 0.0:
+            self.step.set_anchor(self.clock())
         if arrivals is None:
             arrivals = self.admit_specs(build_requests(self.scenario.workload,
                                                        horizon_s or self.scenario.horizon_s))
@@ -200,6 +217,7 @@ class LiveEngine(Engine):
                 self._on_arrival(arrivals.popleft())
                 self._dirty = True
             self._poll_async()
+            self._resolve_iterations()
             if self._dirty and self._runnable():
                 self._dirty = False
                 if self._live_iteration(self._plan()):
@@ -211,4 +229,8 @@ class LiveEngine(Engine):
                     and not self._swapin_wait and not self._runnable():
                 break
             time.sleep(2e-5)
+        self._resolve_iterations(block=True)
         return n
+
+    def drain(self) -> None:
+        self._resolve_iterations(block=True)

@@ -94,13 +94,17 @@ _CTX_SIGS = {
     "hs_swap_out_async": [C.c_void_p, C.c_int, C.c_int, _IP],
     "hs_swap_in_async": [C.c_void_p, C.c_int, C.c_int, _IP],
     "hs_swap_done": [C.c_void_p, C.c_int],
+    "hs_anchor": [C.c_void_p],
+    "hs_iter_end_async": [C.c_void_p, _IP],
+    "hs_iter_poll": [C.c_void_p, C.c_int, _IP, C.c_int, C.POINTER(C.c_double)],
+    "hs_iter_ntokens": [C.c_void_p, C.c_int],
     "hs_mark": [C.c_void_p],
     "hs_wait_mark": [C.c_void_p, C.c_int],
     "hs_timer": [C.c_void_p],
     "hs_timer_elapsed": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)],
 }
 _NONNEG_RETURNS = {"hs_iter_end", "hs_cpu_poll", "hs_cpu_in_flight", "hs_swap_done", "hs_mark",
-                   "hs_timer"}
+                   "hs_timer", "hs_iter_poll", "hs_iter_ntokens"}
 _lib._SIGNATURES.update(_CTX_SIGS)
 
 
@@ -273,6 +277,23 @@ class HsContext:
     def swap_done(self, ticket: int) -> bool:
         return self._call("hs_swap_done", ticket) == 1
 
+    def anchor(self) -> None:
+        self._call("hs_anchor")
+
+    def iter_end_async(self) -> int:
+        t = C.c_int(0)
+        self._call("hs_iter_end_async", C.byref(t))
+        return t.value
+
+    def iter_poll(self, ticket: int):
+        """(tokens, done_ms after the anchor) once finished, else None."""
+        ms = C.c_double(0)
+        rc = self._call("hs_iter_poll", ticket, _ip(self._tok), len(self._tok), C.byref(ms))
+        if rc == 0:
+            return None
+        n = self._call("hs_iter_ntokens", ticket)
+        return self._tok[:n].copy(), ms.value
+
     def mark(self) -> int:
         return self._call("hs_mark")
 
@@ -394,6 +415,9 @@ class CudaStep(LayerStep):
 
     def tokens_of(self, req) -> np.ndarray:
         """Prompt ids followed by generated ids (for recompute rebuilds)."""
+        need = req.prompt_len + req.rebuild_tokens
+        if need > req.prompt_len and len(self.generated.get(req.id, [])) < req.rebuild_tokens:
+            self.drain()  # tokens of in-flight iterations are needed now
         p = self.prompts.get(req.id)
         if p is None:
             p = self.prompts[req.id] = prompt_tokens(req.id, req.prompt_len, self.model.vocab,
@@ -540,6 +564,9 @@ class CudaStep(LayerStep):
             self.free_slots.append(s)
         self._pending_release.clear()
 
+    def drain(self) -> None:
+        """Synchronous steps have no iterations in flight."""
+
     def finish(self) -> None:
         self.ctx.sync()
         self._release_pending()
@@ -552,19 +579,21 @@ class LiveCudaStep(CudaStep):
     def __init__(self, *args, **kw):
         super().__init__(*args, **kw)
         self._marks: list[int] = []
-        self._t_begin = -1
         self.last_device_ms = 0.0
-        self.device_ms_total = 0.0
         self.swap_out_tickets: dict[int, str] = {}
+        self._inflight: list[tuple[int, list[str], object]] = []  # (ticket, reqs, payload)
+        self.anchor_wall = 0.0
 
-    def begin_iteration(self, plan) -> None:
-        super().begin_iteration(plan)
-        self._t_begin = self.ctx.timer()
-        self._marks = []
+    def set_anchor(self, wall: float) -> None:
+        """Device events are reported relative to this host time."""
+        self.ctx.anchor()
+        self.anchor_wall = wall
 
     def layer(self, layer: int, merges):
         shipped = super().layer(layer, merges)
         self._marks.append(self.ctx.mark())
+        if len(self._marks) > 64:
+            del self._marks[:-16]
         return shipped
 
     def pace(self, lag: int) -> None:
@@ -572,11 +601,35 @@ class LiveCudaStep(CudaStep):
         if len(self._marks) > lag:
             self.ctx.wait_mark(self._marks[-lag - 1])
 
-    def end_iteration(self, plan) -> None:
-        t_end = self.ctx.timer()
-        super().end_iteration(plan)
-        self.last_device_ms = self.ctx.elapsed_ms(self._t_begin, t_end)
-        self.device_ms_total += self.last_device_ms
+    def end_iteration(self, plan, payload=None) -> None:
+        """Queue the token readback; the iteration completes asynchronously."""
+        ticket = self.ctx.iter_end_async()
+        self._inflight.append((ticket, self._logit_reqs + self._merge_L, payload))
+        self.iterations += 1
+
+    def drain(self):
+        return self.poll_iterations(block=True)
+
+    def poll_iterations(self, block: bool = False):
+        """Finished iterations in order: [(payload, t_done_wall, tokens)]."""
+        out = []
+        while self._inflight:
+            ticket, reqs, payload = self._inflight[0]
+            res = self.ctx.iter_poll(ticket)
+            if res is None:
+                if not block:
+                    break
+                self.ctx.wait_mark(self._marks[-1]) if self._marks else self.ctx.sync()
+                continue
+            toks, ms = res
+            self._inflight.pop(0)
+            if len(toks) != len(reqs):
+                raise RuntimeError(f"libhs returned {len(toks)} tokens for {len(reqs)} rows")
+            self.d2h_bytes += 4 * len(toks)
+            for rid, t in zip(reqs, toks):
+                self.generated.setdefault(rid, []).append(int(t))
+            out.append((payload, self.anchor_wall + ms / 1e3, toks))
+        return out
 
     def cpu_submit(self, items) -> None:
         self.ctx.cpu_submit([self.slot_of(it.req_id) for it in items],
