@@ -52,6 +52,13 @@ int hs_device_ok(void);
 /* number of kernels libhs has launched in this process */
 unsigned long long hs_launch_count(void);
 
+/* C1 on the calling thread: decode attention of one row (q [n_q][hd] bf16)
+ * over K/V [n_kv][n_keys][hd] bf16 -> out [n_q][hd] bf16, lse [n_q] (natural
+ * log, may be NULL).  impl: 0 = best available, 1 = AVX-512-BF16, 2 = AVX2.
+ * Pure host code (no device needed). */
+int hs_host_attention(const void* q, const void* k, const void* v, int n_keys, int n_q, int n_kv,
+                      int head_dim, void* out, float* lse, int impl);
+
 /* -------------------------------------------------------------- op level
  * Single-kernel entry points over caller-owned device buffers.  They are the
  * building blocks of hs_layer() below and are exported so parity tests can

@@ -42,6 +42,7 @@ _SIGNATURES: dict[str, list] = {
     "hs_op_silu_mul": [_fp, _i, _i, _i, _vp, _i, _vp],
     "hs_op_argmax": [_fp, _i, _i, _i, _ip, _fp, _vp],
     "hs_op_lse_merge": [_vp, _fp, _i, _i, _i, _i, _i, _i, _vp, _i, _vp],
+    "hs_host_attention": [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _fp, _i],
 }
 
 _lib = None

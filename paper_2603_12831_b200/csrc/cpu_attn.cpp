@@ -178,6 +178,21 @@ static void attend_head(const ModelCfg& m, const uint16_t* q, const uint16_t* K,
   }
 }
 
+void attend_group_avx512(int G, int hd, const uint16_t* q, const uint16_t* K, const uint16_t* V,
+                         int n_keys, uint16_t* out, float* lse);
+bool cpu_has_avx512bf16();
+
+// AVX-512-BF16 when the host has it (cpu_attn_avx512.cpp), else AVX2/FMA.
+static void attend_dispatch(const ModelCfg& m, const uint16_t* q, const uint16_t* K,
+                            const uint16_t* V, int n_keys, uint16_t* out, float* lse,
+                            bool allow_avx512 = true) {
+  const int G = m.n_q / m.n_kv;
+  if (allow_avx512 && cpu_has_avx512bf16() && (m.hd == 64 || m.hd == 128) && G <= 16)
+    attend_group_avx512(G, m.hd, q, K, V, n_keys, out, lse);
+  else
+    attend_head(m, q, K, V, n_keys, out, lse);
+}
+
 void cpu_attend_head(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int cap, int layer,
                      int ctx, int h, bf16* out_row, float* lse_out) {
   const int hd = m.hd, G = m.n_q / m.n_kv;
@@ -191,9 +206,9 @@ void cpu_attend_head(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int
   uint16_t* V = base + ((static_cast<size_t>(layer) * 2 + 1) * m.n_kv + h) * cap * hd;
   std::memcpy(K + static_cast<size_t>(ctx) * hd, k_new, hd * 2);
   std::memcpy(V + static_cast<size_t>(ctx) * hd, v_new, hd * 2);
-  attend_head(m, q, K, V, ctx + 1,
-              reinterpret_cast<uint16_t*>(out_row) + static_cast<size_t>(h) * G * hd,
-              lse_out ? lse_out + h * G : nullptr);
+  attend_dispatch(m, q, K, V, ctx + 1,
+                  reinterpret_cast<uint16_t*>(out_row) + static_cast<size_t>(h) * G * hd,
+                  lse_out ? lse_out + h * G : nullptr);
 }
 
 void cpu_attend_one(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int cap, int layer,
@@ -203,3 +218,27 @@ void cpu_attend_one(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int 
 }
 
 }  // namespace hs
+
+using namespace hs;
+
+extern "C" int hs_host_attention(const void* q, const void* k, const void* v, int n_keys, int n_q,
+                                 int n_kv, int head_dim, void* out, float* lse, int impl) {
+  if (n_keys < 1 || n_q % n_kv || n_q / n_kv > 16 || (head_dim != 64 && head_dim != 128))
+    return set_error(HS_E_CONFIG, "host attention: unsupported shape");
+  if (impl == 1 && !cpu_has_avx512bf16())
+    return set_error(HS_E_CONFIG, "host attention: no AVX-512-BF16 on this CPU");
+  ModelCfg m{};
+  m.n_q = n_q;
+  m.n_kv = n_kv;
+  m.hd = head_dim;
+  const int G = n_q / n_kv;
+  for (int h = 0; h < n_kv; ++h) {
+    const size_t kv_off = static_cast<size_t>(h) * n_keys * head_dim;
+    const uint16_t* qh = static_cast<const uint16_t*>(q) + static_cast<size_t>(h) * G * head_dim;
+    uint16_t* oh = static_cast<uint16_t*>(out) + static_cast<size_t>(h) * G * head_dim;
+    attend_dispatch(m, qh, static_cast<const uint16_t*>(k) + kv_off,
+                    static_cast<const uint16_t*>(v) + kv_off, n_keys, oh, lse ? lse + h * G : nullptr,
+                    impl != 2);
+  }
+  return HS_OK;
+}

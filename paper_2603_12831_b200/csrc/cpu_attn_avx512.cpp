@@ -1,0 +1,167 @@
+// C1 fast path: BE decode attention on AVX-512-BF16 host cores.
+//
+// QK^T: vdpbf16ps on the bf16 q and K rows (32 MACs per instruction); the
+// per-key partial vectors of a 16-key tile are transpose-reduced into one
+// 16-lane score vector.  PV: two keys at a time, their V rows interleaved
+// (unpacklo/hi_epi16) into bf16 pairs and multiplied by the pair of softmax
+// weights with vdpbf16ps — the same bf16 rounding of P the GPU kernel uses.
+// Online softmax across tiles with a vectorised exp2.  Layout: one request's
+// K (or V) for one layer and KV head is contiguous [keys][hd] (host KV arena,
+// DESIGN.md §4).
+#include <immintrin.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "hs_step.h"
+
+#define HS_AVX512 __attribute__((target("avx512f,avx512bw,avx512vl,avx512dq,avx512bf16")))
+
+namespace hs {
+
+namespace {
+
+HS_AVX512 inline __m512 exp2_ps(__m512 x) {
+  // 2^x = 2^n * 2^f, f in [-0.5, 0.5]; degree-6 minimax polynomial
+  x = _mm512_max_ps(x, _mm512_set1_ps(-126.f));
+  const __m512 n = _mm512_roundscale_ps(x, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+  const __m512 f = _mm512_sub_ps(x, n);
+  __m512 p = _mm512_set1_ps(1.5353362e-4f);
+  p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(1.3398874e-3f));
+  p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(9.6180573e-3f));
+  p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(5.5503324e-2f));
+  p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(2.4022652e-1f));
+  p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(6.9314718e-1f));
+  p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(1.0f));
+  const __m512i e = _mm512_slli_epi32(_mm512_add_epi32(_mm512_cvtps_epi32(n), _mm512_set1_epi32(127)), 23);
+  return _mm512_mul_ps(p, _mm512_castsi512_ps(e));
+}
+
+// v[t] (16 vectors of 16 partial sums) -> r[t] = sum of v[t]'s lanes.
+HS_AVX512 inline __m512 transpose_reduce16(const __m512* v) {
+  __m512 w[8], x[4], y[2];
+  for (int k = 0; k < 8; ++k)
+    w[k] = _mm512_add_ps(_mm512_shuffle_f32x4(v[2 * k], v[2 * k + 1], 0x44),
+                         _mm512_shuffle_f32x4(v[2 * k], v[2 * k + 1], 0xEE));
+  for (int k = 0; k < 4; ++k)
+    x[k] = _mm512_add_ps(_mm512_shuffle_f32x4(w[2 * k], w[2 * k + 1], 0x88),
+                         _mm512_shuffle_f32x4(w[2 * k], w[2 * k + 1], 0xDD));
+  for (int k = 0; k < 2; ++k)
+    y[k] = _mm512_add_ps(_mm512_shuffle_ps(x[2 * k], x[2 * k + 1], 0x88),
+                         _mm512_shuffle_ps(x[2 * k], x[2 * k + 1], 0xDD));
+  const __m512 z = _mm512_add_ps(_mm512_shuffle_ps(y[0], y[1], 0x88),
+                                 _mm512_shuffle_ps(y[0], y[1], 0xDD));
+  // lane 4i+j of z holds key i+4j: permute to key order
+  const __m512i idx = _mm512_setr_epi32(0, 4, 8, 12, 1, 5, 9, 13, 2, 6, 10, 14, 3, 7, 11, 15);
+  return _mm512_permutexvar_ps(idx, z);
+}
+
+inline uint16_t f2bf_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+constexpr int kMaxG = 16;
+
+}  // namespace
+
+// q: [G][hd] bf16 (one GQA group), K/V: [n_keys][hd] bf16 -> out [G][hd] bf16,
+// lse [G] (natural log, optional).  hd in {64, 128}.
+HS_AVX512 void attend_group_avx512(int G, int hd, const uint16_t* q, const uint16_t* K,
+                                   const uint16_t* V, int n_keys, uint16_t* out, float* lse) {
+  const int C = hd / 32;  // 32-bf16 chunks per row
+  const float scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(hd));
+  __m512bh qb[kMaxG][4];
+  for (int g = 0; g < G; ++g)
+    for (int c = 0; c < C; ++c)
+      qb[g][c] = reinterpret_cast<__m512bh>(_mm512_loadu_si512(q + g * hd + 32 * c));
+  alignas(64) float acc_lo[kMaxG][4][16], acc_hi[kMaxG][4][16];
+  std::memset(acc_lo, 0, sizeof(acc_lo));
+  std::memset(acc_hi, 0, sizeof(acc_hi));
+  float m[kMaxG], den[kMaxG];
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    den[g] = 0.f;
+  }
+  __m512 part[kMaxG][16];
+  alignas(64) uint32_t ppair[kMaxG][8];
+  for (int t0 = 0; t0 < n_keys; t0 += 16) {
+    const int nt = n_keys - t0 < 16 ? n_keys - t0 : 16;
+    // ---- scores of 16 keys for every head of the group
+    for (int t = 0; t < 16; ++t) {
+      if (t < nt) {
+        const uint16_t* kr = K + static_cast<size_t>(t0 + t) * hd;
+        __m512bh kc[4];
+        for (int c = 0; c < C; ++c)
+          kc[c] = reinterpret_cast<__m512bh>(_mm512_loadu_si512(kr + 32 * c));
+        for (int g = 0; g < G; ++g) {
+          __m512 a = _mm512_dpbf16_ps(_mm512_setzero_ps(), qb[g][0], kc[0]);
+          for (int c = 1; c < C; ++c) a = _mm512_dpbf16_ps(a, qb[g][c], kc[c]);
+          part[g][t] = a;
+        }
+      } else {
+        for (int g = 0; g < G; ++g) part[g][t] = _mm512_setzero_ps();
+      }
+    }
+    const __mmask16 valid = static_cast<__mmask16>((1u << nt) - 1u);
+    for (int g = 0; g < G; ++g) {
+      __m512 s = _mm512_mul_ps(transpose_reduce16(part[g]), _mm512_set1_ps(scale_log2));
+      s = _mm512_mask_blend_ps(valid, _mm512_set1_ps(-INFINITY), s);
+      const float tmax = _mm512_reduce_max_ps(s);
+      const float nm = m[g] > tmax ? m[g] : tmax;
+      const float corr = std::exp2(m[g] - nm);
+      m[g] = nm;
+      const __m512 p = _mm512_maskz_mov_ps(valid, exp2_ps(_mm512_sub_ps(s, _mm512_set1_ps(nm))));
+      den[g] = den[g] * corr + _mm512_reduce_add_ps(p);
+      if (corr != 1.f) {
+        const __m512 cv = _mm512_set1_ps(corr);
+        for (int c = 0; c < C; ++c) {
+          _mm512_store_ps(acc_lo[g][c], _mm512_mul_ps(_mm512_load_ps(acc_lo[g][c]), cv));
+          _mm512_store_ps(acc_hi[g][c], _mm512_mul_ps(_mm512_load_ps(acc_hi[g][c]), cv));
+        }
+      }
+      // P as bf16 pairs (key 2k, key 2k+1)
+      const __m256bh pb = _mm512_cvtneps_pbh(p);
+      _mm256_store_si256(reinterpret_cast<__m256i*>(ppair[g]), reinterpret_cast<__m256i>(pb));
+    }
+    // ---- PV, two keys at a time
+    for (int k = 0; 2 * k < nt; ++k) {
+      const int ta = t0 + 2 * k;
+      const uint16_t* va = V + static_cast<size_t>(ta) * hd;
+      const uint16_t* vb = 2 * k + 1 < nt ? va + hd : nullptr;
+      for (int c = 0; c < C; ++c) {
+        const __m512i a = _mm512_loadu_si512(va + 32 * c);
+        const __m512i b = vb ? _mm512_loadu_si512(vb + 32 * c) : _mm512_setzero_si512();
+        const __m512bh lo = reinterpret_cast<__m512bh>(_mm512_unpacklo_epi16(a, b));
+        const __m512bh hi = reinterpret_cast<__m512bh>(_mm512_unpackhi_epi16(a, b));
+        for (int g = 0; g < G; ++g) {
+          const __m512bh pp = reinterpret_cast<__m512bh>(_mm512_set1_epi32(
+              static_cast<int>(ppair[g][k])));
+          _mm512_store_ps(acc_lo[g][c], _mm512_dpbf16_ps(_mm512_load_ps(acc_lo[g][c]), lo, pp));
+          _mm512_store_ps(acc_hi[g][c], _mm512_dpbf16_ps(_mm512_load_ps(acc_hi[g][c]), hi, pp));
+        }
+      }
+    }
+  }
+  // un-permute: acc_lo[c] lane 4L+j -> dim 32c + 8L + j, acc_hi -> +4
+  for (int g = 0; g < G; ++g) {
+    const float inv = 1.f / den[g];
+    for (int c = 0; c < C; ++c)
+      for (int L = 0; L < 4; ++L)
+        for (int j = 0; j < 4; ++j) {
+          out[g * hd + 32 * c + 8 * L + j] = f2bf_rne(acc_lo[g][c][4 * L + j] * inv);
+          out[g * hd + 32 * c + 8 * L + 4 + j] = f2bf_rne(acc_hi[g][c][4 * L + j] * inv);
+        }
+    if (lse) lse[g] = (m[g] + std::log2(den[g])) * 0.69314718055994530942f;
+  }
+}
+
+bool cpu_has_avx512bf16() {
+  static const int ok = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+                        __builtin_cpu_supports("avx512bf16");
+  return ok;
+}
+
+}  // namespace hs

@@ -1,0 +1,49 @@
+"""C1 host attention (CPU, no GPU needed): AVX-512-BF16 and AVX2 paths of
+the piggyback CPU worker against the numpy oracle, incl. ragged key counts
+(tile tails of 1..15 keys) and every GQA group size used by the configs."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import llama_ops as O
+
+
+def _run(q, k, v, n_q, n_kv, hd, impl):
+    from paper_2603_12831_b200 import _lib
+
+    lib = _lib.load()
+    qb, kb, vb = (np.ascontiguousarray(O.bf16_bits(x)) for x in (q, k, v))
+    out = np.zeros(n_q * hd, np.uint16)
+    lse = np.zeros(n_q, np.float32)
+    rc = lib.hs_host_attention(qb.ctypes.data_as(C.c_void_p), kb.ctypes.data_as(C.c_void_p),
+                               vb.ctypes.data_as(C.c_void_p), k.shape[1], n_q, n_kv, hd,
+                               out.ctypes.data_as(C.c_void_p), lse.ctypes.data_as(C.c_void_p),
+                               impl)
+    _lib.check(rc, "hs_host_attention")
+    return O.from_bf16_bits(out).reshape(n_q, hd), lse
+
+
+def _has_avx512bf16() -> bool:
+    try:
+        return "avx512_bf16" in open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+
+
+@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("n_q,n_kv,hd", [(32, 8, 128), (4, 2, 64), (40, 40, 128), (8, 1, 128)])
+@pytest.mark.parametrize("keys", [1, 15, 16, 17, 63, 300])
+def test_host_attention_matches_oracle(impl, n_q, n_kv, hd, keys):
+    if impl == 1 and not _has_avx512bf16():
+        pytest.skip("no AVX-512-BF16 on this host")
+    rng = np.random.default_rng(keys * 7 + n_q + impl)
+    q = O.to_bf16(rng.standard_normal((n_q, hd)).astype(np.float32))
+    k = O.to_bf16(rng.standard_normal((n_kv, keys, hd)).astype(np.float32))
+    v = O.to_bf16(rng.standard_normal((n_kv, keys, hd)).astype(np.float32))
+    got, lse = _run(q, k, v, n_q, n_kv, hd, impl)
+    ref, ref_lse = O.decode_attention(q, k.transpose(1, 0, 2), v.transpose(1, 0, 2), n_kv)
+    err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-6)
+    assert err < 1.5e-2, err
+    assert np.abs(lse - ref_lse).max() < 1e-2
