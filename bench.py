@@ -121,7 +121,7 @@ def scenario_doc(args, cores: int) -> dict:
     }
 
 
-def prepopulate_be(engine, step, n: int, seed: int) -> list:
+def prepopulate_be(engine, step, n: int, seed: int, start: int = 0) -> list:
     """Saturating BE decode backlog already offloaded to host DRAM: each
     request has finished prefill (token 1 emitted) and its chain is injected
     (the state _finish_swap_out leaves, reference engine.py:437-454)."""
@@ -130,28 +130,47 @@ def prepopulate_be(engine, step, n: int, seed: int) -> list:
 
     pairs = longbench_like(seed=1).pairs
     out = []
-    for i in range(n):
+    for i in range(start, start + n):
         p, o = pairs[(seed * 7919 + i) % len(pairs)]
-        spec = RequestSpec(f"BE-{i:05d}", ServiceClass.BE, p, max(o, 8), 0.0)
+        spec = RequestSpec(f"BE-{i:05d}", ServiceClass.BE, p, max(o, 8), engine.now)
         r = SimRequest(spec)
         engine.requests[r.id] = r
         r.admitted = True
         r.phase = "decode"
         r.prefill_done = p
         r.tokens_out = 1
-        r.token_times = [0.0]
-        r.first_token_time = 0.0
+        r.token_times = [engine.now]
+        r.first_token_time = engine.now
         need = r.prompt_len + r.output_len - r.tokens_out + 1
         engine.kv.alloc_host(0, need)
         r.swap_reserved = need
         r.kv_place = 0
         r.kv_held = r.ctx
-        r.placement_log = [(0.0, "cpu0")]
+        r.placement_log = [(engine.now, "cpu0")]
         slot = step.slot_of(r.id)
         step.ctx.host_kv_reserve(slot, r.prompt_len + r.output_len + 1)
         engine._inject(r)
         out.append(r)
     return out
+
+
+class BeBacklog:
+    """Keeps `n` BE requests live: every completed one is replaced by a new
+    host-resident request (a stationary saturating backlog)."""
+
+    def __init__(self, engine, step, n: int, seed: int):
+        self.engine, self.step, self.n, self.seed = engine, step, n, seed
+        self.next_id = n
+        self.live = prepopulate_be(engine, step, n, seed)
+
+    def __call__(self, _it: int) -> None:
+        alive = [r for r in self.live if r.phase != "done"]
+        short = self.n - len(alive)
+        if short > 0:
+            alive += prepopulate_be(self.engine, self.step, short, self.seed, self.next_id)
+            self.next_id += short
+            self.engine._dirty = True
+        self.live = alive
 
 
 def prepopulate_ls(engine, step, n: int, seed: int) -> list:
@@ -339,7 +358,7 @@ def run_ours(args) -> None:
     else:
         models = profiler.load(models_path)
     engine = LiveEngine(scenario, models=models, step=step, pace_layers=args.pace)
-    prepopulate_be(engine, step, args.be_chains, args.seed + rank)
+    backlog = BeBacklog(engine, step, args.be_chains, args.seed + rank)
     if args.ls_decodes:
         prepopulate_ls(engine, step, args.ls_decodes, args.seed + rank)
     from paper_2603_12831_b200.workload import build_requests
@@ -348,7 +367,8 @@ def run_ours(args) -> None:
     setup_s = time.perf_counter() - t_setup
     engine.t0 = time.perf_counter()
     step.set_anchor(engine.clock())
-    engine.run_live(max_iterations=args.warmup, arrivals=arrivals, idle_exit=False)
+    engine.run_live(max_iterations=args.warmup, arrivals=arrivals, idle_exit=False,
+                    on_iteration=backlog)
     step.ctx.sync()
     engine.drain()
     if dist:
@@ -363,7 +383,8 @@ def run_ours(args) -> None:
         tm0 = step.ctx.timer()
         w0 = host_w0 = engine.clock()
         it0 = len(engine.iteration_log)
-        engine.run_live(max_iterations=args.steps, arrivals=arrivals, idle_exit=False)
+        engine.run_live(max_iterations=args.steps, arrivals=arrivals, idle_exit=False,
+                        on_iteration=backlog)
         tm1 = step.ctx.timer()
         step.ctx.sync()
         engine.drain()
@@ -429,7 +450,8 @@ def run_ours(args) -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights, synthetic KV, Poisson LS trace)",
         "config": {"workload": "llama3-8b live serving: Poisson LS (sharegpt, TPOT SLO 50 ms) + "
-                               f"{args.be_chains} host-resident BE decode chains (longbench)",
+                               f"{args.be_chains} host-resident BE decodes kept live (longbench; "
+                               "completed ones replaced by new prefilled requests)",
                    "model": args.config, "ls_rate_per_s": args.ls_rate,
                    "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
                    "cpu_threads_per_replica": rt.cpu_threads, "parallelism": f"replicas x{world}",
@@ -477,8 +499,8 @@ def main() -> None:
     C_double = ctypes.c_double
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=320)
-    ap.add_argument("--warmup", type=int, default=96)
+    ap.add_argument("--steps", type=int, default=640)
+    ap.add_argument("--warmup", type=int, default=128)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama3-8b")
     ap.add_argument("--seed", type=int, default=0)

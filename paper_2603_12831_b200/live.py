@@ -45,6 +45,12 @@ class LiveEngine(Engine):
         self.pace_layers = pace_layers
         self._unshipped: dict[str, object] = {}   # WorkItems awaiting their ship launch
         self._submitted: dict[str, object] = {}   # WorkItems in the CPU pool
+        # results enter the output FIFO in submission order (a reorder
+        # buffer): the reference services a host queue as one batch whose
+        # results arrive together in item order (engine.py:546-554), which the
+        # FIFO head-run merge rule (engine.py:902-919) relies on
+        self._order: deque = deque()
+        self._finished: set[str] = set()
         self._swaps: dict[int, tuple[str, str]] = {}
         self._swapin_wait: set[str] = set()
         self._collect: Optional[list] = None  # tokens emitted by the iteration being launched
@@ -87,12 +93,17 @@ class LiveEngine(Engine):
 
     def _poll_async(self) -> None:
         now = self.clock()
-        for rid, layer in self.step.cpu_poll():
-            item = self._submitted.pop(rid)
+        for rid, _layer in self.step.cpu_poll():
+            self._finished.add(rid)
+        while self._order and self._order[0].req_id in self._finished:
+            item = self._order.popleft()
+            rid = item.req_id
+            self._finished.discard(rid)
+            self._submitted.pop(rid)
             self.now = now
             if self.opts.record_traces:
-                self.traces.setdefault(rid, []).append((layer, "Attn", "CPU"))
-            self._on_result(ResultItem(rid, layer, now, item.enq_seq))
+                self.traces.setdefault(rid, []).append((item.layer, "Attn", "CPU"))
+            self._on_result(ResultItem(rid, item.layer, now, item.enq_seq))
             self._dirty = True
         for ticket in [t for t in self._swaps if self.step.swap_done(t)]:
             rid, direction = self._swaps.pop(ticket)
@@ -119,6 +130,7 @@ class LiveEngine(Engine):
         self.step.cpu_submit(items)
         for it in items:
             self._submitted[it.req_id] = it
+            self._order.append(it)
             self.queues.input_enq += 1
             self.queues.input_deq += 1
             self._log("workitem_enq", request=it.req_id, layer=it.layer, host=0)
