@@ -88,6 +88,15 @@ int hs_op_decode_attention(const void* kv_pool, int layers, int pages, int n_kv,
                            int layer, const void* q, int q_row_stride, int n_q,
                            const int* page_table, int pt_stride, const int* chunks, int n_chunks,
                            float* o_part, float* lse_part, void* stream);
+/* K1+K2 fused: the last CTA of each (row, KV head) merges the row's chunks
+ * and writes out[row] (bf16); counters: int32[rows * n_kv], zeroed once
+ * (the kernel resets them). */
+int hs_op_decode_attention_fused(const void* kv_pool, int layers, int pages, int n_kv,
+                                 int head_dim, int layer, const void* q, int q_row_stride, int n_q,
+                                 const int* page_table, int pt_stride, const int* chunks,
+                                 int n_chunks, const int* row_chunk_begin, float* o_part,
+                                 float* lse_part, int* counters, void* out, int out_row_stride,
+                                 void* stream);
 /* K2: LSE-merge the chunks of each row (row_chunk_begin: int32[rows+1]). */
 int hs_op_decode_combine(const float* o_part, const float* lse_part, const int* row_chunk_begin,
                          int rows, int n_q, int n_kv, int head_dim, void* out,

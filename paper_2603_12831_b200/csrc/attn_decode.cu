@@ -38,7 +38,9 @@ __global__ void __launch_bounds__(kDecThreads, 2)
                        const bf16* __restrict__ q, int q_row_stride, int n_q,
                        const int* __restrict__ page_table, int pt_stride,
                        const DecodeChunk* __restrict__ chunks, float* __restrict__ o_part,
-                       float* __restrict__ lse_part, float scale_log2) {
+                       float* __restrict__ lse_part, float scale_log2,
+                       const int* __restrict__ row_chunk_begin, int* __restrict__ counters,
+                       bf16* __restrict__ out, int out_row_stride) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   constexpr int kBoxBytes = kPageTokens * 128;
@@ -223,6 +225,26 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   }
   __syncthreads();
   const int base = (blockIdx.x * geom.n_kv + kvh) * G;
+  const int c_lo = out ? row_chunk_begin[ch.row] : 0;
+  const int n_row_chunks = out ? row_chunk_begin[ch.row + 1] - c_lo : 0;
+  if (out && n_row_chunks == 1) {  // whole row in this CTA: normalise and store
+    for (int idx = threadIdx.x; idx < G * HD; idx += kDecThreads) {
+      const int r = idx / HD, d = idx % HD;
+      float Mr = -CUDART_INF_F;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) Mr = fmaxf(Mr, sm_m[w][r]);
+      const float Mur = Mr == -CUDART_INF_F ? 0.f : Mr;
+      float L = 0.f, acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        L += sm_l[w][r] * exp2f(sm_m[w][r] - Mur);
+        acc += so[(w * 16 + r) * HD + d];
+      }
+      out[static_cast<size_t>(ch.row) * out_row_stride + (kvh * G + r) * HD + d] =
+          __float2bfloat16(L > 0.f ? acc / L : 0.f);
+    }
+    return;
+  }
   for (int idx = threadIdx.x; idx < G * HD; idx += kDecThreads) {
     const int r = idx / HD, d = idx % HD;
     float Mr = -CUDART_INF_F;
@@ -239,6 +261,35 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     if (d == 0)
       lse_part[base + r] = L > 0.f ? (Mur + log2f(L)) * 0.69314718055994530942f : -CUDART_INF_F;
   }
+  if (!out) return;
+  // fused K2: the last CTA of this (row, KV head) merges the row's chunks
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(&counters[ch.row * geom.n_kv + kvh], 1);
+    s_last = prev == n_row_chunks - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int idx = threadIdx.x; idx < G * HD; idx += kDecThreads) {
+    const int r = idx / HD, d = idx % HD;
+    float mx = -CUDART_INF_F;
+    for (int c = c_lo; c < c_lo + n_row_chunks; ++c)
+      mx = fmaxf(mx, __ldcg(&lse_part[(c * geom.n_kv + kvh) * G + r]));
+    const float mu = mx == -CUDART_INF_F ? 0.f : mx;
+    float acc = 0.f, ws = 0.f;
+    for (int c = c_lo; c < c_lo + n_row_chunks; ++c) {
+      const int i2 = (c * geom.n_kv + kvh) * G + r;
+      const float w = __expf(__ldcg(&lse_part[i2]) - mu);
+      ws += w;
+      acc += w * __ldcg(&o_part[static_cast<size_t>(i2) * HD + d]);
+    }
+    out[static_cast<size_t>(ch.row) * out_row_stride + (kvh * G + r) * HD + d] =
+        __float2bfloat16(ws > 0.f ? acc / ws : 0.f);
+  }
+  if (threadIdx.x == 0) counters[ch.row * geom.n_kv + kvh] = 0;  // ready for the next launch
 }
 
 // K2: merge the split partials of each (row, query head).  One warp per pair.
@@ -284,7 +335,8 @@ template <int HD>
 static int launch_decode(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
                          int q_row_stride, int n_q, const int* pt, int pt_stride,
                          const DecodeChunk* chunks, int n_chunks, float* o_part, float* lse_part,
-                         cudaStream_t st) {
+                         cudaStream_t st, const int* row_chunk_begin = nullptr,
+                         int* counters = nullptr, bf16* out = nullptr, int out_row_stride = 0) {
   constexpr int kStageBytes = 2 * (HD / 64) * kPageTokens * 128;
   constexpr int kSmem = kDecStages * kStageBytes + 1024;
   static_assert(4 * 16 * HD * 4 <= kDecStages * kStageBytes, "merge scratch must fit");
@@ -296,9 +348,9 @@ static int launch_decode(const CUtensorMap& kv_map, const KvGeom& g, int layer, 
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
   dim3 grid(n_chunks, g.n_kv);
-  return launch_pdl(decode_attn_kernel<HD>, dim3(grid), dim3(kDecThreads), kSmem, st, kv_map, g, layer, q, q_row_stride, n_q,
-                                                           pt, pt_stride, chunks, o_part, lse_part,
-                                                           scale_log2);
+  return launch_pdl(decode_attn_kernel<HD>, dim3(grid), dim3(kDecThreads), kSmem, st, kv_map, g,
+                    layer, q, q_row_stride, n_q, pt, pt_stride, chunks, o_part, lse_part,
+                    scale_log2, row_chunk_begin, counters, out, out_row_stride);
 }
 
 int decode_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
@@ -313,6 +365,24 @@ int decode_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, cons
   if (g.head_dim == 64)
     return launch_decode<64>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride, chunks,
                              n_chunks, o_part, lse_part, st);
+  return HS_E_CONFIG;
+}
+
+int decode_attention_fused(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                           int q_row_stride, int n_q, const int* page_table, int pt_stride,
+                           const DecodeChunk* chunks, int n_chunks, const int* row_chunk_begin,
+                           float* o_part, float* lse_part, int* counters, bf16* out,
+                           int out_row_stride, cudaStream_t st) {
+  if (n_chunks <= 0) return HS_OK;
+  if (n_q % g.n_kv || n_q / g.n_kv > 16) return HS_E_CONFIG;
+  if (g.head_dim == 128)
+    return launch_decode<128>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride,
+                              chunks, n_chunks, o_part, lse_part, st, row_chunk_begin, counters,
+                              out, out_row_stride);
+  if (g.head_dim == 64)
+    return launch_decode<64>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride, chunks,
+                             n_chunks, o_part, lse_part, st, row_chunk_begin, counters, out,
+                             out_row_stride);
   return HS_E_CONFIG;
 }
 

@@ -129,6 +129,24 @@ int hs_op_decode_attention(const void* kv_pool, int layers, int pages, int n_kv,
       "decode_attention");
 }
 
+int hs_op_decode_attention_fused(const void* kv_pool, int layers, int pages, int n_kv,
+                                 int head_dim, int layer, const void* q, int q_row_stride, int n_q,
+                                 const int* page_table, int pt_stride, const int* chunks,
+                                 int n_chunks, const int* row_chunk_begin, float* o_part,
+                                 float* lse_part, int* counters, void* out, int out_row_stride,
+                                 void* stream) {
+  KvGeom g{layers, pages, n_kv, head_dim};
+  CUtensorMap m;
+  if (make_kv_map(&m, static_cast<const bf16*>(kv_pool), g) != HS_OK)
+    return set_error(HS_E_CUDA, "decode: kv map encode failed");
+  return cuda_status(
+      decode_attention_fused(m, g, layer, static_cast<const bf16*>(q), q_row_stride, n_q,
+                             page_table, pt_stride, reinterpret_cast<const DecodeChunk*>(chunks),
+                             n_chunks, row_chunk_begin, o_part, lse_part, counters,
+                             static_cast<bf16*>(out), out_row_stride, S(stream)),
+      "decode_attention_fused");
+}
+
 int hs_op_decode_combine(const float* o_part, const float* lse_part, const int* row_chunk_begin,
                          int rows, int n_q, int n_kv, int head_dim, void* out,
                          int out_row_stride, float* lse_out, void* stream) {
@@ -179,7 +197,8 @@ int hs_op_qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int
   KvGeom g{layers, pages, n_kv, head_dim};
   return cuda_status(
       qkv_rope_scatter(part, splits, rows, n_q, n_kv, head_dim, rope_cos, rope_sin, row_pos,
-                       row_slot, row_mode, static_cast<bf16*>(qbuf), q_row_stride,
+                       row_slot, row_mode, rows, nullptr, nullptr, static_cast<bf16*>(qbuf),
+                       q_row_stride,
                        static_cast<bf16*>(kv_pool), g, layer, page_table, pt_stride,
                        static_cast<bf16*>(ship), ship_stride, S(stream)),
       "qkv_rope_scatter");

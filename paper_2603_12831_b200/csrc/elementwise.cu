@@ -191,7 +191,10 @@ __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int spli
                                         const float* __restrict__ rope_sin,
                                         const int* __restrict__ row_pos,
                                         const int* __restrict__ row_slot,
-                                        const int* __restrict__ row_mode, bf16* __restrict__ qbuf,
+                                        const int* __restrict__ row_mode, int n_batch,
+                                        const int* __restrict__ carry_pos,
+                                        const int* __restrict__ carry_slot,
+                                        bf16* __restrict__ qbuf,
                                         int q_row_stride, bf16* __restrict__ kv_pool, KvGeom geom,
                                         int layer, const int* __restrict__ page_table,
                                         int pt_stride, bf16* __restrict__ ship, int ship_stride) {
@@ -203,7 +206,13 @@ __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int spli
   const size_t plane = static_cast<size_t>(rows) * n_tot;
   const int base = head * hd;
   const float* src = part + static_cast<size_t>(r) * n_tot + base;
-  const int pos = row_pos[r], slot = row_slot[r], mode = row_mode[r];
+  // rows [0, n_batch) come from the iteration's row arrays (mode 0 = KV
+  // page scatter, or per-row modes when given); rows beyond are carry rows
+  // shipped to the host (mode 1)
+  const bool batch = r < n_batch;
+  const int pos = batch ? row_pos[r] : carry_pos[r - n_batch];
+  const int slot = batch ? row_slot[r] : carry_slot[r - n_batch];
+  const int mode = batch ? (row_mode ? row_mode[r] : 0) : 1;
   const float x1 = sum_planes1(src + i, plane, splits);
   const float x2 = sum_planes1(src + i + half, plane, splits);
   bf16 y1, y2;
@@ -233,14 +242,15 @@ __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int spli
 
 int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv, int head_dim,
                      const float* rope_cos, const float* rope_sin, const int* row_pos,
-                     const int* row_slot, const int* row_mode, bf16* qbuf, int q_row_stride,
-                     bf16* kv_pool, const KvGeom& g, int layer, const int* page_table,
-                     int pt_stride, bf16* ship, int ship_stride, cudaStream_t st) {
+                     const int* row_slot, const int* row_mode, int n_batch, const int* carry_pos,
+                     const int* carry_slot, bf16* qbuf, int q_row_stride, bf16* kv_pool,
+                     const KvGeom& g, int layer, const int* page_table, int pt_stride, bf16* ship,
+                     int ship_stride, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
   if (splits > kMaxSplits) return HS_E_CONFIG;
   dim3 grid(rows, n_q + 2 * n_kv);
   return launch_pdl(qkv_rope_scatter_kernel, dim3(grid), dim3(head_dim / 2), 0, st, part, splits, rows, n_q, n_kv, head_dim, rope_cos, rope_sin, row_pos, row_slot, row_mode,
-      qbuf, q_row_stride, kv_pool, g, layer, page_table, pt_stride, ship, ship_stride);
+      n_batch, carry_pos, carry_slot, qbuf, q_row_stride, kv_pool, g, layer, page_table, pt_stride, ship, ship_stride);
 }
 
 // ---------------------------------------------------------------- SwiGLU

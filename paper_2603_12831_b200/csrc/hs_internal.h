@@ -81,6 +81,14 @@ int decode_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, cons
                      int q_row_stride, int n_q, const int* page_table, int pt_stride,
                      const DecodeChunk* chunks, int n_chunks, float* o_part, float* lse_part,
                      cudaStream_t st);
+// Fused variant: the last CTA of each (row, KV head) LSE-merges the row's
+// chunks (self-resetting counters [rows * n_kv], zero-initialised) and writes
+// the bf16 output; single-chunk rows are written directly.
+int decode_attention_fused(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                           int q_row_stride, int n_q, const int* page_table, int pt_stride,
+                           const DecodeChunk* chunks, int n_chunks, const int* row_chunk_begin,
+                           float* o_part, float* lse_part, int* counters, bf16* out,
+                           int out_row_stride, cudaStream_t st);
 int decode_combine(const float* o_part, const float* lse_part, const int* row_chunk_begin,
                    int rows, int n_q, int n_kv, int head_dim, bf16* out, int out_row_stride,
                    float* lse_out, cudaStream_t st);
@@ -103,11 +111,14 @@ int rmsnorm_rows(const float* h, int rows, int d, const float* w, float eps, bf1
 int splitk_reduce(const float* part, int splits, int rows, int n, float* out, cudaStream_t st);
 int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
                       float eps, bf16* out, int ld_out, cudaStream_t st);
+// rows [0, n_batch): row_* arrays (row_mode may be null = all KV-scatter);
+// rows [n_batch, rows): carry_* arrays, shipped to the host mailbox
 int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv, int head_dim,
                      const float* rope_cos, const float* rope_sin, const int* row_pos,
-                     const int* row_slot, const int* row_mode, bf16* qbuf, int q_row_stride,
-                     bf16* kv_pool, const KvGeom& g, int layer, const int* page_table,
-                     int pt_stride, bf16* ship, int ship_stride, cudaStream_t st);
+                     const int* row_slot, const int* row_mode, int n_batch, const int* carry_pos,
+                     const int* carry_slot, bf16* qbuf, int q_row_stride, bf16* kv_pool,
+                     const KvGeom& g, int layer, const int* page_table, int pt_stride, bf16* ship,
+                     int ship_stride, cudaStream_t st);
 int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld_act,
              cudaStream_t st);
 int argmax_rows(const float* part, int splits, int rows, int vocab, int* tokens, float* logits_out,

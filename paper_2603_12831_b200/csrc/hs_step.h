@@ -12,8 +12,8 @@
 
 namespace hs {
 
-int select_tokens(const int* row_token, const int* row_slot, const int* last_token, int rows,
-                  int* tok, cudaStream_t st);
+int select_tokens(const int* row_token, const int* row_slot, int n_batch, const int* carry_slot,
+                  const int* last_token, int rows, int* tok, cudaStream_t st);
 int gather_rows_f32(const float* src, const int* idx, int rows, int d, float* dst,
                     cudaStream_t st);
 int scatter_rows_f32(const float* src, const int* idx, int rows, int d, float* dst,

@@ -92,8 +92,15 @@ struct hs_ctx {
   int stage_half = 0;
   size_t stage_pos = 0;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
-  // iteration state
+  // iteration state; pointers into the packed per-iteration device block
   int B = 0, D = 0, n_chunks = 0, n_tiles = 0, n_logit = 0, n_tok_out = 0, merges_L = 0;
+  int* dm_iter = nullptr;   // packed iteration metadata (one upload per iteration)
+  int* dm_layer = nullptr;  // packed layer metadata (one upload per layer)
+  size_t iter_cap = 0, layer_cap = 0;
+  const int *it_slot = nullptr, *it_pos = nullptr, *it_tok = nullptr, *it_chunks = nullptr,
+            *it_cbeg = nullptr, *it_tiles = nullptr;
+  std::vector<int> h_logit_rows, h_logit_slots;  // host copies (layer-L gather lists)
+  int* dec_counters = nullptr;
   int* tokens_pinned = nullptr;
   // piggyback mailboxes (pinned, mapped)
   bf16 *ship_h = nullptr, *ship_d = nullptr, *result_h = nullptr, *result_d = nullptr;
@@ -289,6 +296,38 @@ int upload_fill(hs_ctx* c, size_t dst_off, int value, size_t n) {
   return HS_OK;
 }
 
+// Packs several int arrays into one pinned staging run and ships them with a
+// single cudaMemcpyAsync into a device block; returns device pointers.
+struct Packer {
+  hs_ctx* c;
+  int* host = nullptr;
+  int* dev;
+  size_t n = 0, cap;
+  Packer(hs_ctx* c_, int* dev_, size_t cap_) : c(c_), dev(dev_), cap(cap_) {}
+  bool reserve(size_t total) {
+    host = stage(c, total);
+    cap = total;
+    return host != nullptr;
+  }
+  const int* add(const int* src, size_t cnt) {
+    const int* d = dev + n;
+    if (cnt) std::memcpy(host + n, src, cnt * sizeof(int));
+    n += cnt;
+    return d;
+  }
+  const int* fill(int v, size_t cnt) {
+    const int* d = dev + n;
+    for (size_t i = 0; i < cnt; ++i) host[n + i] = v;
+    n += cnt;
+    return d;
+  }
+  int flush(cudaStream_t st) {
+    if (n == 0) return HS_OK;
+    CK(cudaMemcpyAsync(dev, host, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    return HS_OK;
+  }
+};
+
 // deterministic N(0, std) weights from a counter hash (splitmix64 + Box-Muller)
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
@@ -384,6 +423,9 @@ void free_all(hs_ctx* c) {
   F(c->rope_sin);
   F(c->logits);
   F(c->dm);
+  F(c->dm_iter);
+  F(c->dm_layer);
+  F(c->dec_counters);
   if (c->hm) cudaFreeHost(c->hm);
   if (c->tokens_pinned) cudaFreeHost(c->tokens_pinned);
   if (c->ship_h) cudaFreeHost(c->ship_h);
@@ -476,6 +518,12 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
   // metadata
   c->meta_ints = layout_of(r).total + 16 * R * (m.layers + 2);
   RC(dalloc(&c->dm, layout_of(r).total));
+  c->iter_cap = 3 * R + 5 * static_cast<size_t>(r.max_chunks) + (R + 1) + 4 * R + 16;
+  c->layer_cap = 9 * R + 16;
+  RC(dalloc(&c->dm_iter, c->iter_cap));
+  RC(dalloc(&c->dm_layer, c->layer_cap));
+  RC(dalloc(&c->dec_counters, R * m.n_kv));
+  CK(cudaMemset(c->dec_counters, 0, R * m.n_kv * sizeof(int)));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hm), 2 * c->meta_ints * sizeof(int),
                    cudaHostAllocDefault));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->tokens_pinned), 2 * R * sizeof(int),
@@ -802,14 +850,23 @@ int hs_iter_begin(hs_ctx* c, const hs_iter_desc* d) {
   c->n_logit = d->n_logit_rows;
   c->n_tok_out = 0;
   c->merges_L = 0;
-  RC(upload(c, L.row_slot, d->row_slot, d->n_rows));
-  RC(upload(c, L.row_pos, d->row_pos, d->n_rows));
-  RC(upload(c, L.row_token, d->row_token, d->n_rows));
-  RC(upload_fill(c, L.row_mode, 0, d->n_rows));
-  RC(upload(c, L.chunks, d->chunks, static_cast<size_t>(d->n_chunks) * 5));
-  RC(upload(c, L.row_chunk_begin, d->row_chunk_begin, d->n_chunks ? d->n_decode + 1 : 0));
-  RC(upload(c, L.tiles, d->tiles, static_cast<size_t>(d->n_tiles) * 4));
-  RC(upload(c, L.logit_rows, d->logit_rows, d->n_logit_rows));
+  {
+    const size_t total = 3 * static_cast<size_t>(d->n_rows) + 5 * static_cast<size_t>(d->n_chunks) +
+                         (d->n_chunks ? d->n_decode + 1 : 0) + 4 * static_cast<size_t>(d->n_tiles);
+    if (total > c->iter_cap) return set_error(HS_E_CAPACITY, "iteration metadata too large");
+    Packer pk(c, c->dm_iter, total);
+    if (!pk.reserve(total)) return set_error(HS_E_CAPACITY, "metadata staging overflow");
+    c->it_slot = pk.add(d->row_slot, d->n_rows);
+    c->it_pos = pk.add(d->row_pos, d->n_rows);
+    c->it_tok = pk.add(d->row_token, d->n_rows);
+    c->it_chunks = pk.add(d->chunks, static_cast<size_t>(d->n_chunks) * 5);
+    c->it_cbeg = pk.add(d->row_chunk_begin, d->n_chunks ? d->n_decode + 1 : 0);
+    c->it_tiles = pk.add(d->tiles, static_cast<size_t>(d->n_tiles) * 4);
+    RC(pk.flush(c->st));
+  }
+  c->h_logit_rows.assign(d->logit_rows, d->logit_rows + d->n_logit_rows);
+  c->h_logit_slots.resize(d->n_logit_rows);
+  for (int i = 0; i < d->n_logit_rows; ++i) c->h_logit_slots[i] = d->row_slot[d->logit_rows[i]];
   c->dec_kv_tokens = 0;
   for (int r = 0; r < d->n_decode && d->n_chunks; ++r)
     c->dec_kv_tokens += d->chunks[static_cast<size_t>(d->row_chunk_begin[r]) * 5 + 4];
@@ -820,9 +877,6 @@ int hs_iter_begin(hs_ctx* c, const hs_iter_desc* d) {
     c->pre_units += nq * pos0 + nq * (nq + 1) / 2;
     c->pre_kv_tokens += pos0 + nq;
   }
-  std::vector<int> lslot(d->n_logit_rows);
-  for (int i = 0; i < d->n_logit_rows; ++i) lslot[i] = d->row_slot[d->logit_rows[i]];
-  RC(upload(c, L.logit_slot, lslot.data(), lslot.size()));
   return HS_OK;
 }
 
@@ -841,46 +895,62 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   const int d_ = m.d, nqh = m.n_q * m.hd;
   int sp = 1;
   ProfScope whole(c, 3, 0.0, 0.0);  // the layer's span on the device
-  // carry rows: ship meta at [B, B+C)
-  RC(upload(c, L.row_slot + B, d->carry_slot, C));
-  RC(upload(c, L.row_pos + B, d->carry_pos, C));
-  RC(upload_fill(c, L.row_token + B, -1, C));
-  RC(upload_fill(c, L.row_mode + B, 1, C));
+  const int R = d->n_restart;
+  const int NL = last ? c->n_logit + M : 0;
+  // one packed upload: carry slots/pos, merge slots, restart slots/pos and,
+  // at the last layer, the LM-head gather rows and their slots
+  Packer pk(c, c->dm_layer, 0);
+  const size_t total = 2 * static_cast<size_t>(C) + M + 2 * static_cast<size_t>(R) + 2 * NL;
+  if (total > c->layer_cap) return set_error(HS_E_CAPACITY, "layer metadata too large");
+  if (total && !pk.reserve(total)) return set_error(HS_E_CAPACITY, "metadata staging overflow");
+  std::vector<int> rslot(R), lrows(NL), lslots(NL);
+  for (int i = 0; i < R; ++i) rslot[i] = d->merge_slot[d->restart_idx[i]];
+  for (int i = 0; i < NL; ++i) {
+    const bool batch = i < c->n_logit;
+    lrows[i] = batch ? c->h_logit_rows[i] : B + (i - c->n_logit);
+    lslots[i] = batch ? c->h_logit_slots[i] : d->merge_slot[i - c->n_logit];
+  }
+  const int* carry_slot = total ? pk.add(d->carry_slot, C) : nullptr;
+  const int* carry_pos = total ? pk.add(d->carry_pos, C) : nullptr;
+  const int* merge_slot = total ? pk.add(d->merge_slot, M) : nullptr;
+  const int* restart_slot = total ? pk.add(rslot.data(), R) : nullptr;
+  const int* restart_pos = total ? pk.add(d->restart_pos, R) : nullptr;
+  const int* logit_rows = total ? pk.add(lrows.data(), NL) : nullptr;
+  const int* logit_slots = total ? pk.add(lslots.data(), NL) : nullptr;
+  if (total) RC(pk.flush(st));
   if (l == 0) {
     // embed batch rows (+ injected chains: fresh token from last_token)
-    RC(select_tokens(dm + L.row_token, dm + L.row_slot, c->last_token, B + C, c->tok, st));
+    RC(select_tokens(c->it_tok, c->it_slot, B, carry_slot, c->last_token, B + C, c->tok, st));
     RC(embed_gather(c->tok, B + C, c->w_embed, d_, c->h, st));
     // residual put for injections (reference _chain_qkv(req, 1), engine.py:997)
-    RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, dm + L.row_slot + B, C, d_, c->resid,
-                        st));
+    RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, carry_slot, C, d_, c->resid, st));
     RC(rmsnorm_rows(c->h, B + C, d_, c->n_in[0], m.eps, c->xn.p, d_, st));
   }
   // QKV over batch + carry rows, RoPE, KV scatter / piggyback ship
   RC(gemm(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, &sp));
   RC(qkv_rope_scatter(c->part, sp, B + C, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
-                      dm + L.row_pos, dm + L.row_slot, dm + L.row_mode, c->qbuf, nqh, c->kv_pool,
-                      c->geom, l, c->page_table, r.max_pages_per_req, c->ship_d, m.qkv_n(), st));
-  // attention of batch rows
+                      c->it_pos, c->it_slot, nullptr, B, carry_pos, carry_slot, c->qbuf, nqh,
+                      c->kv_pool, c->geom, l, c->page_table, r.max_pages_per_req, c->ship_d,
+                      m.qkv_n(), st));
+  // attention of batch rows (K1 with the K2 merge fused into its last CTA)
   {
   ProfScope pd(c, 1, c->dec_kv_tokens * 2.0 * m.n_kv * m.hd * 2.0 + 4.0 * c->D * nqh,
                4.0 * c->dec_kv_tokens * nqh);
-  RC(decode_attention(c->m_kv, c->geom, l, c->qbuf, nqh, m.n_q, c->page_table,
-                      r.max_pages_per_req, reinterpret_cast<const DecodeChunk*>(dm + L.chunks),
-                      c->n_chunks, c->o_part, c->lse_part, st));
-  RC(decode_combine(c->o_part, c->lse_part, dm + L.row_chunk_begin, c->n_chunks ? c->D : 0, m.n_q,
-                    m.n_kv, m.hd, c->attn.p, nqh, nullptr, st));
+  RC(decode_attention_fused(c->m_kv, c->geom, l, c->qbuf, nqh, m.n_q, c->page_table,
+                            r.max_pages_per_req, reinterpret_cast<const DecodeChunk*>(c->it_chunks),
+                            c->n_chunks, c->it_cbeg, c->o_part, c->lse_part, c->dec_counters,
+                            c->attn.p, nqh, st));
   }
   {
   ProfScope pp(c, 2, c->pre_kv_tokens * 2.0 * m.n_kv * m.hd * 2.0, 4.0 * c->pre_units * nqh);
   RC(prefill_attention(c->m_kv, c->geom, l, c->qbuf, nqh, m.n_q, c->page_table,
-                       r.max_pages_per_req, reinterpret_cast<const PrefillTile*>(dm + L.tiles),
+                       r.max_pages_per_req, reinterpret_cast<const PrefillTile*>(c->it_tiles),
                        c->n_tiles, c->attn.p, nqh, st));
   }
   // merged rows: host attention result + stored residual
-  RC(upload(c, L.merge_slot, d->merge_slot, M));
-  RC(gather_rows_bf16(c->result_d, nqh, dm + L.merge_slot, M, nqh,
+  RC(gather_rows_bf16(c->result_d, nqh, merge_slot, M, nqh,
                       c->attn.p + static_cast<size_t>(B) * nqh, nqh, st));
-  RC(gather_rows_f32(c->resid, dm + L.merge_slot, M, d_, c->h + static_cast<size_t>(B) * d_, st));
+  RC(gather_rows_f32(c->resid, merge_slot, M, d_, c->h + static_cast<size_t>(B) * d_, st));
   const int N = B + M;
   // Proj + ResidualAdd
   RC(gemm(c, c->m_o[l], c->attn, N, d_, nqh, &sp));
@@ -893,42 +963,27 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
                        c->xn.p, d_, st));
   if (!last) {
     // residual put for the chains' next layer (engine.py:985)
-    RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, dm + L.merge_slot, M, d_, c->resid,
-                        st));
+    RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, merge_slot, M, d_, c->resid, st));
     return HS_OK;
   }
   // ---- final layer: LM head + greedy token for decode / finishing-prefill
   // rows and for every chain completing a token (engine.py:1005-1013, 1024-1047)
-  const int NL = c->n_logit + M;
-  RC(gather_rows_bf16(c->xn.p, d_, dm + L.logit_rows, c->n_logit, d_, c->lin.p, d_, st));
-  CK(cudaMemcpyAsync(c->lin.p + static_cast<size_t>(c->n_logit) * d_,
-                     c->xn.p + static_cast<size_t>(B) * d_, static_cast<size_t>(M) * d_ * 2,
-                     cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(dm + L.logit_slot + c->n_logit, dm + L.merge_slot, M * sizeof(int),
-                     cudaMemcpyDeviceToDevice, st));
+  RC(gather_rows_bf16(c->xn.p, d_, logit_rows, NL, d_, c->lin.p, d_, st));
   RC(gemm(c, c->m_lm, c->lin, NL, m.vocab, d_, &sp));
   RC(argmax_rows(c->part, sp, NL, m.vocab, c->tok_out, c->keep_logits ? c->logits : nullptr, st));
-  RC(scatter_tokens(c->tok_out, dm + L.logit_slot, NL, c->last_token, st));
+  RC(scatter_tokens(c->tok_out, logit_slots, NL, c->last_token, st));
   c->n_tok_out = NL;
   c->merges_L = M;
   // chains continuing with the next token: embed, residual put, QKV(1), ship
-  const int R = d->n_restart;
   if (R > 0) {
-    std::vector<int> rslot(R);
-    for (int i = 0; i < R; ++i) rslot[i] = d->merge_slot[d->restart_idx[i]];
-    RC(upload(c, L.restart_slot, rslot.data(), R));
-    RC(upload(c, L.restart_pos, d->restart_pos, R));
-    RC(upload_fill(c, L.restart_token, -1, R));
-    RC(upload_fill(c, L.restart_mode, 1, R));
-    RC(select_tokens(dm + L.restart_token, dm + L.restart_slot, c->last_token, R, c->tok, st));
+    RC(select_tokens(nullptr, nullptr, 0, restart_slot, c->last_token, R, c->tok, st));
     RC(embed_gather(c->tok, R, c->w_embed, d_, c->hr, st));
-    RC(scatter_rows_f32(c->hr, dm + L.restart_slot, R, d_, c->resid, st));
+    RC(scatter_rows_f32(c->hr, restart_slot, R, d_, c->resid, st));
     RC(rmsnorm_rows(c->hr, R, d_, c->n_in[0], m.eps, c->xr.p, d_, st));
     RC(gemm(c, c->m_qkv[0], c->xr, R, m.qkv_n(), d_, &sp));
-    RC(qkv_rope_scatter(c->part, sp, R, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
-                        dm + L.restart_pos, dm + L.restart_slot, dm + L.restart_mode, c->qbuf, nqh,
-                        c->kv_pool, c->geom, 0, c->page_table, r.max_pages_per_req, c->ship_d,
-                        m.qkv_n(), st));
+    RC(qkv_rope_scatter(c->part, sp, R, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin, nullptr,
+                        nullptr, nullptr, 0, restart_pos, restart_slot, c->qbuf, nqh, c->kv_pool,
+                        c->geom, 0, c->page_table, r.max_pages_per_req, c->ship_d, m.qkv_n(), st));
   }
   return HS_OK;
 }

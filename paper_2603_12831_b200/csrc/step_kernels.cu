@@ -9,15 +9,21 @@
 
 namespace hs {
 
-// tok[r] = row_token[r] >= 0 ? row_token[r] : last_token[row_slot[r]]
+// rows < n_batch: tok = row_token >= 0 ? row_token : last_token[row_slot];
+// rows >= n_batch (carry rows): tok = last_token[carry_slot]
 __global__ void select_tokens_kernel(const int* __restrict__ row_token,
-                                     const int* __restrict__ row_slot,
+                                     const int* __restrict__ row_slot, int n_batch,
+                                     const int* __restrict__ carry_slot,
                                      const int* __restrict__ last_token, int rows,
                                      int* __restrict__ tok) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
+  if (r >= n_batch) {
+    tok[r] = last_token[carry_slot[r - n_batch]];
+    return;
+  }
   const int t = row_token[r];
   tok[r] = t >= 0 ? t : last_token[row_slot[r]];
 }
@@ -94,11 +100,10 @@ __global__ void kv_swap_kernel(bf16* __restrict__ pool, KvGeom g, const int* __r
 }
 
 // ------------------------------------------------------------------ launchers
-int select_tokens(const int* row_token, const int* row_slot, const int* last_token, int rows,
-                  int* tok, cudaStream_t st) {
+int select_tokens(const int* row_token, const int* row_slot, int n_batch, const int* carry_slot,
+                  const int* last_token, int rows, int* tok, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  return launch_pdl(select_tokens_kernel, dim3((rows + 127) / 128), dim3(128), 0, st, row_token, row_slot, last_token, rows,
-                                                           tok);
+  return launch_pdl(select_tokens_kernel, dim3((rows + 127) / 128), dim3(128), 0, st, row_token, row_slot, n_batch, carry_slot, last_token, rows, tok);
 }
 
 int gather_rows_f32(const float* src, const int* idx, int rows, int d, float* dst,

@@ -285,3 +285,50 @@ def test_gemm_tcgen05_blocked_weights(cuda, tokens, n, k):
     _lib.call("hs_op_splitk_reduce", _p(part), used.value, tokens, n, _p(out), None)
     torch.cuda.synchronize()
     assert _rel(out.cpu().numpy().reshape(tokens, n), O.gemm(x, w)) < 1e-4
+
+
+@pytest.mark.parametrize("n_q,n_kv,hd", [(32, 8, 128), (4, 2, 64)])
+@pytest.mark.parametrize("chunk_pages", [1, 4, 64])
+def test_decode_attention_fused_combine(cuda, n_q, n_kv, hd, chunk_pages):
+    """K1 with K2 fused into the last CTA per (row, KV head); run twice to
+    check the self-resetting counters."""
+    import torch
+    from paper_2603_12831_b200 import _lib
+
+    rng = np.random.default_rng(11 + chunk_pages)
+    layers, pages = 1, 64
+    pool = _make_pool(rng, layers, pages, n_kv, hd)
+    ctxs = [1, 64, 65, 300, 1100]
+    max_pages = 20
+    perm = rng.permutation(pages)
+    pt = np.zeros((len(ctxs), max_pages), np.int32)
+    cur = 0
+    for r, c in enumerate(ctxs):
+        npg = (c + 63) // 64
+        pt[r, :npg] = perm[cur:cur + npg]
+        cur += npg
+    q = _bf16_np(rng, (len(ctxs), n_q, hd))
+    chunks, begin = [], [0]
+    for r, c in enumerate(ctxs):
+        npg = (c + 63) // 64
+        for p0 in range(0, npg, chunk_pages):
+            chunks.append((r, r, p0, min(npg, p0 + chunk_pages), c))
+        begin.append(len(chunks))
+    dpool, dq = _t(pool, cuda, torch.bfloat16), _t(q, cuda, torch.bfloat16)
+    dpt, dch = _t(pt, cuda), _t(np.array(chunks, np.int32), cuda)
+    dbeg = _t(np.array(begin, np.int32), cuda)
+    cnt = torch.zeros(len(ctxs) * n_kv, dtype=torch.int32, device=cuda)
+    opart = torch.zeros(len(chunks) * n_q * hd, dtype=torch.float32, device=cuda)
+    lpart = torch.zeros(len(chunks) * n_q, dtype=torch.float32, device=cuda)
+    for _ in range(2):
+        out = torch.zeros(len(ctxs), n_q * hd, dtype=torch.bfloat16, device=cuda)
+        _lib.call("hs_op_decode_attention_fused", _p(dpool), layers, pages, n_kv, hd, 0, _p(dq),
+                  n_q * hd, n_q, _p(dpt), max_pages, _p(dch), len(chunks), _p(dbeg), _p(opart),
+                  _p(lpart), _p(cnt), _p(out), n_q * hd, None)
+        torch.cuda.synchronize()
+        got = out.float().cpu().numpy().reshape(len(ctxs), n_q, hd)
+        for r, c in enumerate(ctxs):
+            k, v = _gather_kv(pool, 0, pt[r, :(c + 63) // 64], c)
+            ref, _ = O.decode_attention(q[r], k, v, n_kv)
+            assert _rel(got[r], ref) < 1.5e-2, (r, c)
+    assert int(cnt.abs().sum().item()) == 0
