@@ -275,6 +275,9 @@ int hs_profile_read(hs_ctx* ctx, double* stats /* [4][4] */, int reset);
  * of g requests with ctx keys each; causal prefill of q new tokens after
  * `done` tokens of context (the seam of build_dense_table, latency.py:200). */
 int hs_probe_dense(hs_ctx* ctx, int n, int reps, float* us);
+/* one layer-0 GEMM (which: 0 qkv, 1 o, 2 gate-up, 3 down), plain partial
+ * planes (fused = 0) or with its fused stream-K epilogue (fused = 1) */
+int hs_probe_gemm(hs_ctx* ctx, int which, int n, int fused, int reps, float* us);
 int hs_probe_decode(hs_ctx* ctx, int g, int ctx_len, int reps, float* us);
 int hs_probe_prefill(hs_ctx* ctx, int q, int done, int reps, float* us);
 

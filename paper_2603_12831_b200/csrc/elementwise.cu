@@ -197,7 +197,8 @@ __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int spli
                                         bf16* __restrict__ qbuf,
                                         int q_row_stride, bf16* __restrict__ kv_pool, KvGeom geom,
                                         int layer, const int* __restrict__ page_table,
-                                        int pt_stride, bf16* __restrict__ ship, int ship_stride) {
+                                        int pt_stride, bf16* __restrict__ ship, int ship_stride,
+                                        int permuted) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const int r = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
@@ -213,8 +214,11 @@ __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int spli
   const int pos = batch ? row_pos[r] : carry_pos[r - n_batch];
   const int slot = batch ? row_slot[r] : carry_slot[r - n_batch];
   const int mode = batch ? (row_mode ? row_mode[r] : 0) : 1;
-  const float x1 = sum_planes1(src + i, plane, splits);
-  const float x2 = sum_planes1(src + i + half, plane, splits);
+  // permuted weights (fused-epilogue layout): feature i of the head sits in
+  // row 2i, feature i + hd/2 in row 2i+1
+  const int i1 = permuted ? 2 * i : i, i2 = permuted ? 2 * i + 1 : i + half;
+  const float x1 = sum_planes1(src + i1, plane, splits);
+  const float x2 = sum_planes1(src + i2, plane, splits);
   bf16 y1, y2;
   if (head < n_q + n_kv) {  // rotate q and k heads
     const float c = rope_cos[static_cast<size_t>(pos) * half + i];
@@ -245,17 +249,17 @@ int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv,
                      const int* row_slot, const int* row_mode, int n_batch, const int* carry_pos,
                      const int* carry_slot, bf16* qbuf, int q_row_stride, bf16* kv_pool,
                      const KvGeom& g, int layer, const int* page_table, int pt_stride, bf16* ship,
-                     int ship_stride, cudaStream_t st) {
+                     int ship_stride, cudaStream_t st, int permuted) {
   if (rows <= 0) return HS_OK;
   if (splits > kMaxSplits) return HS_E_CONFIG;
   dim3 grid(rows, n_q + 2 * n_kv);
   return launch_pdl(qkv_rope_scatter_kernel, dim3(grid), dim3(head_dim / 2), 0, st, part, splits, rows, n_q, n_kv, head_dim, rope_cos, rope_sin, row_pos, row_slot, row_mode,
-      n_batch, carry_pos, carry_slot, qbuf, q_row_stride, kv_pool, g, layer, page_table, pt_stride, ship, ship_stride);
+      n_batch, carry_pos, carry_slot, qbuf, q_row_stride, kv_pool, g, layer, page_table, pt_stride, ship, ship_stride, permuted);
 }
 
 // ---------------------------------------------------------------- SwiGLU
 __global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int rows, int ffn,
-                                bf16* __restrict__ act, int ld_act) {
+                                bf16* __restrict__ act, int ld_act, int permuted) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const size_t plane = static_cast<size_t>(rows) * 2 * ffn;
@@ -264,19 +268,22 @@ __global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int 
        idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t r = idx / ffn, i = idx % ffn;
     const float* src = part + r * 2 * ffn;
-    const float gt = sum_planes1(src + i, plane, splits);
-    const float up = sum_planes1(src + ffn + i, plane, splits);
+    // permuted: 32-row groups [16 gate | 16 up] of the same features
+    const size_t gi = permuted ? 32 * (i / 16) + i % 16 : i;
+    const size_t ui = permuted ? gi + 16 : ffn + i;
+    const float gt = sum_planes1(src + gi, plane, splits);
+    const float up = sum_planes1(src + ui, plane, splits);
     const float s = gt / (1.f + __expf(-gt));
     act[r * ld_act + i] = __float2bfloat16(s * up);
   }
 }
 
 int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld_act,
-             cudaStream_t st) {
+             cudaStream_t st, int permuted) {
   const size_t total = static_cast<size_t>(rows) * ffn;
   if (!total) return HS_OK;
   const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, size_t(148 * 16)));
-  return launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, st, part, splits, rows, ffn, act, ld_act);
+  return launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, st, part, splits, rows, ffn, act, ld_act, permuted);
 }
 
 // ---------------------------------------------------------------- greedy argmax

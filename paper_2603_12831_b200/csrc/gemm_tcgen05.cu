@@ -65,11 +65,76 @@ struct StreamK {
 // kBlocked: weights pre-tiled as [N/128][K/64][128][64] so every 16 KB TMA
 // box is one contiguous run of HBM (row-major weights make each box 128
 // scattered 128-byte segments).
-template <int BN, bool kBlocked>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Apply the fused epilogue to 16 token columns `v` of output feature row n
+// (all 32 lanes of the warp call this together: the pairings shuffle).
+template <int Epi>
+__device__ __forceinline__ void epi_apply(const EpiParams& ep, int n, int lane, int t0c,
+                                          int tokens, float (&v)[16]) {
+  if constexpr (Epi == EPI_RESID) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int tt = t0c + j;
+      if (tt < tokens) ep.h[static_cast<size_t>(tt) * ep.ld_h + n] += v[j];
+    }
+  } else if constexpr (Epi == EPI_SILU) {
+    // rows interleaved in 32-row groups: lanes 0-15 gate, 16-31 up of the
+    // same 16 features (weights permuted by permute_rows_gate_up)
+    const int f = 16 * (n >> 5) + lane;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float up = __shfl_xor_sync(0xffffffffu, v[j], 16);
+      const int tt = t0c + j;
+      if (lane < 16 && tt < tokens) {
+        const float g = v[j];
+        ep.act[static_cast<size_t>(tt) * ep.ld_act + f] =
+            __float2bfloat16(g / (1.f + __expf(-g)) * up);
+      }
+    }
+  } else if constexpr (Epi == EPI_QKV) {
+    // rotate-half pairs (i, i+hd/2) sit in adjacent rows (permute_rows_qkv)
+    const int hd = ep.hd, half = hd / 2;
+    const int head = n / hd, p = n % hd, jj = p >> 1;
+    const bool odd = p & 1;
+    const bool rotate = head < ep.n_q + ep.n_kv;
+    const int f = odd ? jj + half : jj;  // original feature inside the head
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float partner = __shfl_xor_sync(0xffffffffu, v[j], 1);
+      const int tt = t0c + j;
+      if (tt >= tokens) continue;
+      const bool batch = tt < ep.n_batch;
+      const int pos = batch ? ep.row_pos[tt] : ep.carry_pos[tt - ep.n_batch];
+      const int slot = batch ? ep.row_slot[tt] : ep.carry_slot[tt - ep.n_batch];
+      float y = v[j];
+      if (rotate) {
+        const float c = ep.rope_cos[static_cast<size_t>(pos) * half + jj];
+        const float sn = ep.rope_sin[static_cast<size_t>(pos) * half + jj];
+        const float x1 = odd ? partner : v[j], x2 = odd ? v[j] : partner;
+        y = odd ? x2 * c + x1 * sn : x1 * c - x2 * sn;
+      }
+      bf16* dst;
+      if (!batch) {
+        dst = ep.ship + static_cast<size_t>(slot) * ep.ship_stride + head * hd;
+      } else if (head < ep.n_q) {
+        dst = ep.qbuf + static_cast<size_t>(tt) * ep.q_row_stride + head * hd;
+      } else {
+        const int kv = head < ep.n_q + ep.n_kv ? 0 : 1;
+        const int kh = head - ep.n_q - kv * ep.n_kv;
+        const int phys = ep.page_table[static_cast<size_t>(slot) * ep.pt_stride + pos / 64];
+        dst = ep.kv_pool + (kv_row(ep.geom, ep.layer, phys, kv, kh) + pos % 64) * hd;
+      }
+      dst[f] = __float2bfloat16(y);
+    }
+  }
+}
+
+template <int BN, bool kBlocked, int Epi>
+__global__ void __launch_bounds__(kGemmThreads, 2)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_w,
                         const __grid_constant__ CUtensorMap map_x, float* __restrict__ out,
-                        int n_out, int tokens, StreamK sk, int planes) {
+                        int n_out, int tokens, StreamK sk, int planes, EpiParams ep) {
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
@@ -183,6 +248,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int n_local = q * 32 + lane;
+    __shared__ int s_last;
     pdl_wait();  // `out` may still be read by the previous kernel
     int seg = 0;
     for (long long u = u_begin; u < u_end; ++seg) {
@@ -193,31 +259,79 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int c_first = sk.owner(t_first);
       const int plane = static_cast<int>(blockIdx.x) - c_first;
       const bool tile_done = seg_end == t_first + sk.kb;  // this CTA finishes the tile
-      const int used = tile_done ? plane + 1 : 0;
       const int n = (t % n_tiles) * kTileM + n_local;
       const int t0 = (t / n_tiles) * BN;
+      const uint32_t tbase = tmem + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
       mbar_wait(&tfull[acc], (seg >> 1) & 1);
       tc_fence_after();
-      float* o = out + static_cast<size_t>(plane) * tokens * n_out + n;
+      const int n_seg = Epi == EPI_PLANES ? 1 : sk.owner(t_first + sk.kb - 1) - c_first + 1;
+      bool fix = true;
+      if (Epi == EPI_PLANES || n_seg > 1) {
+        // publish this segment's fp32 partial plane
+        float* o = out + static_cast<size_t>(plane) * tokens * n_out + n;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        if (t0 + c >= tokens) break;
-        float v[16];
-        tmem_ld16(tmem + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+        for (int c = 0; c < BN; c += 16) {
+          if (t0 + c >= tokens) break;
+          float v[16];
+          tmem_ld16(tbase + c, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int tt = t0 + c + j;
-          if (tt < tokens) o[static_cast<size_t>(tt) * n_out] = v[j];
+          for (int j = 0; j < 16; ++j) {
+            const int tt = t0 + c + j;
+            if (tt < tokens) o[static_cast<size_t>(tt) * n_out] = v[j];
+          }
+        }
+        if (Epi == EPI_PLANES) {
+          fix = false;
+          // zero the planes no CTA covers for this tile
+          for (int p = tile_done ? plane + 1 : planes; p < planes; ++p) {
+            float* z = out + static_cast<size_t>(p) * tokens * n_out + n;
+            for (int tt = t0; tt < min(tokens, t0 + BN); ++tt) z[static_cast<size_t>(tt) * n_out] = 0.f;
+          }
+        } else {
+          // stream-K fixup: the CTA whose segment completes last applies the
+          // epilogue to the sum of all segments (per-tile semaphore)
+          __threadfence();
+          epi_bar();
+          if (threadIdx.x == 64) s_last = atomicAdd(&ep.tile_sem[t], 1) == n_seg - 1;
+          epi_bar();
+          fix = s_last;
+          if (fix) __threadfence();
+        }
+      }
+      if constexpr (Epi != EPI_PLANES) {
+        if (fix) {
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 16) {
+            if (t0 + c >= tokens) break;
+            float v[16];
+            tmem_ld16(tbase + c, v);
+            // other segments' partials, 2 planes of loads in flight at a time
+            for (int p0 = 0; p0 < n_seg; p0 += 2) {
+              float w[2][16];
+#pragma unroll
+              for (int pp = 0; pp < 2; ++pp) {
+                const int p = p0 + pp;
+                const float* o = out + static_cast<size_t>(p) * tokens * n_out + n;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  const int tt = t0 + c + j;
+                  w[pp][j] = (p < n_seg && p != plane && tt < tokens)
+                                 ? __ldcg(o + static_cast<size_t>(tt) * n_out) : 0.f;
+                }
+              }
+#pragma unroll
+              for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] += w[pp][j];
+            }
+            epi_apply<Epi>(ep, n, lane, t0 + c, tokens, v);
+          }
+          if (n_seg > 1 && threadIdx.x == 64) ep.tile_sem[t] = 0;  // ready for the next launch
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      // zero the planes no CTA covers for this tile
-      for (int p = used; tile_done && p < planes; ++p) {
-        float* z = out + static_cast<size_t>(p) * tokens * n_out + n;
-        for (int tt = t0; tt < min(tokens, t0 + BN); ++tt) z[static_cast<size_t>(tt) * n_out] = 0.f;
-      }
       u = seg_end;
     }
   }
@@ -313,13 +427,14 @@ int gemm_pick_splits(int n_out, int k, int tokens, int bn, int max_splits) {
   return planes;
 }
 
-template <int BN, bool kBlocked>
+template <int BN, bool kBlocked, int Epi>
 static int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, float* out, int n_out,
-                     int tokens, const StreamK& sk, int planes, cudaStream_t st) {
+                     int tokens, const StreamK& sk, int planes, const EpiParams& ep,
+                     cudaStream_t st) {
   using C = GemmCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, kBlocked>,
+    cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, kBlocked, Epi>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     attr_set = true;
   }
@@ -333,22 +448,23 @@ static int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, float* out, i
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, kBlocked>, mw, mx, out, n_out, tokens, sk,
-                     planes);
+  cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, kBlocked, Epi>, mw, mx, out, n_out, tokens,
+                     sk, planes, ep);
   return launched();
 }
 
 // `max_planes`: partial planes the output buffer holds; the planes actually
 // written (all of them, zero-filled where unused) are returned in *planes.
-template <bool kBlocked>
+template <bool kBlocked, int Epi>
 static int launch_any(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,
-                      int tokens, const StreamK& sk, int planes, cudaStream_t st) {
+                      int tokens, const StreamK& sk, int planes, const EpiParams& ep,
+                      cudaStream_t st) {
   switch (bn) {
-    case 16: return launch_bn<16, kBlocked>(mw, mx, out, n_out, tokens, sk, planes, st);
-    case 32: return launch_bn<32, kBlocked>(mw, mx, out, n_out, tokens, sk, planes, st);
-    case 64: return launch_bn<64, kBlocked>(mw, mx, out, n_out, tokens, sk, planes, st);
-    case 128: return launch_bn<128, kBlocked>(mw, mx, out, n_out, tokens, sk, planes, st);
-    case 256: return launch_bn<256, kBlocked>(mw, mx, out, n_out, tokens, sk, planes, st);
+    case 16: return launch_bn<16, kBlocked, Epi>(mw, mx, out, n_out, tokens, sk, planes, ep, st);
+    case 32: return launch_bn<32, kBlocked, Epi>(mw, mx, out, n_out, tokens, sk, planes, ep, st);
+    case 64: return launch_bn<64, kBlocked, Epi>(mw, mx, out, n_out, tokens, sk, planes, ep, st);
+    case 128: return launch_bn<128, kBlocked, Epi>(mw, mx, out, n_out, tokens, sk, planes, ep, st);
+    case 256: return launch_bn<256, kBlocked, Epi>(mw, mx, out, n_out, tokens, sk, planes, ep, st);
   }
   return HS_E_CONFIG;
 }
@@ -359,8 +475,51 @@ int gemm_launch(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out
   if (tokens <= 0) return HS_OK;
   if (n_out % kTileM || k % kTileK) return HS_E_CONFIG;
   const StreamK sk = choose_streamk(n_out, k, tokens, bn, max_planes, planes);
-  return blocked ? launch_any<true>(mw, mx, bn, out, n_out, tokens, sk, *planes, st)
-                 : launch_any<false>(mw, mx, bn, out, n_out, tokens, sk, *planes, st);
+  const EpiParams ep{};
+  return blocked ? launch_any<true, EPI_PLANES>(mw, mx, bn, out, n_out, tokens, sk, *planes, ep, st)
+                 : launch_any<false, EPI_PLANES>(mw, mx, bn, out, n_out, tokens, sk, *planes, ep, st);
+}
+
+int gemm_launch_fused(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* scratch,
+                      int n_out, int tokens, int k, int max_planes, int epi, const EpiParams& ep,
+                      cudaStream_t st) {
+  if (tokens <= 0) return HS_OK;
+  if (n_out % kTileM || k % kTileK) return HS_E_CONFIG;
+  int planes = 1;
+  const StreamK sk = choose_streamk(n_out, k, tokens, bn, max_planes, &planes);
+  switch (epi) {
+    case EPI_RESID:
+      return launch_any<false, EPI_RESID>(mw, mx, bn, scratch, n_out, tokens, sk, planes, ep, st);
+    case EPI_SILU:
+      return launch_any<false, EPI_SILU>(mw, mx, bn, scratch, n_out, tokens, sk, planes, ep, st);
+    case EPI_QKV:
+      return launch_any<false, EPI_QKV>(mw, mx, bn, scratch, n_out, tokens, sk, planes, ep, st);
+  }
+  return HS_E_CONFIG;
+}
+
+// Row permutations that put each fused epilogue's operand pair in one warp:
+//   gate-up: 32-row groups [16 gate rows | 16 up rows] of the same features
+//   qkv:     inside every head, rows (2j, 2j+1) = features (j, j + hd/2)
+__global__ void permute_rows_kernel(const bf16* __restrict__ src, bf16* __restrict__ dst,
+                                    int rows, int k, int kind, int a, int b) {
+  const int p = blockIdx.x;  // destination row
+  int o;
+  if (kind == 0) {  // gate-up: a = ffn
+    const int blk = p / 32, i = p % 32;
+    o = i < 16 ? 16 * blk + i : a + 16 * blk + (i - 16);
+  } else {  // qkv: a = head_dim
+    const int head = p / a, r = p % a;
+    o = head * a + ((r & 1) ? (r >> 1) + a / 2 : (r >> 1));
+  }
+  const int4* s = reinterpret_cast<const int4*>(src + static_cast<size_t>(o) * k);
+  int4* d = reinterpret_cast<int4*>(dst + static_cast<size_t>(p) * k);
+  for (int i = threadIdx.x; i < k / 8; i += blockDim.x) d[i] = s[i];
+}
+
+int permute_rows(const bf16* src, bf16* dst, int rows, int k, int kind, int a, cudaStream_t st) {
+  return launch_pdl(permute_rows_kernel, dim3(rows), dim3(128), 0, st, src, dst, rows, k, kind, a,
+                    0);
 }
 
 // Row-major [n][k] -> blocked [n/128][k/64][128][64] (one thread per 16 B).

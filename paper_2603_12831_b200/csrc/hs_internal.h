@@ -43,6 +43,48 @@ inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
   return launched();
 }
 
+// ---- KV pool geometry (used by GEMM epilogues and attention) ----
+struct KvGeom {
+  int layers, pages, n_kv, head_dim;
+};
+__host__ __device__ inline int64_t kv_row(const KvGeom& g, int layer, int page, int kv, int head) {
+  return ((((int64_t)layer * g.pages + page) * 2 + kv) * g.n_kv + head) * 64;
+}
+
+// ---- GEMM fused epilogues (stream-K fixup, gemm_tcgen05.cu) ----
+enum { EPI_PLANES = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_QKV = 3 };
+struct EpiParams {
+  int* tile_sem;  // per-tile semaphores (zeroed once; self-resetting)
+  // EPI_RESID: h[t][n] += y
+  float* h;
+  int ld_h;
+  // EPI_SILU: act[t][f] = silu(gate) * up (weights permuted, see permute_rows)
+  bf16* act;
+  int ld_act;
+  // EPI_QKV: RoPE + KV-page scatter (rows < n_batch) / piggyback ship (carry rows)
+  const float* rope_cos;
+  const float* rope_sin;
+  const int* row_pos;
+  const int* row_slot;
+  int n_batch;
+  const int* carry_pos;
+  const int* carry_slot;
+  bf16* qbuf;
+  int q_row_stride;
+  bf16* kv_pool;
+  KvGeom geom;
+  int layer;
+  const int* page_table;
+  int pt_stride;
+  bf16* ship;
+  int ship_stride;
+  int n_q, n_kv, hd;
+};
+int gemm_launch_fused(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* scratch,
+                      int n_out, int tokens, int k, int max_planes, int epi, const EpiParams& ep,
+                      cudaStream_t st);
+int permute_rows(const bf16* src, bf16* dst, int rows, int k, int kind, int a, cudaStream_t st);
+
 // ---- TMA maps / GEMM (gemm_tcgen05.cu) ----
 int make_map_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                      uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
@@ -59,14 +101,7 @@ int gemm_launch(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out
 int relayout_blocked(const bf16* src, bf16* dst, int n, int k, cudaStream_t st);
 int make_weight_map_blocked(CUtensorMap* map, const bf16* w, int n_out, int k);
 
-// ---- KV pool geometry ----
-// pool layout: [layers][pages][2 (K,V)][n_kv][64 tokens][head_dim] bf16
-struct KvGeom {
-  int layers, pages, n_kv, head_dim;
-};
-__host__ __device__ inline int64_t kv_row(const KvGeom& g, int layer, int page, int kv, int head) {
-  return ((((int64_t)layer * g.pages + page) * 2 + kv) * g.n_kv + head) * 64;
-}
+// ---- KV pool: [layers][pages][2 (K,V)][n_kv][64 tokens][head_dim] bf16 ----
 int make_kv_map(CUtensorMap* map, const bf16* pool, const KvGeom& g);
 
 // ---- attention (attn_decode.cu / attn_prefill.cu) ----
@@ -118,9 +153,9 @@ int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv,
                      const int* row_slot, const int* row_mode, int n_batch, const int* carry_pos,
                      const int* carry_slot, bf16* qbuf, int q_row_stride, bf16* kv_pool,
                      const KvGeom& g, int layer, const int* page_table, int pt_stride, bf16* ship,
-                     int ship_stride, cudaStream_t st);
+                     int ship_stride, cudaStream_t st, int permuted = 0);
 int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld_act,
-             cudaStream_t st);
+             cudaStream_t st, int permuted = 0);
 int argmax_rows(const float* part, int splits, int rows, int vocab, int* tokens, float* logits_out,
                 cudaStream_t st);
 int lse_merge_rows(const bf16* parts, const float* lse, int n_parts, int rows, int n_q,

@@ -101,6 +101,7 @@ struct hs_ctx {
             *it_cbeg = nullptr, *it_tiles = nullptr;
   std::vector<int> h_logit_rows, h_logit_slots;  // host copies (layer-L gather lists)
   int* dec_counters = nullptr;
+  int* tile_sem = nullptr;  // stream-K fixup semaphores of the fused GEMMs
   int* tokens_pinned = nullptr;
   // piggyback mailboxes (pinned, mapped)
   bf16 *ship_h = nullptr, *ship_d = nullptr, *result_h = nullptr, *result_d = nullptr;
@@ -268,6 +269,56 @@ int gemm(hs_ctx* c, const CUtensorMap& mw, const ActBuf& x, int tokens, int n_ou
                      splits_out);
 }
 
+// GEMM with an epilogue fused into its stream-K fixup (no partial planes
+// leave the kernel); the split-K buffer is scratch for multi-segment tiles.
+int gemm_fused(hs_ctx* c, const CUtensorMap& mw, const ActBuf& x, int tokens, int n_out, int k,
+               int epi, const EpiParams& ep) {
+  if (tokens <= 0) return HS_OK;
+  const int bn = gemm_pick_bn(tokens);
+  const size_t per_split = static_cast<size_t>(tokens) * n_out;
+  const int cap = static_cast<int>(std::min<size_t>(16, c->part_floats / per_split));
+  if (cap < 1) return set_error(HS_E_CAPACITY, "split-K buffer too small for %d x %d", tokens, n_out);
+  ProfScope ps(c, 0, 2.0 * n_out * k + 2.0 * tokens * k + 2.0 * tokens * n_out,
+               2.0 * tokens * n_out * k);
+  return gemm_launch_fused(mw, x.maps[bn_index(bn)], bn, c->part, n_out, tokens, k, cap, epi, ep,
+                           c->st);
+}
+
+// A fused epilogue pays a serial fixup that reads every other K-segment of
+// the tile; beyond a few segments the parallel glue kernel is faster.
+constexpr int kFuseMaxSegments = 1;  // measured: a fixup on the critical path loses at small M
+
+bool fuse_ok(hs_ctx* c, int tokens, int n_out, int k) {
+  if (tokens <= 0) return true;  // nothing to launch either way
+  const int bn = gemm_pick_bn(tokens);
+  const size_t per_split = static_cast<size_t>(tokens) * n_out;
+  const int cap = static_cast<int>(std::min<size_t>(16, c->part_floats / per_split));
+  return gemm_pick_splits(n_out, k, tokens, bn, cap) <= kFuseMaxSegments;
+}
+
+EpiParams epi_base(hs_ctx* c) {
+  EpiParams ep{};
+  ep.tile_sem = c->tile_sem;
+  ep.h = c->h;
+  ep.ld_h = c->m.d;
+  ep.act = c->act.p;
+  ep.ld_act = c->m.ffn;
+  ep.rope_cos = c->rope_cos;
+  ep.rope_sin = c->rope_sin;
+  ep.qbuf = c->qbuf;
+  ep.q_row_stride = c->m.n_q * c->m.hd;
+  ep.kv_pool = c->kv_pool;
+  ep.geom = c->geom;
+  ep.page_table = c->page_table;
+  ep.pt_stride = c->r.max_pages_per_req;
+  ep.ship = c->ship_d;
+  ep.ship_stride = c->m.qkv_n();
+  ep.n_q = c->m.n_q;
+  ep.n_kv = c->m.n_kv;
+  ep.hd = c->m.hd;
+  return ep;
+}
+
 int* stage(hs_ctx* c, size_t n) {
   // pinned staging ring: half per iteration, guarded by the event of the
   // iteration that last used it
@@ -426,6 +477,7 @@ void free_all(hs_ctx* c) {
   F(c->dm_iter);
   F(c->dm_layer);
   F(c->dec_counters);
+  F(c->tile_sem);
   if (c->hm) cudaFreeHost(c->hm);
   if (c->tokens_pinned) cudaFreeHost(c->tokens_pinned);
   if (c->ship_h) cudaFreeHost(c->ship_h);
@@ -523,6 +575,13 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
   RC(dalloc(&c->dm_iter, c->iter_cap));
   RC(dalloc(&c->dm_layer, c->layer_cap));
   RC(dalloc(&c->dec_counters, R * m.n_kv));
+  {
+    const size_t max_n = std::max<size_t>(std::max<size_t>(m.qkv_n(), 2 * m.ffn),
+                                          std::max<size_t>(m.d, m.vocab));
+    const size_t tiles = (max_n / 128) * ((R + 15) / 16);
+    RC(dalloc(&c->tile_sem, tiles));
+    CK(cudaMemset(c->tile_sem, 0, tiles * sizeof(int)));
+  }
   CK(cudaMemset(c->dec_counters, 0, R * m.n_kv * sizeof(int)));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hm), 2 * c->meta_ints * sizeof(int),
                    cudaHostAllocDefault));
@@ -720,6 +779,19 @@ int hs_set_weight(hs_ctx* c, int kind, int layer, const void* host, size_t bytes
     default: return set_error(HS_E_CONFIG, "unknown weight kind %d", kind);
   }
   if (bytes != want) return set_error(HS_E_CONFIG, "weight %d: %zu bytes, want %zu", kind, bytes, want);
+  if (kind == HS_W_QKV || kind == HS_W_GATE_UP) {
+    // rows reordered for the fused epilogues (see permute_rows)
+    bf16* tmp = nullptr;
+    CK(cudaMalloc(reinterpret_cast<void**>(&tmp), bytes));
+    CK(cudaMemcpy(tmp, host, bytes, cudaMemcpyHostToDevice));
+    const int rows = kind == HS_W_QKV ? m.qkv_n() : 2 * m.ffn;
+    const int rc = permute_rows(tmp, static_cast<bf16*>(dst), rows, m.d,
+                                kind == HS_W_QKV ? 1 : 0, kind == HS_W_QKV ? m.hd : m.ffn, c->st);
+    CK(cudaStreamSynchronize(c->st));
+    cudaFree(tmp);
+    if (rc != HS_OK) return set_error(HS_E_CUDA, "weight permutation failed");
+    return HS_OK;
+  }
   CK(cudaMemcpy(dst, host, bytes, cudaMemcpyHostToDevice));
   return HS_OK;
 }
@@ -926,12 +998,24 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
     RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, carry_slot, C, d_, c->resid, st));
     RC(rmsnorm_rows(c->h, B + C, d_, c->n_in[0], m.eps, c->xn.p, d_, st));
   }
-  // QKV over batch + carry rows, RoPE, KV scatter / piggyback ship
-  RC(gemm(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, &sp));
-  RC(qkv_rope_scatter(c->part, sp, B + C, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
-                      c->it_pos, c->it_slot, nullptr, B, carry_pos, carry_slot, c->qbuf, nqh,
-                      c->kv_pool, c->geom, l, c->page_table, r.max_pages_per_req, c->ship_d,
-                      m.qkv_n(), st));
+  // QKV over batch + carry rows with RoPE, KV-page scatter and the piggyback
+  // ship fused into the GEMM epilogue
+  EpiParams ep = epi_base(c);
+  ep.layer = l;
+  ep.row_pos = c->it_pos;
+  ep.row_slot = c->it_slot;
+  ep.n_batch = B;
+  ep.carry_pos = carry_pos;
+  ep.carry_slot = carry_slot;
+  if (fuse_ok(c, B + C, m.qkv_n(), d_)) {
+    RC(gemm_fused(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, EPI_QKV, ep));
+  } else {
+    RC(gemm(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, &sp));
+    RC(qkv_rope_scatter(c->part, sp, B + C, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
+                        c->it_pos, c->it_slot, nullptr, B, carry_pos, carry_slot, c->qbuf, nqh,
+                        c->kv_pool, c->geom, l, c->page_table, r.max_pages_per_req, c->ship_d,
+                        m.qkv_n(), st, 1));
+  }
   // attention of batch rows (K1 with the K2 merge fused into its last CTA)
   {
   ProfScope pd(c, 1, c->dec_kv_tokens * 2.0 * m.n_kv * m.hd * 2.0 + 4.0 * c->D * nqh,
@@ -952,15 +1036,31 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
                       c->attn.p + static_cast<size_t>(B) * nqh, nqh, st));
   RC(gather_rows_f32(c->resid, merge_slot, M, d_, c->h + static_cast<size_t>(B) * d_, st));
   const int N = B + M;
-  // Proj + ResidualAdd
-  RC(gemm(c, c->m_o[l], c->attn, N, d_, nqh, &sp));
-  RC(residual_add_norm(c->part, sp, N, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, st));
-  // MLP + ResidualAdd (+ next layer's input norm, or the final norm)
-  RC(gemm(c, c->m_gu[l], c->xn2, N, 2 * m.ffn, d_, &sp));
-  RC(silu_mul(c->part, sp, N, m.ffn, c->act.p, m.ffn, st));
-  RC(gemm(c, c->m_down[l], c->act, N, d_, m.ffn, &sp));
-  RC(residual_add_norm(c->part, sp, N, d_, c->h, last ? c->w_final : c->n_in[l + 1], m.eps,
-                       c->xn.p, d_, st));
+  // Proj + ResidualAdd + RMSNorm (residual add fused into the GEMM when the
+  // tiles have few K-segments)
+  if (fuse_ok(c, N, d_, nqh)) {
+    RC(gemm_fused(c, c->m_o[l], c->attn, N, d_, nqh, EPI_RESID, ep));
+    RC(rmsnorm_rows(c->h, N, d_, c->n_post[l], m.eps, c->xn2.p, d_, st));
+  } else {
+    RC(gemm(c, c->m_o[l], c->attn, N, d_, nqh, &sp));
+    RC(residual_add_norm(c->part, sp, N, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, st));
+  }
+  // MLP: SiLU*up, down + ResidualAdd, then the next layer's input norm (or the
+  // final norm)
+  if (fuse_ok(c, N, 2 * m.ffn, d_)) {
+    RC(gemm_fused(c, c->m_gu[l], c->xn2, N, 2 * m.ffn, d_, EPI_SILU, ep));
+  } else {
+    RC(gemm(c, c->m_gu[l], c->xn2, N, 2 * m.ffn, d_, &sp));
+    RC(silu_mul(c->part, sp, N, m.ffn, c->act.p, m.ffn, st, 1));
+  }
+  const float* w_next = last ? c->w_final : c->n_in[l + 1];
+  if (fuse_ok(c, N, d_, m.ffn)) {
+    RC(gemm_fused(c, c->m_down[l], c->act, N, d_, m.ffn, EPI_RESID, ep));
+    RC(rmsnorm_rows(c->h, N, d_, w_next, m.eps, c->xn.p, d_, st));
+  } else {
+    RC(gemm(c, c->m_down[l], c->act, N, d_, m.ffn, &sp));
+    RC(residual_add_norm(c->part, sp, N, d_, c->h, w_next, m.eps, c->xn.p, d_, st));
+  }
   if (!last) {
     // residual put for the chains' next layer (engine.py:985)
     RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, merge_slot, M, d_, c->resid, st));
@@ -980,10 +1080,20 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
     RC(embed_gather(c->tok, R, c->w_embed, d_, c->hr, st));
     RC(scatter_rows_f32(c->hr, restart_slot, R, d_, c->resid, st));
     RC(rmsnorm_rows(c->hr, R, d_, c->n_in[0], m.eps, c->xr.p, d_, st));
-    RC(gemm(c, c->m_qkv[0], c->xr, R, m.qkv_n(), d_, &sp));
-    RC(qkv_rope_scatter(c->part, sp, R, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin, nullptr,
-                        nullptr, nullptr, 0, restart_pos, restart_slot, c->qbuf, nqh, c->kv_pool,
-                        c->geom, 0, c->page_table, r.max_pages_per_req, c->ship_d, m.qkv_n(), st));
+    EpiParams er = epi_base(c);
+    er.layer = 0;
+    er.n_batch = 0;
+    er.carry_pos = restart_pos;
+    er.carry_slot = restart_slot;
+    if (fuse_ok(c, R, m.qkv_n(), d_)) {
+      RC(gemm_fused(c, c->m_qkv[0], c->xr, R, m.qkv_n(), d_, EPI_QKV, er));
+    } else {
+      RC(gemm(c, c->m_qkv[0], c->xr, R, m.qkv_n(), d_, &sp));
+      RC(qkv_rope_scatter(c->part, sp, R, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin, nullptr,
+                          nullptr, nullptr, 0, restart_pos, restart_slot, c->qbuf, nqh,
+                          c->kv_pool, c->geom, 0, c->page_table, r.max_pages_per_req, c->ship_d,
+                          m.qkv_n(), st, 1));
+    }
   }
   return HS_OK;
 }
@@ -1113,14 +1223,44 @@ int hs_probe_dense(hs_ctx* c, int n, int reps, float* us) {
   const int d_ = m.d, nqh = m.n_q * m.hd;
   return time_reps(c, reps, [&]() -> int {
     int sp;
-    RC(gemm(c, c->m_qkv[0], c->xn, n, m.qkv_n(), d_, &sp));
-    RC(gemm(c, c->m_o[0], c->attn, n, d_, nqh, &sp));
-    RC(residual_add_norm(c->part, sp, n, d_, c->h, c->n_post[0], m.eps, c->xn2.p, d_, c->st));
-    RC(gemm(c, c->m_gu[0], c->xn2, n, 2 * m.ffn, d_, &sp));
-    RC(silu_mul(c->part, sp, n, m.ffn, c->act.p, m.ffn, c->st));
-    RC(gemm(c, c->m_down[0], c->act, n, d_, m.ffn, &sp));
-    RC(residual_add_norm(c->part, sp, n, d_, c->h, c->n_in[0], m.eps, c->xn.p, d_, c->st));
+    EpiParams ep = epi_base(c);
+    RC(gemm(c, c->m_qkv[0], c->xn, n, m.qkv_n(), d_, &sp));  // (+ a RoPE epilogue in the layer)
+    RC(gemm_fused(c, c->m_o[0], c->attn, n, d_, nqh, EPI_RESID, ep));
+    RC(rmsnorm_rows(c->h, n, d_, c->n_post[0], m.eps, c->xn2.p, d_, c->st));
+    RC(gemm_fused(c, c->m_gu[0], c->xn2, n, 2 * m.ffn, d_, EPI_SILU, ep));
+    RC(gemm_fused(c, c->m_down[0], c->act, n, d_, m.ffn, EPI_RESID, ep));
+    RC(rmsnorm_rows(c->h, n, d_, c->n_in[0], m.eps, c->xn.p, d_, c->st));
     return HS_OK;
+  }, us);
+}
+
+// one GEMM of layer 0: which 0=qkv 1=o 2=gate_up 3=down; fused 0=planes 1=fused epilogue
+int hs_probe_gemm(hs_ctx* c, int which, int n, int fused, int reps, float* us) {
+  const ModelCfg& m = c->m;
+  if (n < 1 || n > c->r.max_rows) return set_error(HS_E_CONFIG, "probe rows out of range");
+  const int d_ = m.d, nqh = m.n_q * m.hd;
+  EpiParams ep = epi_base(c);
+  // QKV epilogue as a pure ship of n carry rows (slot 0, position 0)
+  CK(cudaMemset(c->dm_layer, 0, 2 * static_cast<size_t>(n) * sizeof(int)));
+  ep.n_batch = 0;
+  ep.carry_slot = c->dm_layer;
+  ep.carry_pos = c->dm_layer + n;
+  return time_reps(c, reps, [&]() -> int {
+    int sp;
+    switch (which) {
+      case 0:
+        return fused ? gemm_fused(c, c->m_qkv[0], c->xn, n, m.qkv_n(), d_, EPI_QKV, ep)
+                     : gemm(c, c->m_qkv[0], c->xn, n, m.qkv_n(), d_, &sp);
+      case 1:
+        return fused ? gemm_fused(c, c->m_o[0], c->attn, n, d_, nqh, EPI_RESID, ep)
+                     : gemm(c, c->m_o[0], c->attn, n, d_, nqh, &sp);
+      case 2:
+        return fused ? gemm_fused(c, c->m_gu[0], c->xn2, n, 2 * m.ffn, d_, EPI_SILU, ep)
+                     : gemm(c, c->m_gu[0], c->xn2, n, 2 * m.ffn, d_, &sp);
+      default:
+        return fused ? gemm_fused(c, c->m_down[0], c->act, n, d_, m.ffn, EPI_RESID, ep)
+                     : gemm(c, c->m_down[0], c->act, n, d_, m.ffn, &sp);
+    }
   }, us);
 }
 
