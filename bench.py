@@ -104,19 +104,22 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- workload
-def scenario_doc(args, cores: int) -> dict:
+def scenario_doc(args, cores: int, ls_rate: float = None) -> dict:
+    from paper_2603_12831_b200.models import get_transformer
+
+    ls_rate = args.ls_rate if ls_rate is None else ls_rate
     return {
         "model": "34B", "policy": "omniserve", "horizon_s": 3600.0, "seed": args.seed,
         "transformer": args.config,
         "profiles": {"cluster": {
-            "layers": 32, "gpu_count": 1, "tp_degree": 1, "cpu_hosts": 1,
+            "layers": get_transformer(args.config).n_layers, "gpu_count": 1, "tp_degree": 1, "cpu_hosts": 1,
             "gpu_kv_capacity": args.gpu_kv_tokens, "cpu_mem_tokens": 10_000_000,
             "cpu_cores_per_host": cores, "max_piggyback_per_layer": args.max_piggyback,
             "merge_cost_per_result": 0.5}},
         "slo": {"ttft_s": TTFT_SLO_S, "tpot_s": TPOT_SLO_S,
                 "piggyback_reserve_us": args.piggyback_reserve_us},
         "engine": {"events": False},
-        "workload": {"seed": args.seed, "ls": {"rate": args.ls_rate,
+        "workload": {"seed": args.seed, "ls": {"rate": ls_rate,
                                                "lengths": {"source": "sharegpt"}}},
     }
 
@@ -327,23 +330,34 @@ def run_ours(args) -> None:
         torch.cuda.set_device(local)
         dist.init_process_group("gloo")
 
-    from paper_2603_12831_b200 import profiler
+    from paper_2603_12831_b200 import profiler, replicas
     from paper_2603_12831_b200.live import LiveEngine
     from paper_2603_12831_b200.models import get_transformer
     from paper_2603_12831_b200.runtime import LiveCudaStep, RuntimeConfig
     from paper_2603_12831_b200.scenario import scenario_from_dict
 
     model = get_transformer(args.config)
-    ncpu = os.cpu_count() or 8
-    cores = max(2, ncpu // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
-    doc = scenario_doc(args, cores)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    # the replica's CPU-attention cores: its GPU's NUMA node, split among the
+    # GPUs on that node; two cores stay free for the engine thread
+    cpus = replicas.core_set(local, local_world)
+    workers = cpus[:-2] if len(cpus) > 3 else cpus[:1]
+    cores = len(cpus)
+    if args.route == "round_robin":
+        # one global trace (world x the per-GPU LS rate) split over replicas
+        doc = scenario_doc(args, cores, ls_rate=args.ls_rate * world)
+    else:
+        # independent per-replica traces (config 3: replica r uses seed + r)
+        doc = scenario_doc(args, cores)
+        doc["seed"] = doc["workload"]["seed"] = replicas.replica_seed(args.seed, rank)
     scenario = scenario_from_dict(doc, "bench")
     be_cap_tokens = 13000 + 400
     rt = RuntimeConfig(max_rows=args.max_rows, max_slots=512,
                        kv_pages=args.gpu_kv_tokens // 64 + 512 + 64, max_pages_per_req=256,
-                       max_pos=16384, max_chunks=8192, cpu_threads=max(1, cores - 2),
+                       max_pos=16384, max_chunks=8192, cpu_threads=len(workers),
                        host_kv_bytes=(args.be_chains + 4) * be_cap_tokens
-                       * model.kv_bytes_per_token_layer * model.n_layers, device=local)
+                       * model.kv_bytes_per_token_layer * model.n_layers, device=local,
+                       cpu_list=tuple(workers) if args.pin else ())
     t_setup = time.perf_counter()
     step = LiveCudaStep(model, rt, weight_seed=args.seed)
     models_path = ROOT / "profiles" / f"b200_{args.config}_models.json"
@@ -363,7 +377,10 @@ def run_ours(args) -> None:
         prepopulate_ls(engine, step, args.ls_decodes, args.seed + rank)
     from paper_2603_12831_b200.workload import build_requests
 
-    arrivals = engine.admit_specs(build_requests(scenario.workload, 600.0))
+    trace = build_requests(scenario.workload, 600.0)
+    if args.route == "round_robin":
+        trace = replicas.route(trace, world)[rank]
+    arrivals = engine.admit_specs(trace)
     setup_s = time.perf_counter() - t_setup
     engine.t0 = time.perf_counter()
     step.set_anchor(engine.clock())
@@ -420,19 +437,14 @@ def run_ours(args) -> None:
     m = window_metrics(engine, w0, w1)
     wall_s = host_w1 - host_w0
     stats = np.array(list(prof), dtype=np.float64).reshape(4, 4)
-    tot = np.array([m["be_tokens"], m["ls_tokens"], device_s, wall_s, stats[0, 1], stats[0, 2],
-                    stats[0, 0], stats[0, 3], launches], dtype=np.float64)
-    if dist:
-        import torch
-
-        t = torch.tensor(tot)
-        mx = torch.tensor([device_s, wall_s])
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        tot = t.numpy()
-        device_max, wall_max = float(mx[0]), float(mx[1])
-    else:
-        device_max, wall_max = device_s, wall_s
+    # whole job: tokens, LS gaps and launches summed over replicas; device and
+    # wall windows and the LS p99 maxed (the slowest replica bounds the job)
+    tot, mx = replicas.aggregate(
+        [m["be_tokens"], m["ls_tokens"], launches, m["ls_gaps"],
+         m["tpot_attainment"] * m["ls_gaps"]],
+        [device_s, wall_s, m["tpot_p99_ms"] or 0.0], dist)
+    device_max, wall_max = float(mx[0]), float(mx[1])
+    attain = tot[4] / tot[3] if tot[3] else 1.0
     if rank != 0:
         return
     pk = peaks()
@@ -476,9 +488,9 @@ def run_ours(args) -> None:
                    "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
                    "cpu_threads_per_replica": rt.cpu_threads, "parallelism": f"replicas x{world}",
                    "l2": "working set (16 GB weights/iteration) > 126 MB L2"},
-        "ls_tpot_attainment": m["tpot_attainment"], "ls_tpot_p99_ms": m["tpot_p99_ms"],
-        "ls_tokens": int(tot[1]), "be_tokens": int(tot[0]), "ls_gaps": m["ls_gaps"],
-        "slo_met": m["tpot_attainment"] >= 0.99,
+        "ls_tpot_attainment": attain, "ls_tpot_p99_ms": float(mx[2]),
+        "ls_tokens": int(tot[1]), "be_tokens": int(tot[0]), "ls_gaps": int(tot[3]),
+        "slo_met": attain >= 0.99,
         "merges": n_merges, "avg_batch_tokens": avg_rows,
         "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters
                                               if i.get("device_ms")) if iters else None,
@@ -493,7 +505,7 @@ def run_ours(args) -> None:
         "e2e": {"value": e2e_val, "unit": UNIT,
                 "h2d_bytes_per_step": (h2d1 - h2d0) / max(args.steps, 1),
                 "d2h_bytes_per_step": (d2h1 - d2h0) / max(args.steps, 1)},
-        "gpu_launches": int(tot[8]),
+        "gpu_launches": int(tot[2]),
         "clocks": clocks.summary(),
         "setup_s": setup_s,
     }
@@ -537,6 +549,9 @@ def main() -> None:
     ap.add_argument("--calibrate", action="store_true")
     ap.add_argument("--calibrate-out", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--route", default="seeded", choices=["seeded", "round_robin"],
+                    help="N>1: per-replica seeded traces, or one global trace routed")
+    ap.add_argument("--pin", type=int, default=1, help="pin CPU-attention workers")
     ap.add_argument("--profile-steps", type=int, default=160,
                     help="profiled iterations after the timed region (roofline, breakdown)")
     ap.add_argument("--ref-ls-rows", type=int, default=8)

@@ -162,6 +162,12 @@ typedef struct {
   int cpu_threads;       /* CPU attention workers of this replica               */
   int64_t host_kv_bytes; /* pinned host KV arena (offloaded BE requests)        */
   int device;
+  /* the replica's CPU-attention core set (NUMA node of `device`, split among
+     the GPUs on that node; "private queues, equal CPU share").
+     Workers are pinned to these cores and the pinned host arenas are
+     first-touched from them.  NULL / 0 = no pinning. */
+  const int* cpu_list;
+  int n_cpu_list;
 } hs_rt_cfg;
 
 enum {

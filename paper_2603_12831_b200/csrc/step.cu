@@ -17,6 +17,9 @@
 //
 // All launches go to one stream; nothing here blocks on the host except
 // hs_iter_end (token readback) and hs_cpu_attend (replay-mode service).
+#include <pthread.h>
+#include <sched.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -111,6 +114,7 @@ struct hs_ctx {
   std::vector<HostRegion> regions;
   std::vector<std::pair<size_t, size_t>> free_list;  // (offset, bytes)
   ThreadPool* pool = nullptr;
+  std::vector<int> cpus;  // the replica's CPU-attention core set (empty: unpinned)
   CpuService* cpu = nullptr;
   // swaps: copy stream + contiguous staging for pack/unpack around one 2D DMA
   cudaStream_t copy_st = nullptr;
@@ -504,6 +508,24 @@ void free_all(hs_ctx* c) {
   delete c->pool;
 }
 
+// Pins the calling thread to `cpus` for its lifetime so that pages it
+// first-touches (cudaHostAlloc pins and zero-fills them) land on that NUMA
+// node under the default local-allocation policy.
+struct AffinityScope {
+  cpu_set_t saved;
+  bool active = false;
+  explicit AffinityScope(const std::vector<int>& cpus) {
+    if (cpus.empty() || pthread_getaffinity_np(pthread_self(), sizeof(saved), &saved)) return;
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    for (int cpu : cpus) CPU_SET(cpu, &set);
+    active = pthread_setaffinity_np(pthread_self(), sizeof(set), &set) == 0;
+  }
+  ~AffinityScope() {
+    if (active) pthread_setaffinity_np(pthread_self(), sizeof(saved), &saved);
+  }
+};
+
 int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
   ModelCfg& m = c->m;
   m = ModelCfg{mc->d_model, mc->n_layers, mc->n_q, mc->n_kv, mc->head_dim, mc->ffn, mc->vocab,
@@ -583,6 +605,12 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
     CK(cudaMemset(c->tile_sem, 0, tiles * sizeof(int)));
   }
   CK(cudaMemset(c->dec_counters, 0, R * m.n_kv * sizeof(int)));
+  // host allocations below are first-touched on the replica's NUMA node
+  c->cpus.assign(r.cpu_list, r.cpu_list + (r.cpu_list ? r.n_cpu_list : 0));
+  c->r.cpu_list = nullptr;  // the caller's array is not retained
+  for (int cpu : c->cpus)
+    if (cpu < 0 || cpu >= CPU_SETSIZE) return set_error(HS_E_CONFIG, "cpu_list entry %d invalid", cpu);
+  AffinityScope near(c->cpus);
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hm), 2 * c->meta_ints * sizeof(int),
                    cudaHostAllocDefault));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->tokens_pinned), 2 * R * sizeof(int),
@@ -603,7 +631,7 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
     CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hkv_d), c->hkv_h, 0));
     c->free_list.push_back({0, c->hkv_bytes});
   }
-  c->pool = new ThreadPool(std::max(0, r.cpu_threads - 1));
+  c->pool = new ThreadPool(std::max(0, r.cpu_threads - 1), c->cpus);
   int lo = 0, hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   CK(cudaStreamCreateWithPriority(&c->copy_st, cudaStreamNonBlocking, lo));
@@ -626,7 +654,7 @@ bf16* host_region(hs_ctx* c, int slot) {
 int ensure_cpu_service(hs_ctx* c) {
   if (c->cpu) return HS_OK;
   if (c->r.cpu_threads <= 0) return set_error(HS_E_CONFIG, "no CPU attention threads configured");
-  c->cpu = make_cpu_service(c->m, c->r.cpu_threads, {});
+  c->cpu = make_cpu_service(c->m, c->r.cpu_threads, c->cpus);
   const int qkv = c->m.qkv_n(), nqh = c->m.n_q * c->m.hd;
   cpu_service_bind(
       c->cpu, [c, qkv](int s) { return c->ship_h + static_cast<size_t>(s) * qkv; },

@@ -547,9 +547,13 @@ class Engine(PlannerMixin):
             else:
                 self._finish_swap_in(req)
 
-    def run(self) -> SimReport:
+    def run(self, specs=None) -> SimReport:
+        """Simulate to the horizon.  `specs` replaces the scenario's generated
+        trace (a replica's share of a routed trace, replicas.route)."""
         horizon = self.scenario.horizon_s
-        for spec in build_requests(self.scenario.workload, horizon):
+        if specs is None:
+            specs = build_requests(self.scenario.workload, horizon)
+        for spec in specs:
             req = SimRequest(spec)
             self.requests[req.id] = req
             self._push(spec.arrival_time, EV_ARRIVAL, req.id)

@@ -50,7 +50,8 @@ class HsModelCfg(C.Structure):
 class HsRtCfg(C.Structure):
     _fields_ = [("max_rows", C.c_int), ("max_slots", C.c_int), ("kv_pages", C.c_int),
                 ("max_pages_per_req", C.c_int), ("max_pos", C.c_int), ("max_chunks", C.c_int),
-                ("cpu_threads", C.c_int), ("host_kv_bytes", C.c_int64), ("device", C.c_int)]
+                ("cpu_threads", C.c_int), ("host_kv_bytes", C.c_int64), ("device", C.c_int),
+                ("cpu_list", _IP), ("n_cpu_list", C.c_int)]
 
 
 class HsIterDesc(C.Structure):
@@ -127,6 +128,7 @@ class RuntimeConfig:
     cpu_threads: int = 8
     host_kv_bytes: int = 1 << 30
     device: int = 0
+    cpu_list: tuple = ()  # the replica's CPU-attention cores (replicas.core_set)
 
 
 class HsContext:
@@ -156,8 +158,10 @@ class HsContext:
         self.rt = rt
         mc = HsModelCfg(model.d_model, model.n_layers, model.n_q, model.n_kv, model.head_dim,
                         model.ffn, model.vocab, model.rope_theta, model.norm_eps)
+        cpus = np.asarray(rt.cpu_list or [], np.int32)
         rc = HsRtCfg(rt.max_rows, rt.max_slots, rt.kv_pages, rt.max_pages_per_req, rt.max_pos,
-                     rt.max_chunks, rt.cpu_threads, rt.host_kv_bytes, rt.device)
+                     rt.max_chunks, rt.cpu_threads, rt.host_kv_bytes, rt.device,
+                     cpus.ctypes.data_as(_IP) if len(cpus) else None, len(cpus))
         h = C.c_void_p()
         _lib.check(lib.hs_create(C.byref(mc), C.byref(rc), C.byref(h)), "hs_create")
         self.h = h
