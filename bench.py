@@ -444,7 +444,7 @@ def run_ours(args) -> None:
          m["tpot_attainment"] * m["ls_gaps"]],
         [device_s, wall_s, m["tpot_p99_ms"] or 0.0], dist)
     device_max, wall_max = float(mx[0]), float(mx[1])
-    attain = tot[4] / tot[3] if tot[3] else 1.0
+    attain = float(tot[4] / tot[3]) if tot[3] else 1.0
     if rank != 0:
         return
     pk = peaks()
@@ -490,7 +490,7 @@ def run_ours(args) -> None:
                    "l2": "working set (16 GB weights/iteration) > 126 MB L2"},
         "ls_tpot_attainment": attain, "ls_tpot_p99_ms": float(mx[2]),
         "ls_tokens": int(tot[1]), "be_tokens": int(tot[0]), "ls_gaps": int(tot[3]),
-        "slo_met": attain >= 0.99,
+        "slo_met": bool(attain >= 0.99),
         "merges": n_merges, "avg_batch_tokens": avg_rows,
         "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters
                                               if i.get("device_ms")) if iters else None,

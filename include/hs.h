@@ -283,6 +283,10 @@ int hs_profile_read(hs_ctx* ctx, double* stats /* [4][4] */, int reset);
 int hs_probe_dense(hs_ctx* ctx, int n, int reps, float* us);
 /* one layer-0 GEMM (which: 0 qkv, 1 o, 2 gate-up, 3 down), plain partial
  * planes (fused = 0) or with its fused stream-K epilogue (fused = 1) */
+/* dense part of `layers` consecutive layers as hs_layer issues it; mode =
+   op bitmask (0 QKV GEMM, 1 RoPE/KV/ship, 2 O GEMM, 3 add-norm, 4 gate-up
+   GEMM, 5 SiLU, 6 down GEMM, 7 add-norm); *us = median per-layer us */
+int hs_probe_dense_mode(hs_ctx* ctx, int n, int mode, int layers, int reps, float* us);
 int hs_probe_gemm(hs_ctx* ctx, int which, int n, int fused, int reps, float* us);
 int hs_probe_decode(hs_ctx* ctx, int g, int ctx_len, int reps, float* us);
 int hs_probe_prefill(hs_ctx* ctx, int q, int done, int reps, float* us);

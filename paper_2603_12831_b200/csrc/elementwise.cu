@@ -19,36 +19,92 @@ namespace hs {
 
 constexpr int kMaxSplits = 16;
 
-// Sum of `splits` fp32 split-K planes at p (plane stride in floats): all
-// loads are issued before the first add so the latency is paid once.
+// Sum of `splits` fp32 split-K planes at p (plane stride in floats), plane 0
+// first (a fixed order: results are bit-reproducible).  Runtime loop issuing
+// four planes' loads at a time: few registers, so the glue kernels keep full
+// occupancy and enough bytes in flight to stream HBM.
+__device__ __forceinline__ void add4(float4& a, const float4& v) {
+  a.x += v.x;
+  a.y += v.y;
+  a.z += v.z;
+  a.w += v.w;
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+
 __device__ __forceinline__ float4 sum_planes4(const float* __restrict__ p, size_t plane,
                                               int splits) {
-  float4 v[kMaxSplits];
-#pragma unroll
-  for (int k = 0; k < kMaxSplits; ++k)
-    if (k < splits) v[k] = __ldg(reinterpret_cast<const float4*>(p + k * plane));
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  int k = 0;
+  for (; k + 4 <= splits; k += 4) {
+    const float4 v0 = ld4(p + k * plane), v1 = ld4(p + (k + 1) * plane),
+                 v2 = ld4(p + (k + 2) * plane), v3 = ld4(p + (k + 3) * plane);
+    add4(a, v0);
+    add4(a, v1);
+    add4(a, v2);
+    add4(a, v3);
+  }
+  for (; k < splits; ++k) add4(a, ld4(p + k * plane));
+  return a;
+}
+
+// two streams at once (gate and up of SwiGLU): twice the loads in flight
+__device__ __forceinline__ void sum_planes4x2(const float* __restrict__ p,
+                                              const float* __restrict__ q, size_t plane,
+                                              int splits, float4& a, float4& b) {
+  a = make_float4(0.f, 0.f, 0.f, 0.f);
+  b = a;
+  int k = 0;
+  for (; k + 2 <= splits; k += 2) {
+    const float4 p0 = ld4(p + k * plane), p1 = ld4(p + (k + 1) * plane);
+    const float4 q0 = ld4(q + k * plane), q1 = ld4(q + (k + 1) * plane);
+    add4(a, p0);
+    add4(a, p1);
+    add4(b, q0);
+    add4(b, q1);
+  }
+  if (k < splits) {
+    add4(a, ld4(p + k * plane));
+    add4(b, ld4(q + k * plane));
+  }
+}
+
+__device__ __forceinline__ float2 sum_planes2(const float* __restrict__ p, size_t plane,
+                                              int splits) {
+  float2 a = make_float2(0.f, 0.f);
+  int k = 0;
+  for (; k + 4 <= splits; k += 4) {
+    float2 v[4];
 #pragma unroll
-  for (int k = 0; k < kMaxSplits; ++k)
-    if (k < splits) {
-      a.x += v[k].x;
-      a.y += v[k].y;
-      a.z += v[k].z;
-      a.w += v[k].w;
+    for (int j = 0; j < 4; ++j) v[j] = __ldg(reinterpret_cast<const float2*>(p + (k + j) * plane));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a.x += v[j].x;
+      a.y += v[j].y;
     }
+  }
+  for (; k < splits; ++k) {
+    const float2 v = __ldg(reinterpret_cast<const float2*>(p + k * plane));
+    a.x += v.x;
+    a.y += v.y;
+  }
   return a;
 }
 
 __device__ __forceinline__ float sum_planes1(const float* __restrict__ p, size_t plane,
                                              int splits) {
-  float v[kMaxSplits];
-#pragma unroll
-  for (int k = 0; k < kMaxSplits; ++k)
-    if (k < splits) v[k] = __ldg(p + k * plane);
   float a = 0.f;
+  int k = 0;
+  for (; k + 4 <= splits; k += 4) {
+    float v[4];
 #pragma unroll
-  for (int k = 0; k < kMaxSplits; ++k)
-    if (k < splits) a += v[k];
+    for (int j = 0; j < 4; ++j) v[j] = __ldg(p + (k + j) * plane);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a += v[j];
+  }
+  for (; k < splits; ++k) a += __ldg(p + k * plane);
   return a;
 }
 
@@ -166,10 +222,84 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
   }
 }
 
+// Many rows: one 256-thread CTA per row holding the row in registers (up to
+// kRowVec float4 per thread, d <= 8192), no cluster barriers.
+constexpr int kRowVec = 8;
+
+__global__ void __launch_bounds__(256)
+    residual_add_norm_rows_kernel(const float* __restrict__ part, int splits, int rows, int d,
+                                  float* __restrict__ h, const float* __restrict__ w, float eps,
+                                  bf16* __restrict__ out, int ld_out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  float* x = h + static_cast<size_t>(r) * d;
+  const size_t plane = static_cast<size_t>(rows) * d;
+  const float* pp = part + static_cast<size_t>(r) * d;
+  // planes outer, the row's vectors inner: kRowVec loads in flight per plane
+  float4 v[kRowVec];
+#pragma unroll
+  for (int k = 0; k < kRowVec; ++k) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < splits; ++s) {
+    const float* ps = pp + s * plane;
+    float4 t[kRowVec];
+#pragma unroll
+    for (int k = 0; k < kRowVec; ++k) {
+      const int i = (threadIdx.x + k * 256) * 4;
+      if (i < d) t[k] = ld4(ps + i);
+    }
+#pragma unroll
+    for (int k = 0; k < kRowVec; ++k) {
+      const int i = (threadIdx.x + k * 256) * 4;
+      if (i < d) add4(v[k], t[k]);
+    }
+  }
+  // h += sum of the planes (the same association as the cluster form)
+#pragma unroll
+  for (int k = 0; k < kRowVec; ++k) {
+    const int i = (threadIdx.x + k * 256) * 4;
+    if (i < d) {
+      float4 hv = *reinterpret_cast<const float4*>(x + i);
+      add4(hv, v[k]);
+      v[k] = hv;
+    }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kRowVec; ++k) {
+    const int i = (threadIdx.x + k * 256) * 4;
+    if (i < d) {
+      if (splits > 0) *reinterpret_cast<float4*>(x + i) = v[k];
+      ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+    }
+  }
+  if (!out) return;
+  const float inv = rsqrtf(block_sum(ss, red) / d + eps);
+  bf16* o = out + static_cast<size_t>(r) * ld_out;
+#pragma unroll
+  for (int k = 0; k < kRowVec; ++k) {
+    const int i = (threadIdx.x + k * 256) * 4;
+    if (i < d) {
+      const float4 g = *reinterpret_cast<const float4*>(w + i);
+      uint2 pk;
+      pk.x = pack_bf16x2(v[k].x * inv * g.x, v[k].y * inv * g.y);
+      pk.y = pack_bf16x2(v[k].z * inv * g.z, v[k].w * inv * g.w);
+      *reinterpret_cast<uint2*>(o + i) = pk;
+    }
+  }
+}
+
+// below this many rows the 8-CTA cluster form spreads a row over more SMs
+constexpr int kClusterRowsMax = 4;
+
 int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
                       float eps, bf16* out, int ld_out, cudaStream_t st) {
   if (rows <= 0) return HS_OK;
   if (d % (4 * kNormCluster) || splits > kMaxSplits) return HS_E_CONFIG;
+  if (rows > kClusterRowsMax && d <= 4 * 256 * kRowVec)
+    return launch_pdl(residual_add_norm_rows_kernel, dim3(rows), dim3(256), 0, st, part, splits,
+                      rows, d, h, w, eps, out, ld_out);
   dim3 grid(kNormCluster, rows);
   return launch_pdl(residual_add_norm_kernel, dim3(grid), dim3(256), 0, st, part, splits, rows, d, h, w, eps, out, ld_out);
 }
@@ -183,27 +313,29 @@ int residual_add_norm(const float* part, int splits, int rows, int d, float* h, 
 //           Piggybacking, reference engine.py:982-989 _chain_qkv)
 //   mode 2: q -> qbuf row, k/v -> ship slot (GPU attention of a row whose KV
 //           lives on the host is not used; reserved)
-// grid (rows, n_q + 2 n_kv): one block per (row, head), hd/2 threads; q and k
+// grid (feature blocks, rows), 256 threads; each thread owns two rotation
+// pairs (j, j+1) of one head: one float4 (permuted layout, pairs adjacent) or
+// two float2 loads per split plane, bf16x2 stores of both halves.  q and k
 // heads are rotated, v heads copied.
-__global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int splits, int rows,
-                                        int n_q, int n_kv, int hd,
-                                        const float* __restrict__ rope_cos,
-                                        const float* __restrict__ rope_sin,
-                                        const int* __restrict__ row_pos,
-                                        const int* __restrict__ row_slot,
-                                        const int* __restrict__ row_mode, int n_batch,
-                                        const int* __restrict__ carry_pos,
-                                        const int* __restrict__ carry_slot,
-                                        bf16* __restrict__ qbuf,
-                                        int q_row_stride, bf16* __restrict__ kv_pool, KvGeom geom,
-                                        int layer, const int* __restrict__ page_table,
-                                        int pt_stride, bf16* __restrict__ ship, int ship_stride,
-                                        int permuted) {
+__global__ void __launch_bounds__(256)
+    qkv_rope_scatter_kernel(const float* __restrict__ part, int splits, int rows, int n_q,
+                            int n_kv, int hd, const float* __restrict__ rope_cos,
+                            const float* __restrict__ rope_sin, const int* __restrict__ row_pos,
+                            const int* __restrict__ row_slot, const int* __restrict__ row_mode,
+                            int n_batch, const int* __restrict__ carry_pos,
+                            const int* __restrict__ carry_slot, bf16* __restrict__ qbuf,
+                            int q_row_stride, bf16* __restrict__ kv_pool, KvGeom geom, int layer,
+                            const int* __restrict__ page_table, int pt_stride,
+                            bf16* __restrict__ ship, int ship_stride, int permuted) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
-  const int r = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
-  const int half = hd / 2;
-  const int n_tot = (n_q + 2 * n_kv) * hd;
+  const int r = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int quarter = hd / 4, half = hd / 2;
+  const int heads = n_q + 2 * n_kv;
+  if (t >= heads * quarter) return;
+  const int head = t / quarter, j = 2 * (t % quarter);
+  const int n_tot = heads * hd;
   const size_t plane = static_cast<size_t>(rows) * n_tot;
   const int base = head * hd;
   const float* src = part + static_cast<size_t>(r) * n_tot + base;
@@ -214,20 +346,23 @@ __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int spli
   const int pos = batch ? row_pos[r] : carry_pos[r - n_batch];
   const int slot = batch ? row_slot[r] : carry_slot[r - n_batch];
   const int mode = batch ? (row_mode ? row_mode[r] : 0) : 1;
-  // permuted weights (fused-epilogue layout): feature i of the head sits in
-  // row 2i, feature i + hd/2 in row 2i+1
-  const int i1 = permuted ? 2 * i : i, i2 = permuted ? 2 * i + 1 : i + half;
-  const float x1 = sum_planes1(src + i1, plane, splits);
-  const float x2 = sum_planes1(src + i2, plane, splits);
-  bf16 y1, y2;
-  if (head < n_q + n_kv) {  // rotate q and k heads
-    const float c = rope_cos[static_cast<size_t>(pos) * half + i];
-    const float s = rope_sin[static_cast<size_t>(pos) * half + i];
-    y1 = __float2bfloat16(x1 * c - x2 * s);
-    y2 = __float2bfloat16(x2 * c + x1 * s);
+  float a1, a2, b1, b2;  // (x1, x2) of pairs j and j+1
+  if (permuted) {  // feature i of the head in row 2i, feature i + hd/2 in row 2i+1
+    const float4 v = sum_planes4(src + 2 * j, plane, splits);
+    a1 = v.x, a2 = v.y, b1 = v.z, b2 = v.w;
   } else {
-    y1 = __float2bfloat16(x1);
-    y2 = __float2bfloat16(x2);
+    const float2 lo = sum_planes2(src + j, plane, splits);
+    const float2 hi = sum_planes2(src + half + j, plane, splits);
+    a1 = lo.x, b1 = lo.y, a2 = hi.x, b2 = hi.y;
+  }
+  float y1a = a1, y2a = a2, y1b = b1, y2b = b2;
+  if (head < n_q + n_kv) {  // rotate q and k heads
+    const float2 c = *reinterpret_cast<const float2*>(rope_cos + static_cast<size_t>(pos) * half + j);
+    const float2 s = *reinterpret_cast<const float2*>(rope_sin + static_cast<size_t>(pos) * half + j);
+    y1a = a1 * c.x - a2 * s.x;
+    y2a = a2 * c.x + a1 * s.x;
+    y1b = b1 * c.y - b2 * s.y;
+    y2b = b2 * c.y + b1 * s.y;
   }
   bf16* dst;
   if (mode == 1) {
@@ -240,8 +375,8 @@ __global__ void qkv_rope_scatter_kernel(const float* __restrict__ part, int spli
     const int phys = page_table[static_cast<size_t>(slot) * pt_stride + pos / kPageTokens];
     dst = kv_pool + (kv_row(geom, layer, phys, kv, kh) + pos % kPageTokens) * hd;
   }
-  dst[i] = y1;
-  dst[i + half] = y2;
+  *reinterpret_cast<uint32_t*>(dst + j) = pack_bf16x2(y1a, y1b);
+  *reinterpret_cast<uint32_t*>(dst + half + j) = pack_bf16x2(y2a, y2b);
 }
 
 int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv, int head_dim,
@@ -251,39 +386,45 @@ int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv,
                      const KvGeom& g, int layer, const int* page_table, int pt_stride, bf16* ship,
                      int ship_stride, cudaStream_t st, int permuted) {
   if (rows <= 0) return HS_OK;
-  if (splits > kMaxSplits) return HS_E_CONFIG;
-  dim3 grid(rows, n_q + 2 * n_kv);
-  return launch_pdl(qkv_rope_scatter_kernel, dim3(grid), dim3(head_dim / 2), 0, st, part, splits, rows, n_q, n_kv, head_dim, rope_cos, rope_sin, row_pos, row_slot, row_mode,
+  if (splits > kMaxSplits || head_dim % 8 || q_row_stride % 2 || ship_stride % 2)
+    return HS_E_CONFIG;
+  const int threads = (n_q + 2 * n_kv) * head_dim / 4;
+  dim3 grid((threads + 255) / 256, rows);
+  return launch_pdl(qkv_rope_scatter_kernel, grid, dim3(256), 0, st, part, splits, rows, n_q, n_kv, head_dim, rope_cos, rope_sin, row_pos, row_slot, row_mode,
       n_batch, carry_pos, carry_slot, qbuf, q_row_stride, kv_pool, g, layer, page_table, pt_stride, ship, ship_stride, permuted);
 }
 
 // ---------------------------------------------------------------- SwiGLU
-__global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int rows, int ffn,
-                                bf16* __restrict__ act, int ld_act, int permuted) {
+// grid (feature blocks, rows); each thread 4 consecutive features: float4
+// loads of gate and up from every split plane, one 8-byte bf16 store.
+__global__ void __launch_bounds__(256)
+    silu_mul_kernel(const float* __restrict__ part, int splits, int rows, int ffn,
+                    bf16* __restrict__ act, int ld_act, int permuted) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
+  const int r = blockIdx.y;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= ffn) return;
   const size_t plane = static_cast<size_t>(rows) * 2 * ffn;
-  const size_t total = static_cast<size_t>(rows) * ffn;
-  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t r = idx / ffn, i = idx % ffn;
-    const float* src = part + r * 2 * ffn;
-    // permuted: 32-row groups [16 gate | 16 up] of the same features
-    const size_t gi = permuted ? 32 * (i / 16) + i % 16 : i;
-    const size_t ui = permuted ? gi + 16 : ffn + i;
-    const float gt = sum_planes1(src + gi, plane, splits);
-    const float up = sum_planes1(src + ui, plane, splits);
-    const float s = gt / (1.f + __expf(-gt));
-    act[r * ld_act + i] = __float2bfloat16(s * up);
-  }
+  const float* src = part + static_cast<size_t>(r) * 2 * ffn;
+  // permuted: 32-row groups [16 gate | 16 up] of the same features
+  const int gi = permuted ? 32 * (i >> 4) + (i & 15) : i;
+  const int ui = permuted ? gi + 16 : ffn + i;
+  float4 g, u;
+  sum_planes4x2(src + gi, src + ui, plane, splits, g, u);
+  auto f = [](float gt, float up) { return gt / (1.f + __expf(-gt)) * up; };
+  uint2 pk;
+  pk.x = pack_bf16x2(f(g.x, u.x), f(g.y, u.y));
+  pk.y = pack_bf16x2(f(g.z, u.z), f(g.w, u.w));
+  *reinterpret_cast<uint2*>(act + static_cast<size_t>(r) * ld_act + i) = pk;
 }
 
 int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld_act,
              cudaStream_t st, int permuted) {
-  const size_t total = static_cast<size_t>(rows) * ffn;
-  if (!total) return HS_OK;
-  const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, size_t(148 * 16)));
-  return launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, st, part, splits, rows, ffn, act, ld_act, permuted);
+  if (rows <= 0 || ffn <= 0) return HS_OK;
+  if (ffn % 16 || ld_act % 4 || splits > kMaxSplits) return HS_E_CONFIG;
+  dim3 grid((ffn / 4 + 255) / 256, rows);
+  return launch_pdl(silu_mul_kernel, grid, dim3(256), 0, st, part, splits, rows, ffn, act, ld_act, permuted);
 }
 
 // ---------------------------------------------------------------- greedy argmax

@@ -1262,6 +1262,54 @@ int hs_probe_dense(hs_ctx* c, int n, int reps, float* us) {
   }, us);
 }
 
+// The dense part of `layers` consecutive layers exactly as hs_layer issues it
+// on the unfused path (QKV GEMM + RoPE/KV/ship, O GEMM + residual-add-norm,
+// gate-up GEMM + SiLU, down GEMM + residual-add-norm), back to back with no
+// events in between.  `mode` selects the ops (bit list below); the per-layer
+// time of each subset shows how much of the layer is launch/ramp overhead
+// rather than streaming.
+int hs_probe_dense_mode(hs_ctx* c, int n, int mode, int layers, int reps, float* us) {
+  const ModelCfg& m = c->m;
+  if (n < 1 || n > c->r.max_rows) return set_error(HS_E_CONFIG, "probe rows out of range");
+  if (layers < 1 || layers > m.layers) return set_error(HS_E_CONFIG, "probe layers out of range");
+  const int d_ = m.d, nqh = m.n_q * m.hd;
+  // op bits: 0 QKV GEMM, 1 RoPE/KV/ship, 2 O GEMM, 3 residual-add-norm,
+  // 4 gate-up GEMM, 5 SiLU, 6 down GEMM, 7 residual-add-norm
+  auto on = [mode](int b) { return (mode >> b) & 1; };
+  // every row a carry row of slot 0 at position 0 (page-table row 0 valid)
+  RC(probe_pages(c, 1, 64));
+  CK(cudaMemset(c->dm_layer, 0, 2 * static_cast<size_t>(n) * sizeof(int)));
+  const int* cslot = c->dm_layer;
+  const int* cpos = c->dm_layer + n;
+  auto planes = [&](int n_out, int k) {
+    return std::max(1, gemm_pick_splits(n_out, k, n, gemm_pick_bn(n), 16));
+  };
+  const int s_qkv = planes(m.qkv_n(), d_), s_o = planes(d_, nqh), s_gu = planes(2 * m.ffn, d_),
+            s_dn = planes(d_, m.ffn);
+  int err = time_reps(c, reps, [&]() -> int {
+    int s;
+    for (int l = 0; l < layers; ++l) {
+      if (on(0)) RC(gemm(c, c->m_qkv[l], c->xn, n, m.qkv_n(), d_, &s));
+      if (on(1))
+        RC(qkv_rope_scatter(c->part, s_qkv, n, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
+                            nullptr, nullptr, nullptr, 0, cpos, cslot, c->qbuf, nqh, c->kv_pool,
+                            c->geom, l, c->page_table, c->r.max_pages_per_req, c->ship_d,
+                            m.qkv_n(), c->st, 1));
+      if (on(2)) RC(gemm(c, c->m_o[l], c->attn, n, d_, nqh, &s));
+      if (on(3))
+        RC(residual_add_norm(c->part, s_o, n, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, c->st));
+      if (on(4)) RC(gemm(c, c->m_gu[l], c->xn2, n, 2 * m.ffn, d_, &s));
+      if (on(5)) RC(silu_mul(c->part, s_gu, n, m.ffn, c->act.p, m.ffn, c->st, 1));
+      if (on(6)) RC(gemm(c, c->m_down[l], c->act, n, d_, m.ffn, &s));
+      if (on(7))
+        RC(residual_add_norm(c->part, s_dn, n, d_, c->h, c->n_in[l], m.eps, c->xn.p, d_, c->st));
+    }
+    return HS_OK;
+  }, us);
+  *us /= layers;
+  return err;
+}
+
 // one GEMM of layer 0: which 0=qkv 1=o 2=gate_up 3=down; fused 0=planes 1=fused epilogue
 int hs_probe_gemm(hs_ctx* c, int which, int n, int fused, int reps, float* us) {
   const ModelCfg& m = c->m;
@@ -1297,12 +1345,14 @@ int hs_probe_decode(hs_ctx* c, int g, int ctx_len, int reps, float* us) {
   if (g < 1 || g > c->r.max_rows) return set_error(HS_E_CONFIG, "probe rows out of range");
   RC(probe_pages(c, g, ctx_len));
   const int per = (ctx_len + kPageTokens - 1) / kPageTokens;
-  const int chunk = std::max(1, std::min(64, (g * per * m.n_kv + 295) / 296));
+  // the runtime's chunking (runtime.decode_chunks): smallest chunk keeping
+  // one wave of 296 CTAs, rows split into near-equal chunks
+  int chunk = std::max(1, std::min(64, (g * per * m.n_kv + 295) / 296));
+  while (chunk < 64 && m.n_kv * g * ((per + chunk - 1) / chunk) > 296) ++chunk;
+  const int k = std::max(1, (per + chunk - 1) / chunk);
   std::vector<int> ch, beg{0};
   for (int r = 0; r < g; ++r) {
-    for (int p0 = 0; p0 < per; p0 += chunk) {
-      ch.insert(ch.end(), {r, r, p0, std::min(per, p0 + chunk), ctx_len});
-    }
+    for (int i = 0; i < k; ++i) ch.insert(ch.end(), {r, r, i * per / k, (i + 1) * per / k, ctx_len});
     beg.push_back(static_cast<int>(ch.size() / 5));
   }
   if (static_cast<int>(ch.size() / 5) > c->r.max_chunks)

@@ -328,15 +328,21 @@ def prompt_tokens(req_id: str, length: int, vocab: int, seed: int = 0) -> np.nda
 
 
 def decode_chunks(ctxs: list[int], n_kv: int, target_ctas: int = 296, max_pages: int = 64):
-    """Split-K work list: each decode row's KV pages cut into chunks so that
-    chunks x KV heads ~ 2 CTAs per SM (148 SMs)."""
+    """Split-K work list for decode attention (K1): each decode row's KV
+    pages are cut into near-equal chunks, the chunk size being the smallest
+    that keeps chunks x KV heads within one wave of `target_ctas` (2 CTAs
+    per SM x 148 SMs), so the launch has no tail wave of short chunks.
+    Rows longer than `max_pages` pages always split (bounded merge fan-in)."""
     pages = [(c + PAGE - 1) // PAGE for c in ctxs]
     total = sum(pages)
     per = max(1, min(max_pages, -(-total * n_kv // target_ctas))) if total else 1
+    while per < max_pages and n_kv * sum(-(-n // per) for n in pages) > target_ctas:
+        per += 1
     chunks, begin = [], [0]
     for r, (c, n) in enumerate(zip(ctxs, pages)):
-        for p0 in range(0, n, per):
-            chunks.append((r, -1, p0, min(n, p0 + per), c))
+        k = max(1, -(-n // per))
+        for i in range(k):
+            chunks.append((r, -1, i * n // k, (i + 1) * n // k, c))
         begin.append(len(chunks))
     return chunks, begin
 

@@ -332,3 +332,40 @@ def test_decode_attention_fused_combine(cuda, n_q, n_kv, hd, chunk_pages):
             ref, _ = O.decode_attention(q[r], k, v, n_kv)
             assert _rel(got[r], ref) < 1.5e-2, (r, c)
     assert int(cnt.abs().sum().item()) == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,d,splits", [(33, 4096, 3), (300, 256, 1), (64, 5120, 16),
+                                           (8, 4096, 0)])
+def test_residual_add_norm_row_and_cluster_forms(cuda, rows, d, splits):
+    """Both launch forms of K4 (8-CTA cluster per row for <= 32 rows, one CTA
+    per row above) against the fp64 oracle."""
+    import torch
+    from paper_2603_12831_b200 import _lib
+
+    rng = np.random.default_rng(rows + d)
+    h0 = rng.standard_normal((rows, d)).astype(np.float32)
+    w = (1.0 + 0.1 * rng.standard_normal(d)).astype(np.float32)
+    part = rng.standard_normal((max(splits, 1), rows, d)).astype(np.float32)
+    h = _t(h0, cuda)
+    out = torch.zeros(rows, d, dtype=torch.bfloat16, device=cuda)
+    _lib.call("hs_op_residual_add_norm", _p(_t(part, cuda)), splits, rows, d, _p(h),
+              _p(_t(w, cuda)), C.c_float(1e-5), _p(out), d, None)
+    torch.cuda.synchronize()
+    h2 = h0 + (part.sum(0) if splits else 0.0)
+    assert np.allclose(h.cpu().numpy().reshape(rows, d), h2, atol=1e-4)
+    assert _rel(out.float().cpu().numpy(), O.rmsnorm(h2, w, 1e-5)) < 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,ffn,splits", [(1, 14336, 7), (129, 768, 2), (40, 13824, 16)])
+def test_silu_mul_shapes(cuda, rows, ffn, splits):
+    import torch
+    from paper_2603_12831_b200 import _lib
+
+    rng = np.random.default_rng(rows + ffn)
+    gu = rng.standard_normal((splits, rows, 2 * ffn)).astype(np.float32)
+    act = torch.zeros(rows, ffn, dtype=torch.bfloat16, device=cuda)
+    _lib.call("hs_op_silu_mul", _p(_t(gu, cuda)), splits, rows, ffn, _p(act), ffn, None)
+    torch.cuda.synchronize()
+    assert _rel(act.float().cpu().numpy(), O.silu_mul(gu.sum(0), ffn)) < 1e-2
