@@ -41,8 +41,6 @@ __global__ void __launch_bounds__(kDecThreads, 2)
                        float* __restrict__ lse_part, float scale_log2,
                        const int* __restrict__ row_chunk_begin, int* __restrict__ counters,
                        bf16* __restrict__ out, int out_row_stride) {
-  pdl_wait();  // dependent data of the previous kernel is visible
-  pdl_trigger();
   constexpr int kBoxBytes = kPageTokens * 128;
   constexpr int kHalf = (HD / 64) * kBoxBytes;  // K (or V) of one page
   constexpr int kStageBytes = 2 * kHalf;
@@ -83,9 +81,18 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       tma_load_2d(dst + kHalf + b * kBoxBytes, &kv_map, &full[s], b * 64, rv);
     }
   };
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < min(kDecStages, npages); ++i) issue(i);
-  }
+  // Before the previous kernel's results are visible (PDL): only pages that
+  // cannot hold this layer's new token (position ctx-1, written by the QKV
+  // epilogue just before) are safe to stream; the chunk list and the page
+  // table were uploaded ahead of the iteration.
+  const int safe = max(0, min(npages, (ch.ctx - 1) / kPageTokens - ch.page_begin));
+  const int first = min(kDecStages, npages);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < min(first, safe); ++i) issue(i);
+  pdl_wait();  // q and the new token's K/V are visible from here on
+  pdl_trigger();
+  if (threadIdx.x == 0)
+    for (int i = min(first, safe); i < first; ++i) issue(i);
 
   // Q fragments (A operand, rows = query heads of this GQA group)
   uint32_t qa[KS][4];
@@ -214,14 +221,16 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   }
   const float Mu0 = M0 == -CUDART_INF_F ? 0.f : M0, Mu1 = M1 == -CUDART_INF_F ? 0.f : M1;
   const float f0 = exp2f(m0 - Mu0), f1 = exp2f(m1 - Mu1);
-  float* so = reinterpret_cast<float*>(smem);  // [4 warps][16 rows][HD]
+  // [4 warps][16 rows][HD + 8]: the pad spreads the 8 row groups of a warp
+  // over different banks
+  constexpr int SO = HD + 8;
+  float* so = reinterpret_cast<float*>(smem);
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int d = nt * 8 + tig * 2;
-    so[(warp * 16 + g) * HD + d] = o[nt][0] * f0;
-    so[(warp * 16 + g) * HD + d + 1] = o[nt][1] * f0;
-    so[(warp * 16 + g + 8) * HD + d] = o[nt][2] * f1;
-    so[(warp * 16 + g + 8) * HD + d + 1] = o[nt][3] * f1;
+    *reinterpret_cast<float2*>(&so[(warp * 16 + g) * SO + d]) = make_float2(o[nt][0] * f0, o[nt][1] * f0);
+    *reinterpret_cast<float2*>(&so[(warp * 16 + g + 8) * SO + d]) =
+        make_float2(o[nt][2] * f1, o[nt][3] * f1);
   }
   __syncthreads();
   const int base = (blockIdx.x * geom.n_kv + kvh) * G;
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         L += sm_l[w][r] * exp2f(sm_m[w][r] - Mur);
-        acc += so[(w * 16 + r) * HD + d];
+        acc += so[(w * 16 + r) * SO + d];
       }
       out[static_cast<size_t>(ch.row) * out_row_stride + (kvh * G + r) * HD + d] =
           __float2bfloat16(L > 0.f ? acc / L : 0.f);
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       L += sm_l[w][r] * exp2f(sm_m[w][r] - Mur);
-      acc += so[(w * 16 + r) * HD + d];
+      acc += so[(w * 16 + r) * SO + d];
     }
     o_part[static_cast<size_t>(base + r) * HD + d] = L > 0.f ? acc / L : 0.f;
     if (d == 0)
@@ -273,21 +282,46 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // every chunk's LSE of this (row, KV head) into smem with independent
+  // loads, per-head weights, then the weighted sum with 4 loads in flight
+  float* s_w = reinterpret_cast<float*>(smem);  // [n_row_chunks][G]
+  float* s_inv = s_w + n_row_chunks * G;        // [G]
+  for (int i = threadIdx.x; i < n_row_chunks * G; i += kDecThreads) {
+    const int c = c_lo + i / G, r = i % G;
+    s_w[i] = __ldcg(&lse_part[(c * geom.n_kv + kvh) * G + r]);
+  }
+  __syncthreads();
+  if (threadIdx.x < G) {
+    const int r = threadIdx.x;
+    float mx = -CUDART_INF_F;
+    for (int c = 0; c < n_row_chunks; ++c) mx = fmaxf(mx, s_w[c * G + r]);
+    const float mu = mx == -CUDART_INF_F ? 0.f : mx;
+    float ws = 0.f;
+    for (int c = 0; c < n_row_chunks; ++c) {
+      const float w = __expf(s_w[c * G + r] - mu);
+      s_w[c * G + r] = w;
+      ws += w;
+    }
+    s_inv[r] = ws > 0.f ? 1.f / ws : 0.f;
+  }
+  __syncthreads();
   for (int idx = threadIdx.x; idx < G * HD; idx += kDecThreads) {
     const int r = idx / HD, d = idx % HD;
-    float mx = -CUDART_INF_F;
-    for (int c = c_lo; c < c_lo + n_row_chunks; ++c)
-      mx = fmaxf(mx, __ldcg(&lse_part[(c * geom.n_kv + kvh) * G + r]));
-    const float mu = mx == -CUDART_INF_F ? 0.f : mx;
-    float acc = 0.f, ws = 0.f;
-    for (int c = c_lo; c < c_lo + n_row_chunks; ++c) {
-      const int i2 = (c * geom.n_kv + kvh) * G + r;
-      const float w = __expf(__ldcg(&lse_part[i2]) - mu);
-      ws += w;
-      acc += w * __ldcg(&o_part[static_cast<size_t>(i2) * HD + d]);
+    const float* src = o_part + (static_cast<size_t>(c_lo * geom.n_kv + kvh) * G + r) * HD + d;
+    const size_t cstride = static_cast<size_t>(geom.n_kv) * G * HD;
+    float acc = 0.f;
+    int c = 0;
+    for (; c + 4 <= n_row_chunks; c += 4) {
+      const float v0 = __ldcg(src + c * cstride), v1 = __ldcg(src + (c + 1) * cstride),
+                  v2 = __ldcg(src + (c + 2) * cstride), v3 = __ldcg(src + (c + 3) * cstride);
+      acc += s_w[c * G + r] * v0;
+      acc += s_w[(c + 1) * G + r] * v1;
+      acc += s_w[(c + 2) * G + r] * v2;
+      acc += s_w[(c + 3) * G + r] * v3;
     }
+    for (; c < n_row_chunks; ++c) acc += s_w[c * G + r] * __ldcg(src + c * cstride);
     out[static_cast<size_t>(ch.row) * out_row_stride + (kvh * G + r) * HD + d] =
-        __float2bfloat16(ws > 0.f ? acc / ws : 0.f);
+        __float2bfloat16(acc * s_inv[r]);
   }
   if (threadIdx.x == 0) counters[ch.row * geom.n_kv + kvh] = 0;  // ready for the next launch
 }

@@ -18,6 +18,9 @@
 // projections ("QKV + proj + MLP", profiles.py:135).
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "hs_common.cuh"
 #include "hs_internal.h"
 
@@ -373,12 +376,23 @@ int make_map_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_
   return r == CUDA_SUCCESS ? HS_OK : HS_E_CUDA;
 }
 
+// HS_GEMM_MAX_BN (tuning knob, read once): cap on the token-tile width.
+static int max_bn() {
+  static const int cap = [] {
+    const char* e = getenv("HS_GEMM_MAX_BN");
+    const int v = e ? atoi(e) : 256;
+    return (v == 16 || v == 32 || v == 64 || v == 128) ? v : 256;
+  }();
+  return cap;
+}
+
 int gemm_pick_bn(int tokens) {
-  if (tokens <= 16) return 16;
-  if (tokens <= 32) return 32;
-  if (tokens <= 64) return 64;
-  if (tokens <= 128) return 128;
-  return 256;
+  int bn = 256;
+  if (tokens <= 16) bn = 16;
+  else if (tokens <= 32) bn = 32;
+  else if (tokens <= 64) bn = 64;
+  else if (tokens <= 128) bn = 128;
+  return std::min(bn, max_bn());
 }
 
 static StreamK plan_streamk(int n_out, int k, int tokens, int bn, int G) {
