@@ -392,6 +392,7 @@ def run_ours(args) -> None:
         dist.barrier()
     launches0 = step.ctx.lib.hs_launch_count()
     h2d0, d2h0 = step.h2d_bytes, step.d2h_bytes
+    cpu0, be_cpu0 = step.ctx.cpu_busy_seconds(), engine.counters["be_tokens_cpu"]
     # timed region: no per-kernel events (an event between two PDL launches
     # serialises them; measured +2.6 ms/step on llama3-8b)
     with ClockSampler(local) as clocks:
@@ -410,6 +411,8 @@ def run_ours(args) -> None:
     device_s = step.ctx.elapsed_ms(tm0, tm1) / 1e3
     launches = step.ctx.lib.hs_launch_count() - launches0
     h2d1, d2h1 = step.h2d_bytes, step.d2h_bytes
+    cpu_busy = step.ctx.cpu_busy_seconds() - cpu0
+    be_cpu = engine.counters["be_tokens_cpu"] - be_cpu0
     it1 = len(engine.iteration_log)
     # profiled window: the same workload continued for --profile-steps more
     # iterations with per-kernel-class CUDA events on the launch stream; the
@@ -492,6 +495,10 @@ def run_ours(args) -> None:
         "ls_tokens": int(tot[1]), "be_tokens": int(tot[0]), "ls_gaps": int(tot[3]),
         "slo_met": bool(attain >= 0.99),
         "merges": n_merges, "avg_batch_tokens": avg_rows,
+        "batch_tokens_p90": sorted(i["batch_tokens"] for i in iters)[int(0.9 * len(iters))]
+        if iters else 0,
+        "be_tokens_via_cpu_attention": be_cpu,
+        "cpu_pool_busy_frac": cpu_busy / max(wall_s * rt.cpu_threads, 1e-9),
         "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters
                                               if i.get("device_ms")) if iters else None,
         "device_breakdown_ms": {"window": f"{args.profile_steps} profiled steps after the timed "
