@@ -2,6 +2,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <ctime>
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
@@ -9,6 +11,17 @@
 namespace hs {
 thread_local char g_last_error[512] = {0};
 unsigned long long g_launches = 0;
+int g_hprof_on = [] {
+  const char* e = getenv("HS_HOST_PROF");
+  return e && e[0] == '1' ? 1 : 0;
+}();
+double g_hprof_ns[8] = {0};
+unsigned long long g_hprof_n[8] = {0};
+double hprof_now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec * 1e9 + ts.tv_nsec;
+}
 
 int set_error(int code, const char* fmt, ...) {
   va_list ap;

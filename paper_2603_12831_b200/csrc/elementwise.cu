@@ -137,10 +137,7 @@ int embed_gather(const int* tokens, int rows, const bf16* emb, int d, float* h, 
 }
 
 // ---------------------------------------------------------------- RMSNorm
-// (the residual_add_norm cluster kernel with no partials to add; defined below)
-int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
-                      float eps, bf16* out, int ld_out, cudaStream_t st);
-
+// (the residual_add_norm kernels with no partials to add; defined below)
 int rmsnorm_rows(const float* h, int rows, int d, const float* w, float eps, bf16* out, int ld_out,
                  cudaStream_t st) {
   return residual_add_norm(nullptr, 0, rows, d, const_cast<float*>(h), w, eps, out, ld_out, st);
@@ -175,7 +172,7 @@ constexpr int kNormCluster = 8;
 __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
     residual_add_norm_kernel(const float* __restrict__ part, int splits, int rows, int d,
                              float* __restrict__ h, const float* __restrict__ w, float eps,
-                             bf16* __restrict__ out, int ld_out) {
+                             bf16* __restrict__ out, int ld_out, RowIo io) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   __shared__ float red[32];
@@ -186,19 +183,23 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
   const int cols = d / kNormCluster;  // multiple of 4
   const int c0 = rank * cols;
   float* x = h + static_cast<size_t>(r) * d + c0;
+  const float* xin = io.row_src(h, r, d) + c0;
+  float* put = io.row_put(r, d);
+  const bool write = splits > 0 || xin != x;
   const size_t plane = static_cast<size_t>(rows) * d;
   const float* pp = part + static_cast<size_t>(r) * d + c0;
   float ss = 0.f;
   for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<float4*>(x + i);
+    float4 v = *reinterpret_cast<const float4*>(xin + i);
     if (splits > 0) {
       const float4 a = sum_planes4(pp + i, plane, splits);
       v.x += a.x;
       v.y += a.y;
       v.z += a.z;
       v.w += a.w;
-      *reinterpret_cast<float4*>(x + i) = v;
     }
+    if (write) *reinterpret_cast<float4*>(x + i) = v;
+    if (put) *reinterpret_cast<float4*>(put + c0 + i) = v;
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   if (!out) return;
@@ -229,12 +230,15 @@ constexpr int kRowVec = 8;
 __global__ void __launch_bounds__(256)
     residual_add_norm_rows_kernel(const float* __restrict__ part, int splits, int rows, int d,
                                   float* __restrict__ h, const float* __restrict__ w, float eps,
-                                  bf16* __restrict__ out, int ld_out) {
+                                  bf16* __restrict__ out, int ld_out, RowIo io) {
   pdl_wait();
   pdl_trigger();
   __shared__ float red[32];
   const int r = blockIdx.x;
   float* x = h + static_cast<size_t>(r) * d;
+  const float* xin = io.row_src(h, r, d);
+  float* put = io.row_put(r, d);
+  const bool write = splits > 0 || xin != x;
   const size_t plane = static_cast<size_t>(rows) * d;
   const float* pp = part + static_cast<size_t>(r) * d;
   // planes outer, the row's vectors inner: kRowVec loads in flight per plane
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(256)
   for (int k = 0; k < kRowVec; ++k) {
     const int i = (threadIdx.x + k * 256) * 4;
     if (i < d) {
-      float4 hv = *reinterpret_cast<const float4*>(x + i);
+      float4 hv = *reinterpret_cast<const float4*>(xin + i);
       add4(hv, v[k]);
       v[k] = hv;
     }
@@ -270,7 +274,8 @@ __global__ void __launch_bounds__(256)
   for (int k = 0; k < kRowVec; ++k) {
     const int i = (threadIdx.x + k * 256) * 4;
     if (i < d) {
-      if (splits > 0) *reinterpret_cast<float4*>(x + i) = v[k];
+      if (write) *reinterpret_cast<float4*>(x + i) = v[k];
+      if (put) *reinterpret_cast<float4*>(put + i) = v[k];
       ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
     }
   }
@@ -294,14 +299,15 @@ __global__ void __launch_bounds__(256)
 constexpr int kClusterRowsMax = 4;
 
 int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
-                      float eps, bf16* out, int ld_out, cudaStream_t st) {
+                      float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io) {
   if (rows <= 0) return HS_OK;
   if (d % (4 * kNormCluster) || splits > kMaxSplits) return HS_E_CONFIG;
   if (rows > kClusterRowsMax && d <= 4 * 256 * kRowVec)
     return launch_pdl(residual_add_norm_rows_kernel, dim3(rows), dim3(256), 0, st, part, splits,
-                      rows, d, h, w, eps, out, ld_out);
+                      rows, d, h, w, eps, out, ld_out, io);
   dim3 grid(kNormCluster, rows);
-  return launch_pdl(residual_add_norm_kernel, dim3(grid), dim3(256), 0, st, part, splits, rows, d, h, w, eps, out, ld_out);
+  return launch_pdl(residual_add_norm_kernel, dim3(grid), dim3(256), 0, st, part, splits, rows, d,
+                    h, w, eps, out, ld_out, io);
 }
 
 // ---------------------------------------------------------------- QKV epilogue
@@ -326,10 +332,18 @@ __global__ void __launch_bounds__(256)
                             const int* __restrict__ carry_slot, bf16* __restrict__ qbuf,
                             int q_row_stride, bf16* __restrict__ kv_pool, KvGeom geom, int layer,
                             const int* __restrict__ page_table, int pt_stride,
-                            bf16* __restrict__ ship, int ship_stride, int permuted) {
+                            bf16* __restrict__ ship, int ship_stride, int permuted, RowCopy rc) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const int r = blockIdx.y;
+  if (r >= rows) {  // merged rows: host attention result -> attention buffer
+    const int i = r - rows;
+    const uint4* src = reinterpret_cast<const uint4*>(rc.src + static_cast<size_t>(rc.idx[i]) * rc.src_stride);
+    uint4* dst = reinterpret_cast<uint4*>(rc.dst + static_cast<size_t>(i) * rc.dst_stride);
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < rc.width / 8; v += gridDim.x * blockDim.x)
+      dst[v] = src[v];
+    return;
+  }
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int quarter = hd / 4, half = hd / 2;
   const int heads = n_q + 2 * n_kv;
@@ -384,14 +398,17 @@ int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv,
                      const int* row_slot, const int* row_mode, int n_batch, const int* carry_pos,
                      const int* carry_slot, bf16* qbuf, int q_row_stride, bf16* kv_pool,
                      const KvGeom& g, int layer, const int* page_table, int pt_stride, bf16* ship,
-                     int ship_stride, cudaStream_t st, int permuted) {
-  if (rows <= 0) return HS_OK;
-  if (splits > kMaxSplits || head_dim % 8 || q_row_stride % 2 || ship_stride % 2)
+                     int ship_stride, cudaStream_t st, int permuted, const RowCopy& rc) {
+  if (rows + rc.n <= 0) return HS_OK;
+  if (splits > kMaxSplits || head_dim % 8 || q_row_stride % 2 || ship_stride % 2 ||
+      (rc.n && (rc.width % 8 || rc.src_stride % 8 || rc.dst_stride % 8)))
     return HS_E_CONFIG;
   const int threads = (n_q + 2 * n_kv) * head_dim / 4;
-  dim3 grid((threads + 255) / 256, rows);
-  return launch_pdl(qkv_rope_scatter_kernel, grid, dim3(256), 0, st, part, splits, rows, n_q, n_kv, head_dim, rope_cos, rope_sin, row_pos, row_slot, row_mode,
-      n_batch, carry_pos, carry_slot, qbuf, q_row_stride, kv_pool, g, layer, page_table, pt_stride, ship, ship_stride, permuted);
+  dim3 grid((threads + 255) / 256, rows + rc.n);
+  return launch_pdl(qkv_rope_scatter_kernel, grid, dim3(256), 0, st, part, splits, rows, n_q, n_kv,
+                    head_dim, rope_cos, rope_sin, row_pos, row_slot, row_mode, n_batch, carry_pos,
+                    carry_slot, qbuf, q_row_stride, kv_pool, g, layer, page_table, pt_stride, ship,
+                    ship_stride, permuted, rc);
 }
 
 // ---------------------------------------------------------------- SwiGLU
@@ -424,7 +441,8 @@ int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld
   if (rows <= 0 || ffn <= 0) return HS_OK;
   if (ffn % 16 || ld_act % 4 || splits > kMaxSplits) return HS_E_CONFIG;
   dim3 grid((ffn / 4 + 255) / 256, rows);
-  return launch_pdl(silu_mul_kernel, grid, dim3(256), 0, st, part, splits, rows, ffn, act, ld_act, permuted);
+  return launch_pdl(silu_mul_kernel, grid, dim3(256), 0, st, part, splits, rows, ffn, act, ld_act,
+                    permuted);
 }
 
 // ---------------------------------------------------------------- greedy argmax

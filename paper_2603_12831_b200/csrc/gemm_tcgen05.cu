@@ -41,29 +41,11 @@ struct GemmCfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-// Stream-K work split.  The GEMM is `tiles` output tiles (128 features x BN
-// tokens) of `kb` k-blocks each: U = tiles * kb units.  CTA c of G owns the
-// contiguous units [start(c), start(c+1)) — tile-aligned when there are at
-// least G tiles — so every CTA streams the same number of weight bytes in a
-// single wave.  A tile whose k-range spans several CTAs gets one fp32
-// partial plane per CTA (plane = c - first owner of the tile); the CTA that
-// finishes a tile zero-fills the tile's unused planes, so consumers always
-// sum exactly `planes` planes and the result is deterministic.
-struct StreamK {
-  int tiles, kb, G, aligned;
-  __host__ __device__ long long start(int c) const {
-    if (aligned) return (static_cast<long long>(c) * tiles / G) * kb;
-    return static_cast<long long>(c) * tiles * kb / G;
-  }
-  __host__ __device__ int owner(long long u) const {  // largest c with start(c) <= u
-    int lo = 0, hi = G - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (start(mid) <= u) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-  }
-};
+// Stream-K work split (StreamK, hs_internal.h).  A tile whose k-range spans
+// several CTAs gets one fp32 partial plane per CTA (plane = c - first owner
+// of the tile); the CTA that finishes a tile zero-fills the tile's unused
+// planes, so consumers always sum exactly `planes` planes and the result is
+// deterministic.
 
 // kBlocked: weights pre-tiled as [N/128][K/64][128][64] so every 16 KB TMA
 // box is one contiguous run of HBM (row-major weights make each box 128
@@ -417,7 +399,8 @@ static int streamk_planes(const StreamK& sk) {
 
 // CTAs of one wave (148 SMs x resident CTAs), capped by the work and by the
 // number of partial planes the caller can hold.
-static StreamK choose_streamk(int n_out, int k, int tokens, int bn, int max_planes, int* planes) {
+static StreamK choose_streamk_uncached(int n_out, int k, int tokens, int bn, int max_planes,
+                                      int* planes) {
   const int per_sm = bn <= 64 ? 2 : 1;
   const int tiles = (n_out / kTileM) * ((tokens + bn - 1) / bn);
   const int units = tiles * (k / kTileK);
@@ -433,6 +416,36 @@ static StreamK choose_streamk(int n_out, int k, int tokens, int bn, int max_plan
     }
     G = max(1, G * max_planes / (p + 1));
   }
+}
+
+// The schedule is a pure function of the shape; the step asks for the same
+// few shapes every layer, so plans are memoised (host issue cost: the plane
+// count walks every tile).  Per thread: each replica's engine thread issues.
+static StreamK choose_streamk(int n_out, int k, int tokens, int bn, int max_planes, int* planes) {
+  HProf hp(HP_PLAN);
+  struct Entry {
+    int n_out, k, tokens, bn, max_planes, planes;
+    StreamK sk;
+  };
+  constexpr int kWays = 256;
+  thread_local Entry cache[kWays];
+  thread_local bool init = false;
+  if (!init) {
+    for (auto& e : cache) e.n_out = -1;
+    init = true;
+  }
+  const unsigned h = (static_cast<unsigned>(n_out) * 2654435761u) ^ (static_cast<unsigned>(k) * 40503u) ^
+                     (static_cast<unsigned>(tokens) * 97u) ^ (static_cast<unsigned>(bn) << 7) ^
+                     (static_cast<unsigned>(max_planes) << 13);
+  Entry& e = cache[(h ^ (h >> 11)) % kWays];
+  if (e.n_out == n_out && e.k == k && e.tokens == tokens && e.bn == bn &&
+      e.max_planes == max_planes) {
+    *planes = e.planes;
+    return e.sk;
+  }
+  const StreamK sk = choose_streamk_uncached(n_out, k, tokens, bn, max_planes, planes);
+  e = Entry{n_out, k, tokens, bn, max_planes, *planes, sk};
+  return sk;
 }
 
 int gemm_pick_splits(int n_out, int k, int tokens, int bn, int max_splits) {
@@ -462,6 +475,7 @@ static int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, float* out, i
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  HProf hp(HP_LAUNCH);
   cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, kBlocked, Epi>, mw, mx, out, n_out, tokens,
                      sk, planes, ep);
   return launched();

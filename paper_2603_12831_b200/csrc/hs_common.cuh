@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "hs_internal.h"
+
 #ifndef __CUDA_ARCH__
 #define HS_HOST_ONLY 1
 #endif

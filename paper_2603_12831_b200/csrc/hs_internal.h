@@ -17,6 +17,24 @@ namespace hs {
 // every kernel launch site returns through launched(): counts the launch
 // (the bench's gpu_launches) and reports a launch error as HS_E_CUDA
 extern unsigned long long g_launches;
+// host-side issue profiler (HS_HOST_PROF=1): nanoseconds per section,
+// printed by hs_destroy
+extern int g_hprof_on;
+extern double g_hprof_ns[8];
+extern unsigned long long g_hprof_n[8];
+double hprof_now_ns();
+struct HProf {
+  int sec;
+  double t0;
+  explicit HProf(int s) : sec(s), t0(g_hprof_on ? hprof_now_ns() : 0.0) {}
+  ~HProf() {
+    if (g_hprof_on) {
+      g_hprof_ns[sec] += hprof_now_ns() - t0;
+      g_hprof_n[sec] += 1;
+    }
+  }
+};
+enum { HP_LAYER = 0, HP_PACK = 1, HP_PLAN = 2, HP_LAUNCH = 3, HP_BEGIN = 4, HP_END = 5 };
 inline int launched() {
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 4;
@@ -39,6 +57,7 @@ inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  HProf hp(HP_LAUNCH);
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
   return launched();
 }
@@ -50,6 +69,26 @@ struct KvGeom {
 __host__ __device__ inline int64_t kv_row(const KvGeom& g, int layer, int page, int kv, int head) {
   return ((((int64_t)layer * g.pages + page) * 2 + kv) * g.n_kv + head) * 64;
 }
+
+// ---- GEMM stream-K schedule (gemm_tcgen05.cu) ----
+// The GEMM is `tiles` output tiles (128 features x BN tokens) of `kb`
+// k-blocks each: U = tiles * kb units.  CTA c of G owns the contiguous units
+// [start(c), start(c+1)) -- tile-aligned when there are at least 4G tiles.
+struct StreamK {
+  int tiles, kb, G, aligned;
+  __host__ __device__ long long start(int c) const {
+    if (aligned) return (static_cast<long long>(c) * tiles / G) * kb;
+    return static_cast<long long>(c) * tiles * kb / G;
+  }
+  __host__ __device__ int owner(long long u) const {  // largest c with start(c) <= u
+    int lo = 0, hi = G - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (start(mid) <= u) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  }
+};
 
 // ---- GEMM fused epilogues (stream-K fixup, gemm_tcgen05.cu) ----
 enum { EPI_PLANES = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_QKV = 3 };
@@ -144,8 +183,39 @@ int embed_gather(const int* tokens, int rows, const bf16* emb, int d, float* h, 
 int rmsnorm_rows(const float* h, int rows, int d, const float* w, float eps, bf16* out, int ld_out,
                  cudaStream_t st);
 int splitk_reduce(const float* part, int splits, int rows, int n, float* out, cudaStream_t st);
+// Row indirections of the add-norm (the piggyback residual store,
+// engine.py:982-1004): rows >= src_from start from src[src_idx[r - src_from]]
+// instead of h[r] (residual get); rows >= put_from also store their new h
+// into put[put_idx[r - put_from]] (residual put).  Zero = plain rows.
+struct RowIo {
+  const float* src = nullptr;
+  const int* src_idx = nullptr;
+  int src_from = 0;
+  float* put = nullptr;
+  const int* put_idx = nullptr;
+  int put_from = 0;
+  __device__ __forceinline__ const float* row_src(const float* h, int r, int d) const {
+    return (src_idx && r >= src_from) ? src + static_cast<size_t>(src_idx[r - src_from]) * d
+                                      : h + static_cast<size_t>(r) * d;
+  }
+  __device__ __forceinline__ float* row_put(int r, int d) const {
+    return (put_idx && r >= put_from) ? put + static_cast<size_t>(put_idx[r - put_from]) * d
+                                      : nullptr;
+  }
+};
+// n rows gathered dst[i] = src[idx[i]] (bf16, width multiple of 8): the host
+// attention results of merged rows, folded into the RoPE launch
+struct RowCopy {
+  const bf16* src = nullptr;
+  int src_stride = 0;
+  const int* idx = nullptr;
+  int n = 0;
+  bf16* dst = nullptr;
+  int dst_stride = 0;
+  int width = 0;
+};
 int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
-                      float eps, bf16* out, int ld_out, cudaStream_t st);
+                      float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io = RowIo{});
 // rows [0, n_batch): row_* arrays (row_mode may be null = all KV-scatter);
 // rows [n_batch, rows): carry_* arrays, shipped to the host mailbox
 int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv, int head_dim,
@@ -153,7 +223,8 @@ int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv,
                      const int* row_slot, const int* row_mode, int n_batch, const int* carry_pos,
                      const int* carry_slot, bf16* qbuf, int q_row_stride, bf16* kv_pool,
                      const KvGeom& g, int layer, const int* page_table, int pt_stride, bf16* ship,
-                     int ship_stride, cudaStream_t st, int permuted = 0);
+                     int ship_stride, cudaStream_t st, int permuted = 0,
+                     const RowCopy& rc = RowCopy{});
 int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld_act,
              cudaStream_t st, int permuted = 0);
 int argmax_rows(const float* part, int splits, int rows, int vocab, int* tokens, float* logits_out,

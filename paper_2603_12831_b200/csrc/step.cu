@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <new>
 #include <vector>
@@ -90,7 +91,8 @@ struct hs_ctx {
   bool keep_logits = false;
   // metadata (device) and pinned staging
   int* dm = nullptr;   // iteration + layer metadata
-  int* hm = nullptr;   // pinned staging (two halves)
+  int* hm = nullptr;   // pinned staging (two halves), mapped
+  int* hm_d = nullptr;  // its device alias (zero-copy layer metadata)
   size_t meta_ints = 0;
   int stage_half = 0;
   size_t stage_pos = 0;
@@ -353,15 +355,19 @@ int upload_fill(hs_ctx* c, size_t dst_off, int value, size_t n) {
 
 // Packs several int arrays into one pinned staging run and ships them with a
 // single cudaMemcpyAsync into a device block; returns device pointers.
+// With dev == nullptr the kernels read the staging run itself through its
+// mapped device alias (zero-copy: no copy node between two PDL launches).
 struct Packer {
   hs_ctx* c;
   int* host = nullptr;
   int* dev;
   size_t n = 0, cap;
-  Packer(hs_ctx* c_, int* dev_, size_t cap_) : c(c_), dev(dev_), cap(cap_) {}
+  bool zero_copy;
+  Packer(hs_ctx* c_, int* dev_, size_t cap_) : c(c_), dev(dev_), cap(cap_), zero_copy(!dev_) {}
   bool reserve(size_t total) {
     host = stage(c, total);
     cap = total;
+    if (host && zero_copy) dev = c->hm_d + (host - c->hm);
     return host != nullptr;
   }
   const int* add(const int* src, size_t cnt) {
@@ -377,7 +383,7 @@ struct Packer {
     return d;
   }
   int flush(cudaStream_t st) {
-    if (n == 0) return HS_OK;
+    if (n == 0 || zero_copy) return HS_OK;
     CK(cudaMemcpyAsync(dev, host, n * sizeof(int), cudaMemcpyHostToDevice, st));
     return HS_OK;
   }
@@ -612,7 +618,8 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
     if (cpu < 0 || cpu >= CPU_SETSIZE) return set_error(HS_E_CONFIG, "cpu_list entry %d invalid", cpu);
   AffinityScope near(c->cpus);
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hm), 2 * c->meta_ints * sizeof(int),
-                   cudaHostAllocDefault));
+                   cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hm_d), c->hm, 0));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->tokens_pinned), 2 * R * sizeof(int),
                    cudaHostAllocDefault));
   for (auto& e : c->stage_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -778,6 +785,13 @@ int hs_create(const hs_model_cfg* m, const hs_rt_cfg* r, hs_ctx** out) {
 
 int hs_destroy(hs_ctx* c) {
   if (!c) return HS_OK;
+  if (g_hprof_on) {
+    static const char* names[6] = {"layer", "pack", "plan", "launch", "iter_begin", "iter_end"};
+    for (int i = 0; i < 6; ++i)
+      if (g_hprof_n[i])
+        fprintf(stderr, "[hs host] %-10s n=%8llu  %8.2f us/call  %10.1f ms total\n", names[i],
+                g_hprof_n[i], g_hprof_ns[i] / g_hprof_n[i] / 1e3, g_hprof_ns[i] / 1e6);
+  }
   cudaStreamSynchronize(c->st);
   free_all(c);
   delete c;
@@ -930,6 +944,7 @@ int hs_swap_out(hs_ctx* c, int slot, int tokens) { return kv_swap_pages(c, slot,
 int hs_swap_in(hs_ctx* c, int slot, int tokens) { return kv_swap_pages(c, slot, tokens, false); }
 
 int hs_iter_begin(hs_ctx* c, const hs_iter_desc* d) {
+  HProf hp_begin(HP_BEGIN);
   const hs_rt_cfg& r = c->r;
   if (d->n_rows < 0 || d->n_rows > r.max_rows || d->n_decode > d->n_rows ||
       d->n_chunks > r.max_chunks || d->n_logit_rows > d->n_rows || d->n_tiles > r.max_rows)
@@ -981,6 +996,7 @@ int hs_iter_begin(hs_ctx* c, const hs_iter_desc* d) {
 }
 
 int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
+  HProf hp_layer(HP_LAYER);
   const ModelCfg& m = c->m;
   const hs_rt_cfg& r = c->r;
   const MetaLayout L = layout_of(r);
@@ -997,9 +1013,10 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   ProfScope whole(c, 3, 0.0, 0.0);  // the layer's span on the device
   const int R = d->n_restart;
   const int NL = last ? c->n_logit + M : 0;
-  // one packed upload: carry slots/pos, merge slots, restart slots/pos and,
-  // at the last layer, the LM-head gather rows and their slots
-  Packer pk(c, c->dm_layer, 0);
+  // one packed staging run: carry slots/pos, merge slots, restart slots/pos
+  // and, at the last layer, the LM-head gather rows and their slots; the
+  // kernels read it in place from pinned host memory (a few hundred bytes)
+  Packer pk(c, nullptr, 0);
   const size_t total = 2 * static_cast<size_t>(C) + M + 2 * static_cast<size_t>(R) + 2 * NL;
   if (total > c->layer_cap) return set_error(HS_E_CAPACITY, "layer metadata too large");
   if (total && !pk.reserve(total)) return set_error(HS_E_CAPACITY, "metadata staging overflow");
@@ -1017,7 +1034,10 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   const int* restart_pos = total ? pk.add(d->restart_pos, R) : nullptr;
   const int* logit_rows = total ? pk.add(lrows.data(), NL) : nullptr;
   const int* logit_slots = total ? pk.add(lslots.data(), NL) : nullptr;
-  if (total) RC(pk.flush(st));
+  if (total) {
+    HProf hp(HP_PACK);
+    RC(pk.flush(st));
+  }
   if (l == 0) {
     // embed batch rows (+ injected chains: fresh token from last_token)
     RC(select_tokens(c->it_tok, c->it_slot, B, carry_slot, c->last_token, B + C, c->tok, st));
@@ -1029,6 +1049,7 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   // QKV over batch + carry rows with RoPE, KV-page scatter and the piggyback
   // ship fused into the GEMM epilogue
   EpiParams ep = epi_base(c);
+  bool gathered = false;  // host results already copied by the RoPE launch
   ep.layer = l;
   ep.row_pos = c->it_pos;
   ep.row_slot = c->it_slot;
@@ -1039,10 +1060,13 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
     RC(gemm_fused(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, EPI_QKV, ep));
   } else {
     RC(gemm(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, &sp));
+    // + merged rows: host attention results into the attention buffer
+    RowCopy rc{c->result_d, nqh, merge_slot, M, c->attn.p + static_cast<size_t>(B) * nqh, nqh, nqh};
     RC(qkv_rope_scatter(c->part, sp, B + C, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
                         c->it_pos, c->it_slot, nullptr, B, carry_pos, carry_slot, c->qbuf, nqh,
                         c->kv_pool, c->geom, l, c->page_table, r.max_pages_per_req, c->ship_d,
-                        m.qkv_n(), st, 1));
+                        m.qkv_n(), st, 1, rc));
+    gathered = true;
   }
   // attention of batch rows (K1 with the K2 merge fused into its last CTA)
   {
@@ -1060,18 +1084,24 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
                        c->n_tiles, c->attn.p, nqh, st));
   }
   // merged rows: host attention result + stored residual
-  RC(gather_rows_bf16(c->result_d, nqh, merge_slot, M, nqh,
-                      c->attn.p + static_cast<size_t>(B) * nqh, nqh, st));
-  RC(gather_rows_f32(c->resid, merge_slot, M, d_, c->h + static_cast<size_t>(B) * d_, st));
+  if (!gathered)
+    RC(gather_rows_bf16(c->result_d, nqh, merge_slot, M, nqh,
+                        c->attn.p + static_cast<size_t>(B) * nqh, nqh, st));
   const int N = B + M;
   // Proj + ResidualAdd + RMSNorm (residual add fused into the GEMM when the
   // tiles have few K-segments)
   if (fuse_ok(c, N, d_, nqh)) {
+    RC(gather_rows_f32(c->resid, merge_slot, M, d_, c->h + static_cast<size_t>(B) * d_, st));
     RC(gemm_fused(c, c->m_o[l], c->attn, N, d_, nqh, EPI_RESID, ep));
     RC(rmsnorm_rows(c->h, N, d_, c->n_post[l], m.eps, c->xn2.p, d_, st));
   } else {
     RC(gemm(c, c->m_o[l], c->attn, N, d_, nqh, &sp));
-    RC(residual_add_norm(c->part, sp, N, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, st));
+    // merged rows start from their stored residual (the residual get)
+    RowIo io;
+    io.src = c->resid;
+    io.src_idx = M ? merge_slot : nullptr;
+    io.src_from = B;
+    RC(residual_add_norm(c->part, sp, N, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, st, io));
   }
   // MLP: SiLU*up, down + ResidualAdd, then the next layer's input norm (or the
   // final norm)
@@ -1082,16 +1112,24 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
     RC(silu_mul(c->part, sp, N, m.ffn, c->act.p, m.ffn, st, 1));
   }
   const float* w_next = last ? c->w_final : c->n_in[l + 1];
+  bool put = false;  // residual put for the chains' next layer (engine.py:985)
   if (fuse_ok(c, N, d_, m.ffn)) {
     RC(gemm_fused(c, c->m_down[l], c->act, N, d_, m.ffn, EPI_RESID, ep));
     RC(rmsnorm_rows(c->h, N, d_, w_next, m.eps, c->xn.p, d_, st));
   } else {
     RC(gemm(c, c->m_down[l], c->act, N, d_, m.ffn, &sp));
-    RC(residual_add_norm(c->part, sp, N, d_, c->h, w_next, m.eps, c->xn.p, d_, st));
+    RowIo io;
+    if (!last && M) {
+      io.put = c->resid;
+      io.put_idx = merge_slot;
+      io.put_from = B;
+      put = true;
+    }
+    RC(residual_add_norm(c->part, sp, N, d_, c->h, w_next, m.eps, c->xn.p, d_, st, io));
   }
   if (!last) {
-    // residual put for the chains' next layer (engine.py:985)
-    RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, merge_slot, M, d_, c->resid, st));
+    if (!put)
+      RC(scatter_rows_f32(c->h + static_cast<size_t>(B) * d_, merge_slot, M, d_, c->resid, st));
     return HS_OK;
   }
   // ---- final layer: LM head + greedy token for decode / finishing-prefill
