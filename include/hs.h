@@ -287,6 +287,10 @@ int hs_probe_dense(hs_ctx* ctx, int n, int reps, float* us);
    op bitmask (0 QKV GEMM, 1 RoPE/KV/ship, 2 O GEMM, 3 add-norm, 4 gate-up
    GEMM, 5 SiLU, 6 down GEMM, 7 add-norm); *us = median per-layer us */
 int hs_probe_dense_mode(hs_ctx* ctx, int n, int mode, int layers, int reps, float* us);
+/* the 4 Dense GEMMs of all layers at n rows back to back (PDL chain intact)
+ * between one event pair on the step stream: median us per launch and the
+ * algorithmic bytes per launch (bench roofline) */
+int hs_probe_gemm_stream(hs_ctx* ctx, int n, int reps, float* us, double* bytes);
 int hs_probe_gemm(hs_ctx* ctx, int which, int n, int fused, int reps, float* us);
 int hs_probe_decode(hs_ctx* ctx, int g, int ctx_len, int reps, float* us);
 int hs_probe_prefill(hs_ctx* ctx, int q, int done, int reps, float* us);

@@ -26,7 +26,7 @@ CUDA_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "-I", str(ROOT / "include"), "-I", str(CSRC),
-]
+] + os.environ.get("HS_NVCC_DEFS", "").split()  # tuning experiments (-DHS_...)
 CXX_FLAGS = [
     "-O3", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-march=x86-64-v3",
     "-I", str(ROOT / "include"), "-I", str(CSRC), "-I", "/usr/local/cuda/include", "-pthread",

@@ -23,7 +23,10 @@
 
 namespace hs {
 
-constexpr int kDecStages = 3;
+#ifndef HS_DEC_STAGES
+#define HS_DEC_STAGES 3
+#endif
+constexpr int kDecStages = HS_DEC_STAGES;
 constexpr int kDecThreads = 128;
 
 int make_kv_map(CUtensorMap* map, const bf16* pool, const KvGeom& g) {

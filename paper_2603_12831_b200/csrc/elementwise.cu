@@ -50,6 +50,21 @@ __device__ __forceinline__ float4 sum_planes4(const float* __restrict__ p, size_
   return a;
 }
 
+// Every plane's load in flight at once (one memory round trip for up to
+// kMaxSplits planes), summed plane 0 first -- the same order as sum_planes4.
+__device__ __forceinline__ float4 sum_planes4_all(const float* __restrict__ p, size_t plane,
+                                                  int splits) {
+  float4 v[kMaxSplits];
+#pragma unroll
+  for (int k = 0; k < kMaxSplits; ++k)
+    if (k < splits) v[k] = ld4(p + k * plane);
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < kMaxSplits; ++k)
+    if (k < splits) add4(a, v[k]);
+  return a;
+}
+
 // two streams at once (gate and up of SwiGLU): twice the loads in flight
 __device__ __forceinline__ void sum_planes4x2(const float* __restrict__ p,
                                               const float* __restrict__ q, size_t plane,
@@ -192,7 +207,7 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
   for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4) {
     float4 v = *reinterpret_cast<const float4*>(xin + i);
     if (splits > 0) {
-      const float4 a = sum_planes4(pp + i, plane, splits);
+      const float4 a = sum_planes4_all(pp + i, plane, splits);
       v.x += a.x;
       v.y += a.y;
       v.z += a.z;
@@ -295,8 +310,9 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// below this many rows the 8-CTA cluster form spreads a row over more SMs
-constexpr int kClusterRowsMax = 4;
+// up to this many rows the 8-CTA cluster form (one float4 column group per
+// thread, every plane in flight) beats a CTA per row
+constexpr int kClusterRowsMax = 64;
 
 int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
                       float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io) {
@@ -306,8 +322,9 @@ int residual_add_norm(const float* part, int splits, int rows, int d, float* h, 
     return launch_pdl(residual_add_norm_rows_kernel, dim3(rows), dim3(256), 0, st, part, splits,
                       rows, d, h, w, eps, out, ld_out, io);
   dim3 grid(kNormCluster, rows);
-  return launch_pdl(residual_add_norm_kernel, dim3(grid), dim3(256), 0, st, part, splits, rows, d,
-                    h, w, eps, out, ld_out, io);
+  const int threads = std::min(256, ((d / kNormCluster / 4) + 31) / 32 * 32);
+  return launch_pdl(residual_add_norm_kernel, dim3(grid), dim3(threads), 0, st, part, splits, rows,
+                    d, h, w, eps, out, ld_out, io);
 }
 
 // ---------------------------------------------------------------- QKV epilogue
@@ -362,7 +379,7 @@ __global__ void __launch_bounds__(256)
   const int mode = batch ? (row_mode ? row_mode[r] : 0) : 1;
   float a1, a2, b1, b2;  // (x1, x2) of pairs j and j+1
   if (permuted) {  // feature i of the head in row 2i, feature i + hd/2 in row 2i+1
-    const float4 v = sum_planes4(src + 2 * j, plane, splits);
+    const float4 v = sum_planes4_all(src + 2 * j, plane, splits);
     a1 = v.x, a2 = v.y, b1 = v.z, b2 = v.w;
   } else {
     const float2 lo = sum_planes2(src + j, plane, splits);
@@ -475,10 +492,45 @@ __global__ void __cluster_dims__(kArgCluster, 1, 1) __launch_bounds__(512)
   const float* src = part + static_cast<size_t>(r) * vocab;
   float best = -CUDART_INF_F;
   int bi = 0x7fffffff;
-  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const float v = sum_planes1(src + i, plane, splits);
-    if (logits_out) logits_out[static_cast<size_t>(r) * vocab + i] = v;
-    better(best, bi, v, i);
+  if ((vocab & 3) == 0) {
+    // float4 columns, kArgVec per thread with every load of a plane in flight
+    // (planes summed plane 0 first, as sum_planes1 does)
+    constexpr int kArgVec = 8;
+    const int n4 = vocab / 4, per4 = (n4 + kArgCluster - 1) / kArgCluster;
+    const int lo4 = rank * per4, hi4 = min(n4, lo4 + per4);
+    for (int base = lo4; base < hi4; base += kArgVec * blockDim.x) {
+      float4 acc[kArgVec];
+#pragma unroll
+      for (int j = 0; j < kArgVec; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int sp = 0; sp < splits; ++sp) {
+        float4 t[kArgVec];
+#pragma unroll
+        for (int j = 0; j < kArgVec; ++j) {
+          const int i4 = base + j * blockDim.x + threadIdx.x;
+          if (i4 < hi4) t[j] = ld4(src + sp * plane + 4 * i4);
+        }
+#pragma unroll
+        for (int j = 0; j < kArgVec; ++j)
+          if (base + j * blockDim.x + threadIdx.x < hi4) add4(acc[j], t[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kArgVec; ++j) {
+        const int i4 = base + j * blockDim.x + threadIdx.x;
+        if (i4 >= hi4) continue;
+        if (logits_out)
+          *reinterpret_cast<float4*>(logits_out + static_cast<size_t>(r) * vocab + 4 * i4) = acc[j];
+        better(best, bi, acc[j].x, 4 * i4);
+        better(best, bi, acc[j].y, 4 * i4 + 1);
+        better(best, bi, acc[j].z, 4 * i4 + 2);
+        better(best, bi, acc[j].w, 4 * i4 + 3);
+      }
+    }
+  } else {
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      const float v = sum_planes1(src + i, plane, splits);
+      if (logits_out) logits_out[static_cast<size_t>(r) * vocab + i] = v;
+      better(best, bi, v, i);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)

@@ -30,9 +30,15 @@ constexpr int kGemmThreads = 192;
 constexpr int kTileM = 128;  // output features per CTA tile
 constexpr int kTileK = 64;   // one 128-byte swizzle atom of bf16
 
+#ifndef HS_GEMM_ST16
+#define HS_GEMM_ST16 4
+#endif
+#ifndef HS_GEMM_ST32
+#define HS_GEMM_ST32 4
+#endif
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = BN <= 16 ? 6 : (BN <= 32 ? 5 : 4);
+  static constexpr int kStages = BN <= 16 ? HS_GEMM_ST16 : (BN <= 32 ? HS_GEMM_ST32 : 4);
   static constexpr int kABytes = kTileM * kTileK * 2;
   static constexpr int kBBytes = BN * kTileK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;

@@ -995,8 +995,22 @@ int hs_iter_begin(hs_ctx* c, const hs_iter_desc* d) {
   return HS_OK;
 }
 
+// HS_SKIP (probe knob, read once): bit mask of layer launches to leave out
+// so tools/probe_step.py can measure each kernel's in-stream cost by
+// ablation -- 1 RoPE, 2 decode attention, 4 add-norm after O, 8 SiLU,
+// 16 add-norm after down, 32/64/128/256 the QKV/O/gate-up/down GEMMs.
+// Results are garbage with any bit set; never set in serving.
+static int skip_mask() {
+  static const int m = [] {
+    const char* e = getenv("HS_SKIP");
+    return e ? atoi(e) : 0;
+  }();
+  return m;
+}
+
 int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   HProf hp_layer(HP_LAYER);
+  const int skip = skip_mask();
   const ModelCfg& m = c->m;
   const hs_rt_cfg& r = c->r;
   const MetaLayout L = layout_of(r);
@@ -1059,19 +1073,21 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   if (fuse_ok(c, B + C, m.qkv_n(), d_)) {
     RC(gemm_fused(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, EPI_QKV, ep));
   } else {
-    RC(gemm(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, &sp));
+    if (!(skip & 32)) RC(gemm(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, &sp));
     // + merged rows: host attention results into the attention buffer
     RowCopy rc{c->result_d, nqh, merge_slot, M, c->attn.p + static_cast<size_t>(B) * nqh, nqh, nqh};
-    RC(qkv_rope_scatter(c->part, sp, B + C, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
-                        c->it_pos, c->it_slot, nullptr, B, carry_pos, carry_slot, c->qbuf, nqh,
-                        c->kv_pool, c->geom, l, c->page_table, r.max_pages_per_req, c->ship_d,
-                        m.qkv_n(), st, 1, rc));
+    if (!(skip & 1))
+      RC(qkv_rope_scatter(c->part, sp, B + C, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
+                          c->it_pos, c->it_slot, nullptr, B, carry_pos, carry_slot, c->qbuf, nqh,
+                          c->kv_pool, c->geom, l, c->page_table, r.max_pages_per_req, c->ship_d,
+                          m.qkv_n(), st, 1, rc));
     gathered = true;
   }
   // attention of batch rows (K1 with the K2 merge fused into its last CTA)
   {
   ProfScope pd(c, 1, c->dec_kv_tokens * 2.0 * m.n_kv * m.hd * 2.0 + 4.0 * c->D * nqh,
                4.0 * c->dec_kv_tokens * nqh);
+  if (!(skip & 2))
   RC(decode_attention_fused(c->m_kv, c->geom, l, c->qbuf, nqh, m.n_q, c->page_table,
                             r.max_pages_per_req, reinterpret_cast<const DecodeChunk*>(c->it_chunks),
                             c->n_chunks, c->it_cbeg, c->o_part, c->lse_part, c->dec_counters,
@@ -1095,21 +1111,22 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
     RC(gemm_fused(c, c->m_o[l], c->attn, N, d_, nqh, EPI_RESID, ep));
     RC(rmsnorm_rows(c->h, N, d_, c->n_post[l], m.eps, c->xn2.p, d_, st));
   } else {
-    RC(gemm(c, c->m_o[l], c->attn, N, d_, nqh, &sp));
+    if (!(skip & 64)) RC(gemm(c, c->m_o[l], c->attn, N, d_, nqh, &sp));
     // merged rows start from their stored residual (the residual get)
     RowIo io;
     io.src = c->resid;
     io.src_idx = M ? merge_slot : nullptr;
     io.src_from = B;
-    RC(residual_add_norm(c->part, sp, N, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, st, io));
+    if (!(skip & 4))
+      RC(residual_add_norm(c->part, sp, N, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, st, io));
   }
   // MLP: SiLU*up, down + ResidualAdd, then the next layer's input norm (or the
   // final norm)
   if (fuse_ok(c, N, 2 * m.ffn, d_)) {
     RC(gemm_fused(c, c->m_gu[l], c->xn2, N, 2 * m.ffn, d_, EPI_SILU, ep));
   } else {
-    RC(gemm(c, c->m_gu[l], c->xn2, N, 2 * m.ffn, d_, &sp));
-    RC(silu_mul(c->part, sp, N, m.ffn, c->act.p, m.ffn, st, 1));
+    if (!(skip & 128)) RC(gemm(c, c->m_gu[l], c->xn2, N, 2 * m.ffn, d_, &sp));
+    if (!(skip & 8)) RC(silu_mul(c->part, sp, N, m.ffn, c->act.p, m.ffn, st, 1));
   }
   const float* w_next = last ? c->w_final : c->n_in[l + 1];
   bool put = false;  // residual put for the chains' next layer (engine.py:985)
@@ -1117,7 +1134,7 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
     RC(gemm_fused(c, c->m_down[l], c->act, N, d_, m.ffn, EPI_RESID, ep));
     RC(rmsnorm_rows(c->h, N, d_, w_next, m.eps, c->xn.p, d_, st));
   } else {
-    RC(gemm(c, c->m_down[l], c->act, N, d_, m.ffn, &sp));
+    if (!(skip & 256)) RC(gemm(c, c->m_down[l], c->act, N, d_, m.ffn, &sp));
     RowIo io;
     if (!last && M) {
       io.put = c->resid;
@@ -1125,7 +1142,8 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
       io.put_from = B;
       put = true;
     }
-    RC(residual_add_norm(c->part, sp, N, d_, c->h, w_next, m.eps, c->xn.p, d_, st, io));
+    if (!(skip & 16))
+      RC(residual_add_norm(c->part, sp, N, d_, c->h, w_next, m.eps, c->xn.p, d_, st, io));
   }
   if (!last) {
     if (!put)
@@ -1298,6 +1316,33 @@ int hs_probe_dense(hs_ctx* c, int n, int reps, float* us) {
     RC(rmsnorm_rows(c->h, n, d_, c->n_in[0], m.eps, c->xn.p, d_, c->st));
     return HS_OK;
   }, us);
+}
+
+// The four Dense GEMMs of every layer at n rows, back to back on the step's
+// stream (PDL chain intact, weights streamed from HBM: 16 GB per pass >> L2)
+// between one pair of events, on the live activation buffers; results go to
+// the split-K scratch only, so a running serving context is not disturbed.
+// *us = median time per launch, *bytes = algorithmic bytes per launch.
+int hs_probe_gemm_stream(hs_ctx* c, int n, int reps, float* us, double* bytes) {
+  const ModelCfg& m = c->m;
+  if (n < 1 || n > c->r.max_rows) return set_error(HS_E_CONFIG, "probe rows out of range");
+  const int d_ = m.d, nqh = m.n_q * m.hd;
+  const double per_layer = 2.0 * (static_cast<double>(m.qkv_n()) * d_ + static_cast<double>(d_) * nqh +
+                                  2.0 * m.ffn * d_ + static_cast<double>(d_) * m.ffn) +
+                           2.0 * n * (d_ + m.qkv_n() + nqh + d_ + d_ + 2.0 * m.ffn + m.ffn + d_);
+  int err = time_reps(c, reps, [&]() -> int {
+    int s;
+    for (int l = 0; l < m.layers; ++l) {
+      RC(gemm(c, c->m_qkv[l], c->xn, n, m.qkv_n(), d_, &s));
+      RC(gemm(c, c->m_o[l], c->attn, n, d_, nqh, &s));
+      RC(gemm(c, c->m_gu[l], c->xn2, n, 2 * m.ffn, d_, &s));
+      RC(gemm(c, c->m_down[l], c->act, n, d_, m.ffn, &s));
+    }
+    return HS_OK;
+  }, us);
+  *us /= 4 * m.layers;
+  *bytes = per_layer / 4;
+  return err;
 }
 
 // The dense part of `layers` consecutive layers exactly as hs_layer issues it
