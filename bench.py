@@ -371,7 +371,8 @@ def run_ours(args) -> None:
             profiler.save(models, out, {"config": args.config, "how": "hs_probe_* on B200"})
     else:
         models = profiler.load(models_path)
-    engine = LiveEngine(scenario, models=models, step=step, pace_layers=args.pace)
+    engine = LiveEngine(scenario, models=models, step=step, pace_layers=args.pace,
+                        pace_tail=args.pace_tail)
     backlog = BeBacklog(engine, step, args.be_chains, args.seed + rank)
     if args.ls_decodes:
         prepopulate_ls(engine, step, args.ls_decodes, args.seed + rank)
@@ -393,6 +394,7 @@ def run_ours(args) -> None:
     launches0 = step.ctx.lib.hs_launch_count()
     h2d0, d2h0 = step.h2d_bytes, step.d2h_bytes
     cpu0, be_cpu0 = step.ctx.cpu_busy_seconds(), engine.counters["be_tokens_cpu"]
+    host0 = dict(engine.host_s)
     # timed region: no per-kernel events (an event between two PDL launches
     # serialises them; measured +2.6 ms/step on llama3-8b)
     with ClockSampler(local) as clocks:
@@ -412,6 +414,7 @@ def run_ours(args) -> None:
     launches = step.ctx.lib.hs_launch_count() - launches0
     h2d1, d2h1 = step.h2d_bytes, step.d2h_bytes
     cpu_busy = step.ctx.cpu_busy_seconds() - cpu0
+    host_ms = {k: (engine.host_s[k] - host0[k]) * 1e3 / max(args.steps, 1) for k in host0}
     be_cpu = engine.counters["be_tokens_cpu"] - be_cpu0
     it1 = len(engine.iteration_log)
     # profiled window: the same workload continued for --profile-steps more
@@ -511,6 +514,7 @@ def run_ours(args) -> None:
                    "model": args.config, "ls_rate_per_s": args.ls_rate,
                    "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
                    "cpu_threads_per_replica": rt.cpu_threads, "parallelism": f"replicas x{world}",
+                   "pace_layers": args.pace, "pace_tail": args.pace_tail,
                    "l2": "working set (16 GB weights/iteration) > 126 MB L2"},
         "ls_tpot_attainment": attain, "ls_tpot_p99_ms": float(mx[2]),
         "ls_tokens": int(tot[1]), "be_tokens": int(tot[0]), "ls_gaps": int(tot[3]),
@@ -520,6 +524,7 @@ def run_ours(args) -> None:
         if iters else 0,
         "be_tokens_via_cpu_attention": be_cpu,
         "cpu_pool_busy_frac": cpu_busy / max(wall_s * rt.cpu_threads, 1e-9),
+        "host_ms_per_step": host_ms,
         "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters
                                               if i.get("device_ms")) if iters else None,
         "device_breakdown_ms": {"window": f"{args.profile_steps} profiled steps after the timed "
@@ -575,6 +580,8 @@ def main() -> None:
     ap.add_argument("--piggyback-reserve-us", type=float, default=100.0)
     ap.add_argument("--max-rows", type=int, default=4096)
     ap.add_argument("--pace", type=int, default=2, help="layers the host may run ahead")
+    ap.add_argument("--pace-tail", type=int, default=12,
+                    help="final layers of an iteration launched unpaced (covers host planning)")
     ap.add_argument("--calibrate", action="store_true")
     ap.add_argument("--calibrate-out", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -39,10 +39,16 @@ from .workload import build_requests
 
 
 class LiveEngine(Engine):
-    def __init__(self, scenario, models=None, step=None, pace_layers: int = 1):
+    def __init__(self, scenario, models=None, step=None, pace_layers: int = 1,
+                 pace_tail: int = 0):
         super().__init__(scenario, models=models, step=step)
         self.t0 = time.perf_counter()
         self.pace_layers = pace_layers
+        # the last `pace_tail` layers of an iteration are launched without
+        # waiting for the GPU, so the queue holds enough work to cover the
+        # host's planning of the next iteration (merge decisions of those
+        # layers are made that much earlier)
+        self.pace_tail = pace_tail
         self._unshipped: dict[str, object] = {}   # WorkItems awaiting their ship launch
         self._submitted: dict[str, object] = {}   # WorkItems in the CPU pool
         # results enter the output FIFO in submission order (a reorder
@@ -57,6 +63,9 @@ class LiveEngine(Engine):
         self._dirty = True
         self.iteration_log: list[dict] = []
         self._last_done = None
+        # host-time accounting (seconds): planning, layer issue, waiting on
+        # the GPU in pace(); the bench reports it to tell host- from GPU-bound
+        self.host_s = {"plan": 0.0, "issue": 0.0, "pace_wait": 0.0}
 
     def clock(self) -> float:
         return time.perf_counter() - self.t0
@@ -153,7 +162,11 @@ class LiveEngine(Engine):
         self.step.begin_iteration(plan)
         for layer in range(1, self.layers + 1):
             it.layer = layer
-            self.step.pace(self.pace_layers)
+            tail = layer > self.layers - self.pace_tail
+            t_w = time.perf_counter()
+            self.step.pace(self.pace_tail if tail else self.pace_layers)
+            t_i = time.perf_counter()
+            self.host_s["pace_wait"] += t_i - t_w
             self._poll_async()
             self.now = start = self.clock()
             merged = self._consume_merges(layer, cap)
@@ -164,6 +177,7 @@ class LiveEngine(Engine):
             outcomes = [(item, self._process_merge(item, layer, start, start))
                         for item in merged]
             self._submit_shipped(self.step.layer(layer, outcomes))
+            self.host_s["issue"] += time.perf_counter() - t_i
             if self.opts.record_layer_times:
                 self.layer_start_log.append((it.start, layer, start))
         # Pipelined: queue the token readback and commit now; the host plans
@@ -232,7 +246,10 @@ class LiveEngine(Engine):
             self._resolve_iterations()
             if self._dirty and self._runnable():
                 self._dirty = False
-                if self._live_iteration(self._plan()):
+                t_p = time.perf_counter()
+                plan = self._plan()
+                self.host_s["plan"] += time.perf_counter() - t_p
+                if self._live_iteration(plan):
                     n += 1
                     if on_iteration:
                         on_iteration(n)

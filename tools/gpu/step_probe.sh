@@ -1,5 +1,3 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
-for a in "8 700 0" "32 700 0" "16 2000 0" "8 700 4"; do timeout 300 python tools/probe_step.py $a 30 2>&1 | grep "device"; done
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 400 --csv --log-file gpurun_out/step_launches.csv python tools/probe_step.py 8 700 2 4 > /dev/null 2>&1
-python tools/ncu_summary.py gpurun_out/step_launches.csv
+timeout 300 python tools/probe_gemm_fused.py 8 32 2>&1
+for a in "8 700 0" "32 700 0"; do for f in 0 1 4 5; do printf "fused %d " $f; HS_FUSED=$f timeout 120 python tools/probe_step.py $a 30 2>&1 | grep "device-only\|rror"; done; done
