@@ -469,11 +469,22 @@ def run_ours(args) -> None:
     rc = step.ctx.lib.hs_probe_gemm_stream(step.ctx.h, rows_mean, 5, C_byref(us_l), C_byref(by_l))
     if rc != 0:
         raise RuntimeError(f"hs_probe_gemm_stream failed ({rc})")
-    achieved_gbs = by_l.value / (us_l.value * 1e-6) / 1e9
+    gemm_us, gemm_by = us_l.value, by_l.value
+    achieved_gbs = gemm_by / (gemm_us * 1e-6) / 1e9
+    # PCIe rate of the piggyback mailboxes (q|k|v ship D2H by SM stores into
+    # mapped pinned memory, host results H2D by SM loads), with the copy
+    # engine's rate for the same bytes alongside
+    step.ctx.lib.hs_probe_pcie.argtypes = [C_void_p, C_int, C_int, C_int, C_POINTER(C_float),
+                                          C_POINTER(C_double)]
+    pcie = {}
+    for d_, name in enumerate(("ship_sm_store", "result_sm_load", "copy_engine_d2h",
+                               "copy_engine_h2d")):
+        rc = step.ctx.lib.hs_probe_pcie(step.ctx.h, d_, 64, 7, C_byref(us_l), C_byref(by_l))
+        pcie[name + "_gbs"] = by_l.value / (us_l.value * 1e-6) / 1e9 if rc == 0 else None
     params = (model.qkv_dim * model.d_model + model.d_model * model.n_q * model.head_dim
               + 3 * model.ffn * model.d_model)
     flops_l = 2.0 * rows_mean * params / 4
-    intensity = flops_l / by_l.value
+    intensity = flops_l / gemm_by
     traffic = None
     tr_path = ROOT / "profiles" / "ncu_gemm_traffic.json"
     if tr_path.exists():
@@ -482,11 +493,11 @@ def run_ours(args) -> None:
         roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved_gbs / pk["hbm_gbs"], "traffic": traffic}
     else:
-        tf = flops_l / (us_l.value * 1e-6) / 1e12
+        tf = flops_l / (gemm_us * 1e-6) / 1e12
         roof = {"bound": "tensor", "achieved": tf, "peak": pk["bf16_tflops_sustained"],
                 "unit": "TFLOP/s", "frac": tf / pk["bf16_tflops_sustained"], "traffic": traffic}
     roof.update({"kernel": "gemm_bf16_tn_kernel (tcgen05, Dense QKV/O/gate-up/down)",
-                 "rows": rows_mean, "us_per_launch": us_l.value, "bytes_per_launch": by_l.value,
+                 "rows": rows_mean, "us_per_launch": gemm_us, "bytes_per_launch": gemm_by,
                  "window": f"4 x {model.n_layers} Dense GEMM launches at the run's mean batch "
                            f"({rows_mean} rows) back to back between one event pair (median of 5)",
                  "serialised_window": {
@@ -535,6 +546,14 @@ def run_ours(args) -> None:
                                 "other_kernels": stats[3, 1] - stats[0, 1] - stats[1, 1] - stats[2, 1],
                                 "between_layers": prof_s * 1e3 - stats[3, 1]},
         "roofline": roof,
+        "piggyback": {
+            "ship_bytes_per_step": (d2h1 - d2h0) / max(args.steps, 1),
+            "result_bytes_per_step": (h2d1 - h2d0) / max(args.steps, 1),
+            "items_per_step": n_merges / max(1, len(iters)),
+            "pcie_probe_64_items": pcie,
+            "link_us_per_step": ((d2h1 - d2h0) / max(args.steps, 1) / (pcie["ship_sm_store_gbs"] or 1)
+                                 + (h2d1 - h2d0) / max(args.steps, 1)
+                                 / (pcie["result_sm_load_gbs"] or 1)) / 1e3},
         "e2e": {"value": e2e_val, "unit": UNIT,
                 "h2d_bytes_per_step": (h2d1 - h2d0) / max(args.steps, 1),
                 "d2h_bytes_per_step": (d2h1 - d2h0) / max(args.steps, 1)},

@@ -179,6 +179,19 @@ enum {
 int hs_create(const hs_model_cfg* model, const hs_rt_cfg* rt, hs_ctx** out);
 int hs_destroy(hs_ctx* ctx);
 void* hs_stream(hs_ctx* ctx);
+
+/* Tensor parallelism (config 4; the reference folds it into gamma,
+ * engine.py:944 / latency.py:141-147).  Each rank's context holds its shard
+ * (q/kv heads and ffn columns; O and down row-parallel); the two all-reduces
+ * per layer are fused into the residual-add + RMSNorm launches and read the
+ * peers' partials over NVLink P2P.  Multi-process: every rank exports its
+ * exchange handles (HS_TP_HANDLE_BYTES), the caller all-gathers them (e.g.
+ * torch.distributed over gloo) and passes all ranks' handles in rank order to
+ * hs_tp_open.  Every rank must then issue the same sequence of hs_layer
+ * calls with the same row counts (identical, deterministic engines). */
+#define HS_TP_HANDLE_BYTES 128
+int hs_tp_export(hs_ctx* ctx, void* handles /* HS_TP_HANDLE_BYTES */);
+int hs_tp_open(hs_ctx* ctx, int rank, int world, const void* all_handles /* world x 128 */);
 /* bf16 matrices [out][in] (qkv rows: q heads, k heads, v heads; gate_up
  * rows: gate then up), fp32 norm vectors.  Layer is 0-based. */
 int hs_set_weight(hs_ctx* ctx, int kind, int layer, const void* host, size_t bytes);
@@ -291,6 +304,10 @@ int hs_probe_dense_mode(hs_ctx* ctx, int n, int mode, int layers, int reps, floa
  * between one event pair on the step stream: median us per launch and the
  * algorithmic bytes per launch (bench roofline) */
 int hs_probe_gemm_stream(hs_ctx* ctx, int n, int reps, float* us, double* bytes);
+/* PCIe rate of the piggyback mailboxes: dir 0 SM stores to the mapped ship
+ * mailbox, 1 SM loads from the mapped result mailbox, 2/3 the same bytes by
+ * the copy engine (D2H/H2D); `rows` items; median us and bytes moved */
+int hs_probe_pcie(hs_ctx* ctx, int dir, int rows, int reps, float* us, double* bytes);
 int hs_probe_gemm(hs_ctx* ctx, int which, int n, int fused, int reps, float* us);
 int hs_probe_decode(hs_ctx* ctx, int g, int ctx_len, int reps, float* us);
 int hs_probe_prefill(hs_ctx* ctx, int q, int done, int reps, float* us);

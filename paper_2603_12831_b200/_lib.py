@@ -83,7 +83,7 @@ def load() -> C.CDLL:
 _SPECIAL = ["hs_version", "hs_stream", "hs_cpu_busy_seconds", "hs_wall_seconds",
             "hs_launch_count", "hs_profile", "hs_profile_read", "hs_probe_dense",
             "hs_probe_decode", "hs_probe_prefill", "hs_probe_gemm", "hs_probe_dense_mode",
-            "hs_probe_gemm_stream"]
+            "hs_probe_gemm_stream", "hs_probe_pcie", "hs_tp_export", "hs_tp_open"]
 
 
 def exported_symbols() -> list[str]:

@@ -238,6 +238,110 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
   }
 }
 
+// Tensor-parallel form: h = (io source | h) + sum over ranks (rank order) of
+// each rank's local split-K sum, then the same cluster RMSNorm.  The
+// dependents are released only after every peer has published, so a
+// PDL-launched successor never occupies SMs a peer context still needs.
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
+    tp_add_norm_kernel(const float* __restrict__ part, int splits, int rows, int d,
+                       float* __restrict__ h, const float* __restrict__ w, float eps,
+                       bf16* __restrict__ out, int ld_out, RowIo io, TpPeers peers,
+                       unsigned epoch) {
+  pdl_wait();
+  __shared__ float red[32];
+  __shared__ float ssq_cta;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int cols = d / kNormCluster;
+  const int c0 = rank * cols;
+  const int par = epoch & 1;
+  const size_t plane = static_cast<size_t>(rows) * d;
+  // a fixed grid loops over the rows (every rank's grid is small enough to
+  // be resident next to its peers' even when a group shares one device)
+  for (int r = blockIdx.y; r < rows; r += gridDim.y) {
+    const float* pp = part + static_cast<size_t>(r) * d + c0;
+    const size_t xoff = par * peers.xbuf_par + static_cast<size_t>(r) * d + c0;
+    const size_t foff = par * peers.flag_par + static_cast<size_t>(r) * kNormCluster + rank;
+    // 1. publish this rank's partial of these columns
+    float* mine = peers.xbuf[peers.me] + xoff;
+    for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4)
+      *reinterpret_cast<float4*>(mine + i) = sum_planes4_all(pp + i, plane, splits);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      st_release_sys(peers.flag[peers.me] + foff, epoch);
+      // 2. wait for every peer's partial of the same columns
+      for (int p = 0; p < peers.world; ++p) {
+        unsigned spins = 0;
+        while (static_cast<int>(ld_acquire_sys(peers.flag[p] + foff) - epoch) < 0) {
+          __nanosleep(64);
+          if (++spins > (1u << 25)) __trap();  // a peer never published: fail, do not hang
+        }
+      }
+    }
+    __syncthreads();
+    // 3. h = source + sum of all ranks' partials in rank order
+    float* x = h + static_cast<size_t>(r) * d + c0;
+    const float* xin = io.row_src(h, r, d) + c0;
+    float* put = io.row_put(r, d);
+    float ss = 0.f;
+    for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int p = 0; p < peers.world; ++p)
+        add4(a, __ldcv(reinterpret_cast<const float4*>(peers.xbuf[p] + xoff + i)));
+      float4 v = *reinterpret_cast<const float4*>(xin + i);
+      add4(v, a);
+      *reinterpret_cast<float4*>(x + i) = v;
+      if (put) *reinterpret_cast<float4*>(put + c0 + i) = v;
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = block_sum(ss, red);
+    if (threadIdx.x == 0) ssq_cta = ss;
+    cluster.sync();
+    float total = 0.f;
+#pragma unroll
+    for (int k = 0; k < kNormCluster; ++k) total += *cluster.map_shared_rank(&ssq_cta, k);
+    cluster.sync();
+    const float inv = rsqrtf(total / d + eps);
+    bf16* o = out + static_cast<size_t>(r) * ld_out + c0;
+    const float* wp = w + c0;
+    for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4) {
+      const float4 v = *reinterpret_cast<const float4*>(x + i);
+      const float4 g = *reinterpret_cast<const float4*>(wp + i);
+      uint2 pk;
+      pk.x = pack_bf16x2(v.x * inv * g.x, v.y * inv * g.y);
+      pk.y = pack_bf16x2(v.z * inv * g.z, v.w * inv * g.w);
+      *reinterpret_cast<uint2*>(o + i) = pk;
+    }
+  }
+  // dependents are released only once every peer has published (no
+  // PDL-launched successor may take SMs a peer context still needs)
+  pdl_trigger();
+}
+
+int tp_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
+                float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io,
+                const TpPeers& peers, unsigned epoch) {
+  if (rows <= 0) return HS_OK;
+  if (d % (4 * kNormCluster) || splits > kMaxSplits || splits < 1 || peers.world < 1 ||
+      peers.world > kMaxTp)
+    return HS_E_CONFIG;
+  constexpr int kTpRowCtas = 32;  // clusters per rank (rows are looped over)
+  dim3 grid(kNormCluster, std::min(rows, kTpRowCtas));
+  const int threads = std::min(256, ((d / kNormCluster / 4) + 31) / 32 * 32);
+  return launch_pdl(tp_add_norm_kernel, dim3(grid), dim3(threads), 0, st, part, splits, rows, d,
+                    h, w, eps, out, ld_out, io, peers, epoch);
+}
+
 // Many rows: one 256-thread CTA per row holding the row in registers (up to
 // kRowVec float4 per thread, d <= 8192), no cluster barriers.
 constexpr int kRowVec = 8;

@@ -216,6 +216,25 @@ struct RowCopy {
 };
 int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
                       float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io = RowIo{});
+
+// ---- tensor parallelism: the all-reduce of a row-parallel projection fused
+// into its residual-add + RMSNorm (elementwise.cu).  Every rank publishes its
+// local partial rows into its own exchange buffer and raises a per-(row,
+// column block) flag; peers read the partials straight from that memory
+// (NVLink P2P through CUDA IPC, or the same device for a single-process
+// group) once the flag shows the exchange's epoch, and all ranks sum them in
+// rank order, so the new residual stream is bit-identical on every rank.
+constexpr int kMaxTp = 8;
+struct TpPeers {
+  float* xbuf[kMaxTp];      // each rank's exchange buffer [2][max_rows][d] fp32
+  unsigned* flag[kMaxTp];   // each rank's flags [2][max_rows * 8]
+  int world = 1, me = 0;
+  size_t xbuf_par = 0;      // floats per parity
+  size_t flag_par = 0;      // flags per parity
+};
+int tp_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
+                float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io,
+                const TpPeers& peers, unsigned epoch);
 // rows [0, n_batch): row_* arrays (row_mode may be null = all KV-scatter);
 // rows [n_batch, rows): carry_* arrays, shipped to the host mailbox
 int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv, int head_dim,

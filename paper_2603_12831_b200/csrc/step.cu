@@ -107,6 +107,14 @@ struct hs_ctx {
   std::vector<int> h_logit_rows, h_logit_slots;  // host copies (layer-L gather lists)
   int* dec_counters = nullptr;
   int* tile_sem = nullptr;  // stream-K fixup semaphores of the fused GEMMs
+  // tensor parallelism (hs_tp_*): this rank's exchange buffer and flags, the
+  // group's pointers, the exchange counter and the IPC mappings to close
+  int tp_world = 1, tp_rank = 0;
+  float* tp_xbuf = nullptr;
+  unsigned* tp_flag = nullptr;
+  TpPeers tp{};
+  unsigned tp_epoch = 0;
+  std::vector<void*> tp_opened;
   int* tokens_pinned = nullptr;
   // piggyback mailboxes (pinned, mapped)
   bf16 *ship_h = nullptr, *ship_d = nullptr, *result_h = nullptr, *result_d = nullptr;
@@ -1017,6 +1025,7 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   const int l = d->layer - 1;  // 0-based
   const int B = c->B, C = d->n_carry, M = d->n_merge;
   const bool last = d->layer == m.layers;
+  const bool tp = c->tp_world > 1;  // row-parallel O / down: fused all-reduce
   if (l < 0 || l >= m.layers) return set_error(HS_E_CONFIG, "layer %d out of range", d->layer);
   if (B + C > r.max_rows || B + M > r.max_rows || d->n_restart > M)
     return set_error(HS_E_CAPACITY, "layer rows exceed max_rows");
@@ -1106,7 +1115,15 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   const int N = B + M;
   // Proj + ResidualAdd + RMSNorm (residual add fused into the GEMM when the
   // tiles have few K-segments)
-  if (fuse_ok(c, N, d_, nqh)) {
+  if (tp) {
+    RC(gemm(c, c->m_o[l], c->attn, N, d_, nqh, &sp));
+    RowIo io;
+    io.src = c->resid;
+    io.src_idx = M ? merge_slot : nullptr;
+    io.src_from = B;
+    RC(tp_add_norm(c->part, sp, N, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, st, io, c->tp,
+                   ++c->tp_epoch));
+  } else if (fuse_ok(c, N, d_, nqh)) {
     RC(gather_rows_f32(c->resid, merge_slot, M, d_, c->h + static_cast<size_t>(B) * d_, st));
     RC(gemm_fused(c, c->m_o[l], c->attn, N, d_, nqh, EPI_RESID, ep));
     RC(rmsnorm_rows(c->h, N, d_, c->n_post[l], m.eps, c->xn2.p, d_, st));
@@ -1122,7 +1139,7 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   }
   // MLP: SiLU*up, down + ResidualAdd, then the next layer's input norm (or the
   // final norm)
-  if (fuse_ok(c, N, 2 * m.ffn, d_)) {
+  if (!tp && fuse_ok(c, N, 2 * m.ffn, d_)) {
     RC(gemm_fused(c, c->m_gu[l], c->xn2, N, 2 * m.ffn, d_, EPI_SILU, ep));
   } else {
     if (!(skip & 128)) RC(gemm(c, c->m_gu[l], c->xn2, N, 2 * m.ffn, d_, &sp));
@@ -1130,7 +1147,18 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   }
   const float* w_next = last ? c->w_final : c->n_in[l + 1];
   bool put = false;  // residual put for the chains' next layer (engine.py:985)
-  if (fuse_ok(c, N, d_, m.ffn)) {
+  if (tp) {
+    RC(gemm(c, c->m_down[l], c->act, N, d_, m.ffn, &sp));
+    RowIo io;
+    if (!last && M) {
+      io.put = c->resid;
+      io.put_idx = merge_slot;
+      io.put_from = B;
+      put = true;
+    }
+    RC(tp_add_norm(c->part, sp, N, d_, c->h, w_next, m.eps, c->xn.p, d_, st, io, c->tp,
+                   ++c->tp_epoch));
+  } else if (fuse_ok(c, N, d_, m.ffn)) {
     RC(gemm_fused(c, c->m_down[l], c->act, N, d_, m.ffn, EPI_RESID, ep));
     RC(rmsnorm_rows(c->h, N, d_, w_next, m.eps, c->xn.p, d_, st));
   } else {
@@ -1179,6 +1207,58 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
                           m.qkv_n(), st, 1));
     }
   }
+  return HS_OK;
+}
+
+// ---- tensor parallelism ---------------------------------------------------
+static int tp_alloc(hs_ctx* c) {
+  if (c->tp_xbuf) return HS_OK;
+  const size_t R = c->r.max_rows, d = c->m.d;
+  c->tp.xbuf_par = R * d;
+  c->tp.flag_par = R * 8;
+  CK(cudaMalloc(&c->tp_xbuf, 2 * c->tp.xbuf_par * sizeof(float)));
+  CK(cudaMalloc(&c->tp_flag, 2 * c->tp.flag_par * sizeof(unsigned)));
+  CK(cudaMemset(c->tp_flag, 0, 2 * c->tp.flag_par * sizeof(unsigned)));
+  CK(cudaDeviceSynchronize());
+  return HS_OK;
+}
+
+int hs_tp_export(hs_ctx* c, void* handles) {
+  RC(tp_alloc(c));
+  cudaIpcMemHandle_t hx, hf;
+  CK(cudaIpcGetMemHandle(&hx, c->tp_xbuf));
+  CK(cudaIpcGetMemHandle(&hf, c->tp_flag));
+  std::memcpy(handles, &hx, sizeof(hx));
+  std::memcpy(static_cast<char*>(handles) + HS_TP_HANDLE_BYTES / 2, &hf, sizeof(hf));
+  return HS_OK;
+}
+
+int hs_tp_open(hs_ctx* c, int rank, int world, const void* all_handles) {
+  if (world < 1 || world > kMaxTp || rank < 0 || rank >= world)
+    return set_error(HS_E_CONFIG, "tensor-parallel rank %d of %d out of range", rank, world);
+  RC(tp_alloc(c));
+  for (int p = 0; p < world; ++p) {
+    if (p == rank) {
+      c->tp.xbuf[p] = c->tp_xbuf;
+      c->tp.flag[p] = c->tp_flag;
+      continue;
+    }
+    const char* h = static_cast<const char*>(all_handles) + static_cast<size_t>(p) * HS_TP_HANDLE_BYTES;
+    cudaIpcMemHandle_t hx, hf;
+    std::memcpy(&hx, h, sizeof(hx));
+    std::memcpy(&hf, h + HS_TP_HANDLE_BYTES / 2, sizeof(hf));
+    void *px = nullptr, *pf = nullptr;
+    CK(cudaIpcOpenMemHandle(&px, hx, cudaIpcMemLazyEnablePeerAccess));
+    CK(cudaIpcOpenMemHandle(&pf, hf, cudaIpcMemLazyEnablePeerAccess));
+    c->tp_opened.push_back(px);
+    c->tp_opened.push_back(pf);
+    c->tp.xbuf[p] = static_cast<float*>(px);
+    c->tp.flag[p] = static_cast<unsigned*>(pf);
+  }
+  c->tp.world = world;
+  c->tp.me = rank;
+  c->tp_world = world;
+  c->tp_rank = rank;
   return HS_OK;
 }
 
@@ -1343,6 +1423,37 @@ int hs_probe_gemm_stream(hs_ctx* c, int n, int reps, float* us, double* bytes) {
   *us /= 4 * m.layers;
   *bytes = per_layer / 4;
   return err;
+}
+
+// PCIe rate of the piggyback exchange: `rows` items moved between HBM and the
+// pinned host mailboxes, median over reps (events on the step stream).
+//   dir 0: SM stores into the mapped ship mailbox (q|k|v rows, the D2H of
+//          the step's RoPE/ship launch);  dir 1: SM loads from the mapped
+//          result mailbox (the H2D gather of host attention results);
+//   dir 2 / 3: the same bytes by the copy engine (cudaMemcpyAsync D2H / H2D).
+int hs_probe_pcie(hs_ctx* c, int dir, int rows, int reps, float* us, double* bytes) {
+  const ModelCfg& m = c->m;
+  if (rows < 1 || rows > c->r.max_slots || rows > static_cast<int>(c->layer_cap))
+    return set_error(HS_E_CONFIG, "probe rows out of range");
+  const int qkv = m.qkv_n(), nqh = m.n_q * m.hd;
+  std::vector<int> ident(rows);
+  for (int i = 0; i < rows; ++i) ident[i] = i;
+  CK(cudaMemcpy(c->dm_layer, ident.data(), rows * sizeof(int), cudaMemcpyHostToDevice));
+  bf16* scratch = reinterpret_cast<bf16*>(c->part);
+  const int w = (dir == 0 || dir == 2) ? qkv : nqh;
+  *bytes = 2.0 * rows * w;
+  return time_reps(c, reps, [&]() -> int {
+    switch (dir) {
+      case 0: return gather_rows_bf16(scratch, w, c->dm_layer, rows, w, c->ship_d, w, c->st);
+      case 1: return gather_rows_bf16(c->result_d, w, c->dm_layer, rows, w, scratch, w, c->st);
+      case 2:
+        CK(cudaMemcpyAsync(c->ship_h, scratch, static_cast<size_t>(*bytes), cudaMemcpyDeviceToHost, c->st));
+        return HS_OK;
+      default:
+        CK(cudaMemcpyAsync(scratch, c->result_h, static_cast<size_t>(*bytes), cudaMemcpyHostToDevice, c->st));
+        return HS_OK;
+    }
+  }, us);
 }
 
 // The dense part of `layers` consecutive layers exactly as hs_layer issues it

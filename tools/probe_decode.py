@@ -43,6 +43,9 @@ n_q, n_kv, hd, layers = 32, 8, 128, 32
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 cases = [(8, 700), (16, 700), (24, 700), (32, 700), (16, 2000), (8, 9000), (64, 2048),
          (128, 2048)]
+TARGET = int(sys.argv[1]) if len(sys.argv) > 1 else 296  # decode_chunks target CTAs
+if len(sys.argv) > 2:
+    cases = [tuple(int(v) for v in c.split("x")) for c in sys.argv[2:]]
 for g, ctx in cases:
     npg = (ctx + 63) // 64
     pages = g * npg
@@ -50,7 +53,7 @@ for g, ctx in cases:
     pool.normal_()
     pt = torch.arange(pages, dtype=torch.int32, device=dev).reshape(g, npg)
     q = torch.randn(g, n_q * hd, device=dev).to(torch.bfloat16)
-    chunks, begin = decode_chunks([ctx] * g, n_kv)
+    chunks, begin = decode_chunks([ctx] * g, n_kv, target_ctas=TARGET)
     ch = torch.tensor([[r, r, a, b, c] for r, _, a, b, c in chunks], dtype=torch.int32,
                       device=dev)
     beg = torch.tensor(begin, dtype=torch.int32, device=dev)
@@ -71,7 +74,7 @@ for g, ctx in cases:
     us1 = ev_time(one)
     us32 = ev_time(stream32, reps=5) / layers
     by = g * ctx * 2 * n_kv * hd * 2
-    print(json.dumps({"g": g, "ctx": ctx, "ctas": len(chunks) * n_kv,
+    print(json.dumps({"target": TARGET, "g": g, "ctx": ctx, "ctas": len(chunks) * n_kv,
                       "pages_per_chunk": max(b - a for _, _, a, b, _ in chunks),
                       "us_single": round(us1, 2), "us_in_stream": round(us32, 2),
                       "frac_single": round(by / us1 / 1e3 / HBM, 3),
