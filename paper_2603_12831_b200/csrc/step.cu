@@ -1543,6 +1543,7 @@ int hs_probe_decode(hs_ctx* c, int g, int ctx_len, int reps, float* us) {
   // one wave of 296 CTAs, rows split into near-equal chunks
   int chunk = std::max(1, std::min(64, (g * per * m.n_kv + 295) / 296));
   while (chunk < 64 && m.n_kv * g * ((per + chunk - 1) / chunk) > 296) ++chunk;
+  if (g * per * m.n_kv <= 2048 && per <= 16) chunk = std::max(chunk, per);  // small: rows unsplit
   const int k = std::max(1, (per + chunk - 1) / chunk);
   std::vector<int> ch, beg{0};
   for (int r = 0; r < g; ++r) {

@@ -5,6 +5,7 @@ flushed), and 32 back-to-back launches (one per layer, different layers of
 the pool) like the step issues them.  Algorithmic bytes = sum(ctx) * 4 KiB."""
 import ctypes as C
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -13,7 +14,11 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2603_12831_b200 import _lib  # noqa: E402
+from paper_2603_12831_b200 import runtime  # noqa: E402
 from paper_2603_12831_b200.runtime import decode_chunks  # noqa: E402
+
+if os.environ.get("HS_NO_SMALL"):  # compare against chunking without the small-batch rule
+    runtime.SMALL_KV_PAGE_HEADS = 0
 
 _lib.load()
 dev = torch.device("cuda")
