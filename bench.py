@@ -586,8 +586,8 @@ def main() -> None:
     C_void_p, C_POINTER, C_byref = ctypes.c_void_p, ctypes.POINTER, ctypes.byref
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=640)
-    ap.add_argument("--warmup", type=int, default=128)
+    ap.add_argument("--steps", type=int, default=1500)
+    ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama3-8b")
     ap.add_argument("--seed", type=int, default=0)

@@ -65,6 +65,35 @@ inline uint16_t f2bf_rne(float f) {
 
 constexpr int kMaxG = 16;
 
+// acc[g][c] += sum over the tile's key pairs of P(pair) x V(pair) for GN
+// heads of chunk c (32 dims), accumulators in registers.
+template <int GN>
+HS_AVX512 inline void pv_tile(const uint16_t* V, int hd, int t0, int nt, int c,
+                              const uint32_t (*ppair)[8], float (*acc_lo)[4][16],
+                              float (*acc_hi)[4][16]) {
+  __m512 lo[GN], hi[GN];
+  for (int j = 0; j < GN; ++j) {
+    lo[j] = _mm512_load_ps(acc_lo[j][c]);
+    hi[j] = _mm512_load_ps(acc_hi[j][c]);
+  }
+  for (int k = 0; 2 * k < nt; ++k) {
+    const uint16_t* va = V + static_cast<size_t>(t0 + 2 * k) * hd + 32 * c;
+    const __m512i a = _mm512_loadu_si512(va);
+    const __m512i b = 2 * k + 1 < nt ? _mm512_loadu_si512(va + hd) : _mm512_setzero_si512();
+    const __m512bh ul = reinterpret_cast<__m512bh>(_mm512_unpacklo_epi16(a, b));
+    const __m512bh uh = reinterpret_cast<__m512bh>(_mm512_unpackhi_epi16(a, b));
+    for (int j = 0; j < GN; ++j) {
+      const __m512bh pp = reinterpret_cast<__m512bh>(_mm512_set1_epi32(static_cast<int>(ppair[j][k])));
+      lo[j] = _mm512_dpbf16_ps(lo[j], ul, pp);
+      hi[j] = _mm512_dpbf16_ps(hi[j], uh, pp);
+    }
+  }
+  for (int j = 0; j < GN; ++j) {
+    _mm512_store_ps(acc_lo[j][c], lo[j]);
+    _mm512_store_ps(acc_hi[j][c], hi[j]);
+  }
+}
+
 }  // namespace
 
 // q: [G][hd] bf16 (one GQA group), K/V: [n_keys][hd] bf16 -> out [G][hd] bf16,
@@ -126,24 +155,17 @@ HS_AVX512 void attend_group_avx512(int G, int hd, const uint16_t* q, const uint1
       const __m256bh pb = _mm512_cvtneps_pbh(p);
       _mm256_store_si256(reinterpret_cast<__m256i*>(ppair[g]), reinterpret_cast<__m256i>(pb));
     }
-    // ---- PV, two keys at a time
-    for (int k = 0; 2 * k < nt; ++k) {
-      const int ta = t0 + 2 * k;
-      const uint16_t* va = V + static_cast<size_t>(ta) * hd;
-      const uint16_t* vb = 2 * k + 1 < nt ? va + hd : nullptr;
-      for (int c = 0; c < C; ++c) {
-        const __m512i a = _mm512_loadu_si512(va + 32 * c);
-        const __m512i b = vb ? _mm512_loadu_si512(vb + 32 * c) : _mm512_setzero_si512();
-        const __m512bh lo = reinterpret_cast<__m512bh>(_mm512_unpacklo_epi16(a, b));
-        const __m512bh hi = reinterpret_cast<__m512bh>(_mm512_unpackhi_epi16(a, b));
-        for (int g = 0; g < G; ++g) {
-          const __m512bh pp = reinterpret_cast<__m512bh>(_mm512_set1_epi32(
-              static_cast<int>(ppair[g][k])));
-          _mm512_store_ps(acc_lo[g][c], _mm512_dpbf16_ps(_mm512_load_ps(acc_lo[g][c]), lo, pp));
-          _mm512_store_ps(acc_hi[g][c], _mm512_dpbf16_ps(_mm512_load_ps(acc_hi[g][c]), hi, pp));
+    // ---- PV, two keys at a time: per 32-dim chunk, up to four heads'
+    // accumulators stay in registers across the tile's key pairs
+    for (int c = 0; c < C; ++c)
+      for (int g0 = 0; g0 < G; g0 += 4) {
+        switch (G - g0 < 4 ? G - g0 : 4) {
+          case 1: pv_tile<1>(V, hd, t0, nt, c, ppair + g0, acc_lo + g0, acc_hi + g0); break;
+          case 2: pv_tile<2>(V, hd, t0, nt, c, ppair + g0, acc_lo + g0, acc_hi + g0); break;
+          case 3: pv_tile<3>(V, hd, t0, nt, c, ppair + g0, acc_lo + g0, acc_hi + g0); break;
+          default: pv_tile<4>(V, hd, t0, nt, c, ppair + g0, acc_lo + g0, acc_hi + g0); break;
         }
       }
-    }
   }
   // un-permute: acc_lo[c] lane 4L+j -> dim 32c + 8L + j, acc_hi -> +4
   for (int g = 0; g < G; ++g) {

@@ -54,9 +54,11 @@ TRANSFORMERS: dict[str, TransformerConfig] = {
     "llama3-8b": TransformerConfig("llama3-8b", 4096, 32, 32, 8, 128, 14336, 128256),
     "llama2-13b": TransformerConfig("llama2-13b", 5120, 40, 40, 40, 128, 13824, 32000,
                                     rope_theta=10000.0),
-    # per-GPU shard of Llama-3-70B under 8-way tensor parallelism
-    # (vocab shard 128256/8 padded to a multiple of 128)
-    "llama3-70b-tp8": TransformerConfig("llama3-70b-tp8", 8192, 80, 8, 1, 128, 3584, 16128,
+    # Llama-3-70B (config 4) and its per-GPU shard under 8-way tensor
+    # parallelism (tp.shard_config: 8 q heads, 1 KV head, ffn 3584 per rank;
+    # embedding and LM head replicated)
+    "llama3-70b": TransformerConfig("llama3-70b", 8192, 80, 64, 8, 128, 28672, 128256),
+    "llama3-70b-tp8": TransformerConfig("llama3-70b-tp8", 8192, 80, 8, 1, 128, 3584, 128256,
                                         tp=8),
 }
 

@@ -5,7 +5,10 @@ per layer, N iterations back to back between two events.  Compared with the
 live bench's iteration_ms_p50 it separates kernel time from host-induced
 GPU idle.
 
-    python tools/probe_step.py [B] [ctx] [M] [N]
+    python tools/probe_step.py [B] [ctx] [M] [N] [config]
+
+(config llama3-70b-tp8: one rank's shard of config 4, the exchange with the
+other ranks left out -- its per-rank compute.)
 """
 import sys
 import time
@@ -20,7 +23,7 @@ B = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 CTX = int(sys.argv[2]) if len(sys.argv) > 2 else 700
 M = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 N = int(sys.argv[4]) if len(sys.argv) > 4 else 50
-m = get_transformer("llama3-8b")
+m = get_transformer(sys.argv[5] if len(sys.argv) > 5 else "llama3-8b")
 npg = (CTX + 64) // 64
 ctx = HsContext(m, RuntimeConfig(max_rows=1024, max_slots=B + M + 8, kv_pages=(B + M) * npg + 8,
                                  max_pages_per_req=npg, max_pos=CTX + 64, max_chunks=4096,
@@ -66,9 +69,11 @@ t1 = ctx.timer()
 ctx.sync()
 w2 = time.perf_counter()
 ms = ctx.elapsed_ms(t0, t1) / N
+# every weight byte once per iteration (layers + LM head) at the measured HBM rate
+roof = (m.params_per_layer * m.n_layers + m.vocab * m.d_model) * 2 / 6549.8e9 * 1e3
 print(f"B={B} ctx={CTX} M={M}: device {ms:.3f} ms/iter; host issue {(w1 - w0) * 1e3 / N:.3f} "
-      f"ms/iter; wall {(w2 - w0) * 1e3 / N:.3f} ms/iter; weight roofline 2.45 ms "
-      f"(frac {2.45 / ms:.2f}); host us: begin {T['begin'] * 1e6 / N:.1f}, per layer "
+      f"ms/iter; wall {(w2 - w0) * 1e3 / N:.3f} ms/iter; weight roofline {roof:.2f} ms "
+      f"(frac {roof / ms:.2f}); host us: begin {T['begin'] * 1e6 / N:.1f}, per layer "
       f"{T['layer'] * 1e6 / N / m.n_layers:.1f}, end {T['end'] * 1e6 / N:.1f}", flush=True)
 # device-only: a spin kernel holds the stream while the host issues two
 # iterations (the staging ring lets the host run two ahead), so the events
