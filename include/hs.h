@@ -238,7 +238,15 @@ typedef struct {
                             token (embed + QKV(1) + ship) */
   const int* restart_idx;  /* indices into merge_slot */
   const int* restart_pos;
+  const int* merge_tag;  /* optional (NULL = unchecked): the completion tag each
+                            merged result must carry, HS_RESULT_TAG(ctx, layer)
+                            of its work item; the device verifies it before
+                            consuming the row and hs_iter_end / hs_iter_poll
+                            report a mismatch as HS_E_INTEGRITY */
 } hs_layer_desc;
+/* completion tag a CPU worker publishes (release) after writing a work
+ * item's result row: item context length and 1-based layer */
+#define HS_RESULT_TAG(ctx, layer) ((int)(((unsigned)(ctx) << 8) | (unsigned)(layer)))
 
 int hs_iter_begin(hs_ctx* ctx, const hs_iter_desc* desc);
 /* Engine._run_layer (engine.py:921-950) on the device. */

@@ -60,6 +60,7 @@ class CpuService {
 
   // mailboxes / KV resolution provided by the context
   std::function<bf16*(int slot)> ship_row, result_row, host_kv;
+  std::function<void(int slot, int ctx, int layer)> publish;
   std::function<int(int slot)> host_cap;
 
   int submit(cudaStream_t st, const int* slots, const int* layers, const int* ctxs, int n) {
@@ -145,6 +146,10 @@ class CpuService {
       std::lock_guard<std::mutex> g(mu_);
       CpuItem& ref = items_[t.item];
       if (--ref.heads_left == 0) {
+        // every head's result row is written (the mutex orders the other
+        // workers' writes before this point): publish the completion tag
+        // the device checks before merging the row
+        publish(ref.slot, ref.ctx, ref.layer);
         done_.emplace_back(ref.slot, ref.layer, wall());
         --ev_refs_[ref.ev];
         --in_flight_;
@@ -174,11 +179,13 @@ CpuService* make_cpu_service(const ModelCfg& m, int threads, const std::vector<i
 }
 void destroy_cpu_service(CpuService* s) { delete s; }
 void cpu_service_bind(CpuService* s, std::function<bf16*(int)> ship, std::function<bf16*(int)> res,
-                      std::function<bf16*(int)> kv, std::function<int(int)> cap) {
+                      std::function<bf16*(int)> kv, std::function<int(int)> cap,
+                      std::function<void(int, int, int)> publish) {
   s->ship_row = std::move(ship);
   s->result_row = std::move(res);
   s->host_kv = std::move(kv);
   s->host_cap = std::move(cap);
+  s->publish = std::move(publish);
 }
 int cpu_service_submit(CpuService* s, cudaStream_t st, const int* slots, const int* layers,
                        const int* ctxs, int n) {

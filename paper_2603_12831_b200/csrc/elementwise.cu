@@ -459,6 +459,18 @@ __global__ void __launch_bounds__(256)
   const int r = blockIdx.y;
   if (r >= rows) {  // merged rows: host attention result -> attention buffer
     const int i = r - rows;
+    if (rc.expect && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int slot = rc.idx[i];
+      unsigned tag;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(tag) : "l"(rc.tags + slot) : "memory");
+      if (tag != static_cast<unsigned>(rc.expect[i])) {
+        rc.fault[1] = slot;
+        rc.fault[2] = rc.layer;
+        rc.fault[3] = tag;
+        __threadfence_system();
+        atomicExch(rc.fault, 1u);
+      }
+    }
     const uint4* src = reinterpret_cast<const uint4*>(rc.src + static_cast<size_t>(rc.idx[i]) * rc.src_stride);
     uint4* dst = reinterpret_cast<uint4*>(rc.dst + static_cast<size_t>(i) * rc.dst_stride);
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < rc.width / 8; v += gridDim.x * blockDim.x)

@@ -213,6 +213,13 @@ struct RowCopy {
   bf16* dst = nullptr;
   int dst_stride = 0;
   int width = 0;
+  // completion check (optional): row i is consumed only after its slot's
+  // tag (written by the CPU worker after the result) equals expect[i];
+  // a mismatch is recorded in fault[0..3] = {1, slot, layer, tag seen}
+  const int* expect = nullptr;
+  const unsigned* tags = nullptr;
+  unsigned* fault = nullptr;
+  int layer = 0;
 };
 int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
                       float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io = RowIo{});

@@ -21,6 +21,7 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -118,6 +119,9 @@ struct hs_ctx {
   int* tokens_pinned = nullptr;
   // piggyback mailboxes (pinned, mapped)
   bf16 *ship_h = nullptr, *ship_d = nullptr, *result_h = nullptr, *result_d = nullptr;
+  // completion tags of the result mailbox (one per slot, written by the CPU
+  // workers) and the device fault record (hs_layer_desc.merge_tag checks)
+  unsigned *tag_h = nullptr, *tag_d = nullptr, *fault_h = nullptr, *fault_d = nullptr;
   // host KV arena (pinned, mapped)
   bf16 *hkv_h = nullptr, *hkv_d = nullptr;
   size_t hkv_bytes = 0;
@@ -500,6 +504,8 @@ void free_all(hs_ctx* c) {
   if (c->tokens_pinned) cudaFreeHost(c->tokens_pinned);
   if (c->ship_h) cudaFreeHost(c->ship_h);
   if (c->result_h) cudaFreeHost(c->result_h);
+  if (c->tag_h) cudaFreeHost(c->tag_h);
+  if (c->fault_h) cudaFreeHost(c->fault_h);
   if (c->hkv_h) cudaFreeHost(c->hkv_h);
   for (auto& e : c->stage_ev)
     if (e) cudaEventDestroy(e);
@@ -638,6 +644,13 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->result_h), res_elems * 2, cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->ship_d), c->ship_h, 0));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->result_d), c->result_h, 0));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->tag_h), r.max_slots * sizeof(unsigned),
+                   cudaHostAllocMapped));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->fault_h), 4 * sizeof(unsigned), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->tag_d), c->tag_h, 0));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->fault_d), c->fault_h, 0));
+  std::memset(c->tag_h, 0xff, r.max_slots * sizeof(unsigned));
+  std::memset(c->fault_h, 0, 4 * sizeof(unsigned));
   // host KV arena
   c->regions.assign(r.max_slots, HostRegion{});
   if (r.host_kv_bytes > 0) {
@@ -666,6 +679,25 @@ bf16* host_region(hs_ctx* c, int slot) {
   return reinterpret_cast<bf16*>(reinterpret_cast<uint8_t*>(c->hkv_h) + c->regions[slot].offset);
 }
 
+// A result row is complete: publish its tag (release: the row's bytes are
+// visible to a reader that acquires the tag, the device included).
+void publish_tag(hs_ctx* c, int slot, int ctx, int layer) {
+  reinterpret_cast<std::atomic<unsigned>*>(c->tag_h + slot)
+      ->store(static_cast<unsigned>(HS_RESULT_TAG(ctx, layer)), std::memory_order_release);
+}
+
+// Integrity faults the kernels recorded (a merged result whose completion
+// tag did not match): HS_E_INTEGRITY, the reference's IntegrityFault.
+int check_device_faults(hs_ctx* c) {
+  volatile unsigned* f = c->fault_h;
+  if (!f[0]) return HS_OK;
+  const unsigned slot = f[1], layer = f[2], seen = f[3];
+  f[0] = 0;
+  return set_error(HS_E_INTEGRITY,
+                   "piggyback result of slot %u merged at layer %u before it was complete "
+                   "(completion tag 0x%x)", slot, layer, seen);
+}
+
 int ensure_cpu_service(hs_ctx* c) {
   if (c->cpu) return HS_OK;
   if (c->r.cpu_threads <= 0) return set_error(HS_E_CONFIG, "no CPU attention threads configured");
@@ -674,7 +706,8 @@ int ensure_cpu_service(hs_ctx* c) {
   cpu_service_bind(
       c->cpu, [c, qkv](int s) { return c->ship_h + static_cast<size_t>(s) * qkv; },
       [c, nqh](int s) { return c->result_h + static_cast<size_t>(s) * nqh; },
-      [c](int s) { return host_region(c, s); }, [c](int s) { return c->regions[s].cap; });
+      [c](int s) { return host_region(c, s); }, [c](int s) { return c->regions[s].cap; },
+      [c](int s, int ctx, int layer) { publish_tag(c, s, ctx, layer); });
   return HS_OK;
 }
 
@@ -1040,7 +1073,9 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   // and, at the last layer, the LM-head gather rows and their slots; the
   // kernels read it in place from pinned host memory (a few hundred bytes)
   Packer pk(c, nullptr, 0);
-  const size_t total = 2 * static_cast<size_t>(C) + M + 2 * static_cast<size_t>(R) + 2 * NL;
+  const bool tagged = d->merge_tag != nullptr;
+  const size_t total = 2 * static_cast<size_t>(C) + M + 2 * static_cast<size_t>(R) + 2 * NL +
+                       (tagged ? M : 0);
   if (total > c->layer_cap) return set_error(HS_E_CAPACITY, "layer metadata too large");
   if (total && !pk.reserve(total)) return set_error(HS_E_CAPACITY, "metadata staging overflow");
   std::vector<int> rslot(R), lrows(NL), lslots(NL);
@@ -1057,6 +1092,7 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   const int* restart_pos = total ? pk.add(d->restart_pos, R) : nullptr;
   const int* logit_rows = total ? pk.add(lrows.data(), NL) : nullptr;
   const int* logit_slots = total ? pk.add(lslots.data(), NL) : nullptr;
+  const int* merge_tag = tagged && M ? pk.add(d->merge_tag, M) : nullptr;
   if (total) {
     HProf hp(HP_PACK);
     RC(pk.flush(st));
@@ -1084,7 +1120,8 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   } else {
     if (!(skip & 32)) RC(gemm(c, c->m_qkv[l], c->xn, B + C, m.qkv_n(), d_, &sp));
     // + merged rows: host attention results into the attention buffer
-    RowCopy rc{c->result_d, nqh, merge_slot, M, c->attn.p + static_cast<size_t>(B) * nqh, nqh, nqh};
+    RowCopy rc{c->result_d, nqh, merge_slot, M, c->attn.p + static_cast<size_t>(B) * nqh, nqh,
+               nqh, merge_tag, c->tag_d, c->fault_d, d->layer};
     if (!(skip & 1))
       RC(qkv_rope_scatter(c->part, sp, B + C, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
                           c->it_pos, c->it_slot, nullptr, B, carry_pos, carry_slot, c->qbuf, nqh,
@@ -1108,10 +1145,15 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
                        r.max_pages_per_req, reinterpret_cast<const PrefillTile*>(c->it_tiles),
                        c->n_tiles, c->attn.p, nqh, st));
   }
-  // merged rows: host attention result + stored residual
-  if (!gathered)
-    RC(gather_rows_bf16(c->result_d, nqh, merge_slot, M, nqh,
-                        c->attn.p + static_cast<size_t>(B) * nqh, nqh, st));
+  // merged rows: host attention result (+ completion check), when no RoPE
+  // launch carried it
+  if (!gathered && M > 0) {
+    RowCopy rc{c->result_d, nqh, merge_slot, M, c->attn.p + static_cast<size_t>(B) * nqh, nqh,
+               nqh, merge_tag, c->tag_d, c->fault_d, d->layer};
+    RC(qkv_rope_scatter(nullptr, 1, 0, m.n_q, m.n_kv, m.hd, nullptr, nullptr, nullptr, nullptr,
+                        nullptr, 0, nullptr, nullptr, nullptr, nqh, nullptr, c->geom, l, nullptr, 0,
+                        nullptr, m.qkv_n(), st, 1, rc));
+  }
   const int N = B + M;
   // Proj + ResidualAdd + RMSNorm (residual add fused into the GEMM when the
   // tiles have few K-segments)
@@ -1262,16 +1304,22 @@ int hs_tp_open(hs_ctx* c, int rank, int world, const void* all_handles) {
   return HS_OK;
 }
 
+// Count-returning entry points (hs_iter_end, hs_iter_poll, hs_mark,
+// hs_timer, hs_swap_done) report errors as the negated status code.
 int hs_iter_end(hs_ctx* c, int* tokens_out, int n) {
-  if (n < c->n_tok_out) return set_error(HS_E_CONFIG, "token buffer too small (%d < %d)", n,
-                                         c->n_tok_out);
-  if (c->n_tok_out > 0)
-    CK(cudaMemcpyAsync(c->tokens_pinned, c->tok_out, c->n_tok_out * sizeof(int),
-                       cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  RC(prof_collect(c));
-  if (c->n_tok_out > 0) std::memcpy(tokens_out, c->tokens_pinned, c->n_tok_out * sizeof(int));
-  return c->n_tok_out;
+  const int rc = [&]() -> int {
+    if (n < c->n_tok_out)
+      return set_error(HS_E_CONFIG, "token buffer too small (%d < %d)", n, c->n_tok_out);
+    if (c->n_tok_out > 0)
+      CK(cudaMemcpyAsync(c->tokens_pinned, c->tok_out, c->n_tok_out * sizeof(int),
+                         cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    RC(prof_collect(c));
+    RC(check_device_faults(c));
+    if (c->n_tok_out > 0) std::memcpy(tokens_out, c->tokens_pinned, c->n_tok_out * sizeof(int));
+    return HS_OK;
+  }();
+  return rc ? -rc : c->n_tok_out;
 }
 
 int hs_anchor(hs_ctx* c) {
@@ -1300,19 +1348,25 @@ int hs_iter_end_async(hs_ctx* c, int* ticket) {
 
 // 1 = done (tokens copied, *done_ms = completion time after the anchor), 0 = running
 int hs_iter_poll(hs_ctx* c, int ticket, int* tokens_out, int n, double* done_ms) {
-  if (ticket < c->next_iter - hs_ctx::kIterRing || ticket >= c->next_iter)
-    return set_error(HS_E_CONFIG, "iteration ticket %d out of window", ticket);
-  const int slot = ticket % hs_ctx::kIterRing;
-  const cudaError_t e = cudaEventQuery(c->iter_ev[slot]);
-  if (e == cudaErrorNotReady) return 0;
-  if (e != cudaSuccess) return set_error(HS_E_CUDA, "iteration: %s", cudaGetErrorString(e));
-  if (n < c->iter_n[slot]) return set_error(HS_E_CONFIG, "token buffer too small");
-  std::memcpy(tokens_out, c->tok_ring + static_cast<size_t>(slot) * 2 * c->r.max_rows,
-              c->iter_n[slot] * sizeof(int));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, c->anchor, c->iter_ev[slot]));
-  *done_ms = ms;
-  return 1;
+  int ready = 0;
+  const int rc = [&]() -> int {
+    if (ticket < c->next_iter - hs_ctx::kIterRing || ticket >= c->next_iter)
+      return set_error(HS_E_CONFIG, "iteration ticket %d out of window", ticket);
+    const int slot = ticket % hs_ctx::kIterRing;
+    const cudaError_t e = cudaEventQuery(c->iter_ev[slot]);
+    if (e == cudaErrorNotReady) return HS_OK;
+    if (e != cudaSuccess) return set_error(HS_E_CUDA, "iteration: %s", cudaGetErrorString(e));
+    if (n < c->iter_n[slot]) return set_error(HS_E_CONFIG, "token buffer too small");
+    RC(check_device_faults(c));
+    std::memcpy(tokens_out, c->tok_ring + static_cast<size_t>(slot) * 2 * c->r.max_rows,
+                c->iter_n[slot] * sizeof(int));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->anchor, c->iter_ev[slot]));
+    *done_ms = ms;
+    ready = 1;
+    return HS_OK;
+  }();
+  return rc ? -rc : ready;
 }
 
 int hs_iter_ntokens(hs_ctx* c, int ticket) {
@@ -1339,13 +1393,14 @@ int hs_cpu_attend(hs_ctx* c, const int* slots, const int* layers, const int* ctx
                     layers[i] - 1, ctxs[i], h, c->result_h + static_cast<size_t>(s) * m.n_q * m.hd,
                     nullptr);
   });
+  for (int i = 0; i < n; ++i) publish_tag(c, slots[i], ctxs[i], layers[i]);
   return HS_OK;
 }
 
 int hs_mark(hs_ctx* c) {
   const int id = c->next_mark++;
-  CK(cudaEventRecord(c->marks[id % c->marks.size()], c->st));
-  return id;
+  const cudaError_t e = cudaEventRecord(c->marks[id % c->marks.size()], c->st);
+  return e == cudaSuccess ? id : -set_error(HS_E_CUDA, "hs_mark: %s", cudaGetErrorString(e));
 }
 
 int hs_wait_mark(hs_ctx* c, int id) {
@@ -1356,8 +1411,8 @@ int hs_wait_mark(hs_ctx* c, int id) {
 
 int hs_timer(hs_ctx* c) {
   const int id = c->next_timer++;
-  CK(cudaEventRecord(c->timers[id % c->timers.size()], c->st));
-  return id;
+  const cudaError_t e = cudaEventRecord(c->timers[id % c->timers.size()], c->st);
+  return e == cudaSuccess ? id : -set_error(HS_E_CUDA, "hs_timer: %s", cudaGetErrorString(e));
 }
 
 int hs_timer_elapsed(hs_ctx* c, int a, int b, float* ms) {
@@ -1594,10 +1649,10 @@ int hs_swap_in_async(hs_ctx* c, int slot, int tokens, int* ticket) {
 
 int hs_swap_done(hs_ctx* c, int ticket) {
   auto it = c->swap_ev.find(ticket);
-  if (it == c->swap_ev.end()) return set_error(HS_E_CONFIG, "unknown swap ticket %d", ticket);
+  if (it == c->swap_ev.end()) return -set_error(HS_E_CONFIG, "unknown swap ticket %d", ticket);
   const cudaError_t e = cudaEventQuery(it->second);
   if (e == cudaErrorNotReady) return 0;
-  if (e != cudaSuccess) return set_error(HS_E_CUDA, "swap: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) return -set_error(HS_E_CUDA, "swap: %s", cudaGetErrorString(e));
   cudaEventDestroy(it->second);
   c->swap_ev.erase(it);
   return 1;

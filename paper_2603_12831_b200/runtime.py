@@ -64,7 +64,15 @@ class HsIterDesc(C.Structure):
 class HsLayerDesc(C.Structure):
     _fields_ = [("layer", C.c_int), ("n_carry", C.c_int), ("carry_slot", _IP),
                 ("carry_pos", _IP), ("n_merge", C.c_int), ("merge_slot", _IP),
-                ("n_restart", C.c_int), ("restart_idx", _IP), ("restart_pos", _IP)]
+                ("n_restart", C.c_int), ("restart_idx", _IP), ("restart_pos", _IP),
+                ("merge_tag", _IP)]
+
+
+def result_tag(ctx: int, layer: int) -> int:
+    """HS_RESULT_TAG(ctx, layer) of include/hs.h: the completion tag a CPU
+    worker publishes after writing a work item's result row."""
+    v = ((ctx << 8) | layer) & 0xFFFFFFFF
+    return v - (1 << 32) if v >= 1 << 31 else v
 
 
 W_EMBED, W_LM_HEAD, W_FINAL_NORM, W_QKV, W_O, W_GATE_UP, W_DOWN, W_NORM_IN, W_NORM_POST = range(9)
@@ -239,11 +247,13 @@ class HsContext:
                        len(ti) // 4, _ip(ti), len(lr), _ip(lr))
         self._call("hs_iter_begin", C.byref(d))
 
-    def layer(self, layer: int, carry_slot, carry_pos, merge_slot, restart_idx, restart_pos):
+    def layer(self, layer: int, carry_slot, carry_pos, merge_slot, restart_idx, restart_pos,
+              merge_tag=None):
         cs, cp, ms, ri, rp = (_i32(carry_slot), _i32(carry_pos), _i32(merge_slot),
                               _i32(restart_idx), _i32(restart_pos))
+        mt = _i32(merge_tag) if merge_tag is not None else None
         d = HsLayerDesc(layer, len(cs), _ip(cs), _ip(cp), len(ms), _ip(ms), len(ri), _ip(ri),
-                        _ip(rp))
+                        _ip(rp), _ip(mt) if mt is not None else None)
         self._call("hs_layer", C.byref(d))
 
     def iter_end(self) -> np.ndarray:
@@ -414,6 +424,7 @@ class CudaStep(LayerStep):
         self.last_tokens: Optional[np.ndarray] = None
         self.iterations = 0
         self._pending_release: list[str] = []
+        self._tags: dict[str, int] = {}  # completion tag of each request's outstanding result
         # host<->device bytes moved by the step (metadata, tokens, piggyback rows)
         self.h2d_bytes = 0
         self.d2h_bytes = 0
@@ -506,6 +517,7 @@ class CudaStep(LayerStep):
         eng = self.engine
         carry = list(self._carry)
         merge_slots, merge_ids, restart_idx, restart_pos, next_carry = [], [], [], [], []
+        merge_tags = []
         for item, outcome in merges:
             r = eng.requests[item.req_id]
             s = self.slot_of(item.req_id)
@@ -519,8 +531,10 @@ class CudaStep(LayerStep):
                 restart_pos.append(r.ctx)
             merge_slots.append(s)
             merge_ids.append(item.req_id)
+            merge_tags.append(self._tags.pop(item.req_id))
+        # the device checks every merged row's completion tag before use
         self.ctx.layer(layer, [c[0] for c in carry], [c[1] for c in carry], merge_slots,
-                       restart_idx, restart_pos)
+                       restart_idx, restart_pos, merge_tags)
         shipped = [c[2] for c in carry] + [merge_ids[i] for i in restart_idx]
         m = self.model
         self.h2d_bytes += 4 * (4 * len(carry) + len(merge_slots) + 4 * len(restart_idx))
@@ -546,7 +560,8 @@ class CudaStep(LayerStep):
         self.iterations += 1
 
     def cpu_service(self, host_id: int, items) -> None:
-        eng = self.engine
+        for it in items:
+            self._tags[it.req_id] = result_tag(it.ctx_tokens, it.layer)
         self.ctx.cpu_attend([self.slot_of(it.req_id) for it in items], [it.layer for it in items],
                             [it.ctx_tokens for it in items])
 
@@ -577,6 +592,7 @@ class CudaStep(LayerStep):
 
     def _release_pending(self) -> None:
         for rid in self._pending_release:
+            self._tags.pop(rid, None)
             s = self.slots.pop(rid, None)
             if s is None:
                 continue
@@ -654,6 +670,8 @@ class LiveCudaStep(CudaStep):
         return out
 
     def cpu_submit(self, items) -> None:
+        for it in items:
+            self._tags[it.req_id] = result_tag(it.ctx_tokens, it.layer)
         self.ctx.cpu_submit([self.slot_of(it.req_id) for it in items],
                             [it.layer for it in items], [it.ctx_tokens for it in items])
 
