@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+HS_SKIP=511 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:"gemm|argmax|embed|select|scatter|gather|norm|rope" -s 20 -c 60 --csv --log-file gpurun_out/lm.csv python tools/probe_step.py 8 700 0 4 > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/lm.csv
+HS_SKIP=511 timeout 120 python tools/probe_step.py 8 700 0 30 2>&1 | grep device-only
+HS_SKIP=511 timeout 120 python tools/probe_step.py 32 700 0 30 2>&1 | grep device-only
