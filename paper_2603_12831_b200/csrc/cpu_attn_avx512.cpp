@@ -1,21 +1,29 @@
 // C1 fast path: BE decode attention on AVX-512-BF16 host cores.
 //
-// QK^T: vdpbf16ps on the bf16 q and K rows (32 MACs per instruction); the
-// per-key partial vectors of a 16-key tile are transpose-reduced into one
-// 16-lane score vector.  PV: two keys at a time, their V rows interleaved
+// QK^T: on AMX-BF16 tiles where the CPU and kernel allow it (K rows loaded
+// as tile rows straight from the host KV, Q^T packed once), else vdpbf16ps
+// on the bf16 q and K rows (32 MACs per instruction) with the per-key
+// partial vectors of a 16-key tile transpose-reduced into one 16-lane score
+// vector.  PV: two keys at a time, their V rows interleaved
 // (unpacklo/hi_epi16) into bf16 pairs and multiplied by the pair of softmax
 // weights with vdpbf16ps — the same bf16 rounding of P the GPU kernel uses.
 // Online softmax across tiles with a vectorised exp2.  Layout: one request's
 // K (or V) for one layer and KV head is contiguous [keys][hd] (host KV arena,
 // DESIGN.md §4).
 #include <immintrin.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "hs_step.h"
 
 #define HS_AVX512 __attribute__((target("avx512f,avx512bw,avx512vl,avx512dq,avx512bf16")))
+#define HS_AMX \
+  __attribute__((target("avx512f,avx512bw,avx512vl,avx512dq,avx512bf16,amx-tile,amx-bf16")))
 
 namespace hs {
 
@@ -96,9 +104,74 @@ HS_AVX512 inline void pv_tile(const uint16_t* V, int hd, int t0, int nt, int c,
 
 }  // namespace
 
+// ---- AMX for QK^T: S^T[16 keys][G] = K[16 keys][hd] . Q^T, the K rows
+// loaded as tile rows straight from the host KV (no repacking), Q^T packed
+// once per call in the VNNI pair layout.  tmm0 = K chunk (16 x 32 bf16),
+// tmm2 = scores (16 x G fp32), tmm4..7 = Q^T chunks (16 pairs x G).
+// AMX needs the process's permission for the tile state (Linux
+// ARCH_REQ_XCOMP_PERM); without it, or on CPUs without AMX-BF16, QK^T stays
+// on vdpbf16ps (HS_CPU_AMX=0 forces that too).
+bool amx_ready() {
+  static const bool ok = [] {
+    const char* e = getenv("HS_CPU_AMX");
+    if (e && e[0] == '0') return false;
+    unsigned a, b, c, d;
+    __asm__ __volatile__("cpuid" : "=a"(a), "=b"(b), "=c"(c), "=d"(d) : "a"(7), "c"(0));
+    const bool has = ((d >> 22) & 1) && ((d >> 24) & 1);  // AMX-BF16, AMX-TILE
+    if (!has) return false;
+    constexpr long kArchReqXcompPerm = 0x1023, kXfeatureXtiledata = 18;
+    return syscall(SYS_arch_prctl, kArchReqXcompPerm, kXfeatureXtiledata) == 0;
+  }();
+  return ok;
+}
+
+struct alignas(64) TileCfg {
+  uint8_t palette, start_row, reserved[14];
+  uint16_t colsb[16];
+  uint8_t rows[16];
+};
+
+HS_AMX inline void amx_config(int G) {
+  thread_local int configured_g = -1;
+  if (configured_g == G) return;
+  TileCfg cfg{};
+  cfg.palette = 1;
+  cfg.rows[0] = 16;
+  cfg.colsb[0] = 64;  // K chunk: 16 keys x 32 bf16
+  cfg.rows[2] = 16;
+  cfg.colsb[2] = static_cast<uint16_t>(4 * G);  // scores: 16 keys x G fp32
+  for (int t = 4; t < 8; ++t) {
+    cfg.rows[t] = 16;  // 32 dims as 16 bf16 pairs
+    cfg.colsb[t] = static_cast<uint16_t>(4 * G);
+  }
+  _tile_loadconfig(&cfg);
+  configured_g = G;
+}
+
+// scores[16][G] (fp32) of keys [t0, t0 + 16) over the C = hd/32 chunks;
+// keys past n_keys come from the zero-padded `tail` copy.
+HS_AMX inline void amx_scores(const uint16_t* K, int hd, int C, int t0, int nt, const uint16_t* tail,
+                              float* scores, int G) {
+  const uint16_t* base = nt == 16 ? K + static_cast<size_t>(t0) * hd : tail;
+  _tile_zero(2);
+  _tile_loadd(0, base, hd * 2);
+  _tile_dpbf16ps(2, 0, 4);
+  if (C > 1) {
+    _tile_loadd(0, base + 32, hd * 2);
+    _tile_dpbf16ps(2, 0, 5);
+  }
+  if (C > 2) {
+    _tile_loadd(0, base + 64, hd * 2);
+    _tile_dpbf16ps(2, 0, 6);
+    _tile_loadd(0, base + 96, hd * 2);
+    _tile_dpbf16ps(2, 0, 7);
+  }
+  _tile_stored(2, scores, 4 * G);
+}
+
 // q: [G][hd] bf16 (one GQA group), K/V: [n_keys][hd] bf16 -> out [G][hd] bf16,
 // lse [G] (natural log, optional).  hd in {64, 128}.
-HS_AVX512 void attend_group_avx512(int G, int hd, const uint16_t* q, const uint16_t* K,
+HS_AMX void attend_group_avx512(int G, int hd, const uint16_t* q, const uint16_t* K,
                                    const uint16_t* V, int n_keys, uint16_t* out, float* lse) {
   const int C = hd / 32;  // 32-bf16 chunks per row
   const float scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(hd));
@@ -115,28 +188,82 @@ HS_AVX512 void attend_group_avx512(int G, int hd, const uint16_t* q, const uint1
     den[g] = 0.f;
   }
   __m512 part[kMaxG][16];
+  __m512 raw[kMaxG];
   alignas(64) uint32_t ppair[kMaxG][8];
+  // AMX: Q^T chunks in the VNNI pair layout, loaded once into tmm4..7
+  const bool amx = amx_ready();
+  alignas(64) uint16_t qv[4][16][32];
+  alignas(64) uint16_t tail[16 * 128];
+  alignas(64) float sc[16 * kMaxG];
+  if (amx) {
+    amx_config(G);
+    std::memset(qv, 0, sizeof(qv));
+    for (int c = 0; c < C; ++c)
+      for (int r = 0; r < 16; ++r)
+        for (int g = 0; g < G; ++g) {
+          qv[c][r][2 * g] = q[g * hd + 32 * c + 2 * r];
+          qv[c][r][2 * g + 1] = q[g * hd + 32 * c + 2 * r + 1];
+        }
+    _tile_loadd(4, qv[0], 64);
+    _tile_loadd(5, qv[1], 64);
+    _tile_loadd(6, qv[2], 64);
+    _tile_loadd(7, qv[3], 64);
+  }
+  const __m512i lane = _mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15);
+  // software prefetch of the K/V rows pf_tiles 16-key tiles ahead: one
+  // host core's hardware prefetchers alone leave DRAM latency exposed
+  // (B200 box, 14 workers, 32 x 9000 ctx: 103 GB/s without, 129 GB/s with
+  // 2 tiles + AMX QK^T; HS_CPU_PF tunes it, 0 = off)
+  static const int pf_tiles = [] {
+    const char* e = getenv("HS_CPU_PF");
+    return e ? atoi(e) : 2;
+  }();
+  const size_t row_bytes = static_cast<size_t>(hd) * 2;
   for (int t0 = 0; t0 < n_keys; t0 += 16) {
     const int nt = n_keys - t0 < 16 ? n_keys - t0 : 16;
-    // ---- scores of 16 keys for every head of the group
-    for (int t = 0; t < 16; ++t) {
-      if (t < nt) {
-        const uint16_t* kr = K + static_cast<size_t>(t0 + t) * hd;
-        __m512bh kc[4];
-        for (int c = 0; c < C; ++c)
-          kc[c] = reinterpret_cast<__m512bh>(_mm512_loadu_si512(kr + 32 * c));
-        for (int g = 0; g < G; ++g) {
-          __m512 a = _mm512_dpbf16_ps(_mm512_setzero_ps(), qb[g][0], kc[0]);
-          for (int c = 1; c < C; ++c) a = _mm512_dpbf16_ps(a, qb[g][c], kc[c]);
-          part[g][t] = a;
+    if (pf_tiles > 0) {
+      const int tp = t0 + 16 * pf_tiles;
+      if (tp < n_keys) {
+        const int np = n_keys - tp < 16 ? n_keys - tp : 16;
+        const char* kp = reinterpret_cast<const char*>(K + static_cast<size_t>(tp) * hd);
+        const char* vp = reinterpret_cast<const char*>(V + static_cast<size_t>(tp) * hd);
+        for (size_t off = 0; off < np * row_bytes; off += 64) {
+          _mm_prefetch(kp + off, _MM_HINT_T0);
+          _mm_prefetch(vp + off, _MM_HINT_T0);
         }
-      } else {
-        for (int g = 0; g < G; ++g) part[g][t] = _mm512_setzero_ps();
       }
+    }
+    // ---- scores of 16 keys for every head of the group
+    if (amx) {
+      if (nt < 16) {
+        std::memset(tail, 0, sizeof(tail));
+        std::memcpy(tail, K + static_cast<size_t>(t0) * hd, static_cast<size_t>(nt) * hd * 2);
+      }
+      amx_scores(K, hd, C, t0, nt, tail, sc, G);
+      const __m512i idx = _mm512_mullo_epi32(lane, _mm512_set1_epi32(G));
+      for (int g = 0; g < G; ++g)
+        raw[g] = _mm512_i32gather_ps(_mm512_add_epi32(idx, _mm512_set1_epi32(g)), sc, 4);
+    } else {
+      for (int t = 0; t < 16; ++t) {
+        if (t < nt) {
+          const uint16_t* kr = K + static_cast<size_t>(t0 + t) * hd;
+          __m512bh kc[4];
+          for (int c = 0; c < C; ++c)
+            kc[c] = reinterpret_cast<__m512bh>(_mm512_loadu_si512(kr + 32 * c));
+          for (int g = 0; g < G; ++g) {
+            __m512 a = _mm512_dpbf16_ps(_mm512_setzero_ps(), qb[g][0], kc[0]);
+            for (int c = 1; c < C; ++c) a = _mm512_dpbf16_ps(a, qb[g][c], kc[c]);
+            part[g][t] = a;
+          }
+        } else {
+          for (int g = 0; g < G; ++g) part[g][t] = _mm512_setzero_ps();
+        }
+      }
+      for (int g = 0; g < G; ++g) raw[g] = transpose_reduce16(part[g]);
     }
     const __mmask16 valid = static_cast<__mmask16>((1u << nt) - 1u);
     for (int g = 0; g < G; ++g) {
-      __m512 s = _mm512_mul_ps(transpose_reduce16(part[g]), _mm512_set1_ps(scale_log2));
+      __m512 s = _mm512_mul_ps(raw[g], _mm512_set1_ps(scale_log2));
       s = _mm512_mask_blend_ps(valid, _mm512_set1_ps(-INFINITY), s);
       const float tmax = _mm512_reduce_max_ps(s);
       const float nm = m[g] > tmax ? m[g] : tmax;
