@@ -47,3 +47,31 @@ def test_host_attention_matches_oracle(impl, n_q, n_kv, hd, keys):
     err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-6)
     assert err < 1.5e-2, err
     assert np.abs(lse - ref_lse).max() < 1e-2
+
+
+def test_host_attention_without_amx_matches_oracle():
+    """The vdpbf16ps QK^T path (hosts without AMX, or HS_CPU_AMX=0) in a fresh
+    process, since the AMX choice is made once per process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    if not _has_avx512bf16():
+        pytest.skip("no AVX-512-BF16 on this host")
+    root = Path(__file__).resolve().parent.parent
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
+        "from test_cpu_attention import _run\n"
+        "from oracle import llama_ops as O\n"
+        "rng = np.random.default_rng(3)\n"
+        "q = O.to_bf16(rng.standard_normal((32, 128)).astype(np.float32))\n"
+        "k = O.to_bf16(rng.standard_normal((8, 301, 128)).astype(np.float32))\n"
+        "v = O.to_bf16(rng.standard_normal((8, 301, 128)).astype(np.float32))\n"
+        "got, _ = _run(q, k, v, 32, 8, 128, 1)\n"
+        "ref, _ = O.decode_attention(q, k.transpose(1, 0, 2), v.transpose(1, 0, 2), 8)\n"
+        "print(float(np.abs(got - ref).max() / np.abs(ref).max()))\n")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**os.environ, "HS_CPU_AMX": "0"}, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert float(out.stdout.strip().splitlines()[-1]) < 1.5e-2
