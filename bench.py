@@ -124,14 +124,14 @@ def scenario_doc(args, cores: int, ls_rate: float = None) -> dict:
     }
 
 
-def prepopulate_be(engine, step, n: int, seed: int, start: int = 0) -> list:
+def prepopulate_be(engine, step, n: int, seed: int, start: int = 0, fixed=None) -> list:
     """Saturating BE decode backlog already offloaded to host DRAM: each
     request has finished prefill (token 1 emitted) and its chain is injected
     (the state _finish_swap_out leaves, reference engine.py:437-454)."""
     from paper_2603_12831_b200.state import SimRequest
     from paper_2603_12831_b200.workload import RequestSpec, ServiceClass, longbench_like
 
-    pairs = longbench_like(seed=1).pairs
+    pairs = [fixed] if fixed else longbench_like(seed=1).pairs
     out = []
     for i in range(start, start + n):
         p, o = pairs[(seed * 7919 + i) % len(pairs)]
@@ -161,16 +161,17 @@ class BeBacklog:
     """Keeps `n` BE requests live: every completed one is replaced by a new
     host-resident request (a stationary saturating backlog)."""
 
-    def __init__(self, engine, step, n: int, seed: int):
-        self.engine, self.step, self.n, self.seed = engine, step, n, seed
+    def __init__(self, engine, step, n: int, seed: int, fixed=None):
+        self.engine, self.step, self.n, self.seed, self.fixed = engine, step, n, seed, fixed
         self.next_id = n
-        self.live = prepopulate_be(engine, step, n, seed)
+        self.live = prepopulate_be(engine, step, n, seed, fixed=fixed)
 
     def __call__(self, _it: int) -> None:
         alive = [r for r in self.live if r.phase != "done"]
         short = self.n - len(alive)
         if short > 0:
-            alive += prepopulate_be(self.engine, self.step, short, self.seed, self.next_id)
+            alive += prepopulate_be(self.engine, self.step, short, self.seed, self.next_id,
+                                    fixed=self.fixed)
             self.next_id += short
             self.engine._dirty = True
         self.live = alive
@@ -351,10 +352,14 @@ def run_ours(args) -> None:
         doc = scenario_doc(args, cores)
         doc["seed"] = doc["workload"]["seed"] = replicas.replica_seed(args.seed, rank)
     scenario = scenario_from_dict(doc, "bench")
-    be_cap_tokens = 13000 + 400
+    # config 5 (--workload longctx): every BE request a 32768-token prompt with
+    # 136 output tokens, KV in host DRAM (4.3 GB each for Llama-3-8B)
+    be_fixed = (32768, 136) if args.workload == "longctx" else None
+    be_cap_tokens = (be_fixed[0] + be_fixed[1] + 64) if be_fixed else 13000 + 400
     rt = RuntimeConfig(max_rows=args.max_rows, max_slots=512,
                        kv_pages=args.gpu_kv_tokens // 64 + 512 + 64, max_pages_per_req=256,
-                       max_pos=16384, max_chunks=8192, cpu_threads=len(workers),
+                       max_pos=max(16384, be_cap_tokens + 64), max_chunks=8192,
+                       cpu_threads=len(workers),
                        host_kv_bytes=(args.be_chains + 4) * be_cap_tokens
                        * model.kv_bytes_per_token_layer * model.n_layers, device=local,
                        cpu_list=tuple(workers) if args.pin else ())
@@ -373,7 +378,7 @@ def run_ours(args) -> None:
         models = profiler.load(models_path)
     engine = LiveEngine(scenario, models=models, step=step, pace_layers=args.pace,
                         pace_tail=args.pace_tail)
-    backlog = BeBacklog(engine, step, args.be_chains, args.seed + rank)
+    backlog = BeBacklog(engine, step, args.be_chains, args.seed + rank, fixed=be_fixed)
     if args.ls_decodes:
         prepopulate_ls(engine, step, args.ls_decodes, args.seed + rank)
     from paper_2603_12831_b200.workload import build_requests
@@ -519,9 +524,11 @@ def run_ours(args) -> None:
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights, synthetic KV, Poisson LS trace)",
-        "config": {"workload": "llama3-8b live serving: Poisson LS (sharegpt, TPOT SLO 50 ms) + "
-                               f"{args.be_chains} host-resident BE decodes kept live (longbench; "
-                               "completed ones replaced by new prefilled requests)",
+        "config": {"workload": ("llama3-8b live serving: Poisson LS (sharegpt, TPOT SLO 50 ms) + "
+                                f"{args.be_chains} host-resident BE decodes kept live ("
+                                + ("32768-token prompts, 136 outputs; config 5" if be_fixed
+                                   else "longbench") +
+                                "; completed ones replaced by new prefilled requests)"),
                    "model": args.config, "ls_rate_per_s": args.ls_rate,
                    "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
                    "cpu_threads_per_replica": rt.cpu_threads, "parallelism": f"replicas x{world}",
@@ -590,9 +597,12 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama3-8b")
+    ap.add_argument("--workload", default="saturating", choices=["saturating", "longctx"],
+                    help="BE backlog: longbench-like (config 2) or 32k-token prompts (config 5)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ls-rate", type=float, default=8.0)
-    ap.add_argument("--be-chains", type=int, default=32)
+    ap.add_argument("--be-chains", type=int, default=None,
+                    help="host-resident BE requests kept live (default 32; 8 for --workload longctx)")
     ap.add_argument("--ls-decodes", type=int, default=0)
     ap.add_argument("--gpu-kv-tokens", type=int, default=24576)
     ap.add_argument("--max-piggyback", type=int, default=64)
@@ -612,6 +622,8 @@ def main() -> None:
     ap.add_argument("--ref-ls-rows", type=int, default=8)
     ap.add_argument("--ref-merge-rows", type=int, default=16)
     args = ap.parse_args()
+    if args.be_chains is None:
+        args.be_chains = 8 if args.workload == "longctx" else 32
     if args.impl == "reference":
         # each CPU step is a seconds-long bounded sample: cap the count so the
         # arm finishes within minutes (the line reports the steps actually run)
