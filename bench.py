@@ -356,6 +356,15 @@ def run_ours(args) -> None:
     # 136 output tokens, KV in host DRAM (4.3 GB each for Llama-3-8B)
     be_fixed = (32768, 136) if args.workload == "longctx" else None
     be_cap_tokens = (be_fixed[0] + be_fixed[1] + 64) if be_fixed else 13000 + 400
+    # the pinned host KV arena of all replicas on this node must fit in RAM:
+    # at most half of the available memory, split among the local replicas
+    per_req = be_cap_tokens * model.kv_bytes_per_token_layer * model.n_layers
+    fit = int(0.5 * replicas.mem_available_bytes() / max(local_world, 1) // per_req) - 4
+    if fit < args.be_chains:
+        if rank == 0:
+            print(f"bench: host RAM holds {max(fit, 1)} BE requests per replica "
+                  f"(asked {args.be_chains})", file=sys.stderr)
+        args.be_chains = max(fit, 1)
     rt = RuntimeConfig(max_rows=args.max_rows, max_slots=512,
                        kv_pages=args.gpu_kv_tokens // 64 + 512 + 64, max_pages_per_req=256,
                        max_pos=max(16384, be_cap_tokens + 64), max_chunks=8192,

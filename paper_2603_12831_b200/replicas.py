@@ -168,3 +168,14 @@ def aggregate(sums: Sequence[float], maxes: Sequence[float], dist=None
     dist.all_reduce(ts, op=dist.ReduceOp.SUM)
     dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     return ts.numpy(), tm.numpy()
+
+
+def mem_available_bytes() -> int:
+    """MemAvailable of this host (/proc/meminfo); a large value if unknown."""
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 1 << 50
