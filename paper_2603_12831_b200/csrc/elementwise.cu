@@ -191,7 +191,7 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   __shared__ float red[32];
-  __shared__ float ssq_cta;
+  __shared__ float ssq_all[kNormCluster];
   cg::cluster_group cluster = cg::this_cluster();
   const int r = blockIdx.y;
   const int rank = static_cast<int>(cluster.block_rank());
@@ -219,12 +219,14 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
   }
   if (!out) return;
   ss = block_sum(ss, red);
-  if (threadIdx.x == 0) ssq_cta = ss;
+  // push this CTA's partial into every rank's slot table, one cluster
+  // barrier, then each rank sums the table in rank order (no remote reads
+  // after the barrier, so no second barrier to keep shared memory alive)
+  if (threadIdx.x < kNormCluster) *cluster.map_shared_rank(&ssq_all[rank], threadIdx.x) = ss;
   cluster.sync();
   float total = 0.f;
 #pragma unroll
-  for (int k = 0; k < kNormCluster; ++k) total += *cluster.map_shared_rank(&ssq_cta, k);
-  cluster.sync();  // keep every CTA's smem alive until all ranks have read it
+  for (int k = 0; k < kNormCluster; ++k) total += ssq_all[k];
   const float inv = rsqrtf(total / d + eps);
   bf16* o = out + static_cast<size_t>(r) * ld_out + c0;
   const float* wp = w + c0;
