@@ -185,7 +185,7 @@ int splitk_reduce(const float* part, int splits, int rows, int n, float* out, cu
 constexpr int kNormCluster = 8;
 
 __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
-    residual_add_norm_kernel(const float* __restrict__ part, int splits, int rows, int d,
+    residual_add_norm_kernel(const float* __restrict__ part, Planes splits, int rows, int d,
                              float* __restrict__ h, const float* __restrict__ w, float eps,
                              bf16* __restrict__ out, int ld_out, RowIo io) {
   pdl_wait();  // dependent data of the previous kernel is visible
@@ -200,14 +200,14 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
   float* x = h + static_cast<size_t>(r) * d + c0;
   const float* xin = io.row_src(h, r, d) + c0;
   float* put = io.row_put(r, d);
-  const bool write = splits > 0 || xin != x;
+  const bool write = splits.n > 0 || xin != x;
   const size_t plane = static_cast<size_t>(rows) * d;
   const float* pp = part + static_cast<size_t>(r) * d + c0;
   float ss = 0.f;
   for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4) {
     float4 v = *reinterpret_cast<const float4*>(xin + i);
-    if (splits > 0) {
-      const float4 a = sum_planes4_all(pp + i, plane, splits);
+    if (splits.n > 0) {
+      const float4 a = sum_planes4_all(pp + i, plane, splits.count(r, c0 + i));
       v.x += a.x;
       v.y += a.y;
       v.z += a.z;
@@ -254,7 +254,7 @@ __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
 }
 
 __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
-    tp_add_norm_kernel(const float* __restrict__ part, int splits, int rows, int d,
+    tp_add_norm_kernel(const float* __restrict__ part, Planes splits, int rows, int d,
                        float* __restrict__ h, const float* __restrict__ w, float eps,
                        bf16* __restrict__ out, int ld_out, RowIo io, TpPeers peers,
                        unsigned epoch) {
@@ -276,7 +276,7 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
     // 1. publish this rank's partial of these columns
     float* mine = peers.xbuf[peers.me] + xoff;
     for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4)
-      *reinterpret_cast<float4*>(mine + i) = sum_planes4_all(pp + i, plane, splits);
+      *reinterpret_cast<float4*>(mine + i) = sum_planes4_all(pp + i, plane, splits.count(r, c0 + i));
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence_system();
@@ -330,11 +330,11 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
   pdl_trigger();
 }
 
-int tp_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
+int tp_add_norm(const float* part, const Planes& splits, int rows, int d, float* h, const float* w,
                 float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io,
                 const TpPeers& peers, unsigned epoch) {
   if (rows <= 0) return HS_OK;
-  if (d % (4 * kNormCluster) || splits > kMaxSplits || splits < 1 || peers.world < 1 ||
+  if (d % (4 * kNormCluster) || splits.n > kMaxSplits || splits.n < 1 || peers.world < 1 ||
       peers.world > kMaxTp)
     return HS_E_CONFIG;
   constexpr int kTpRowCtas = 32;  // clusters per rank (rows are looped over)
@@ -349,7 +349,7 @@ int tp_add_norm(const float* part, int splits, int rows, int d, float* h, const 
 constexpr int kRowVec = 8;
 
 __global__ void __launch_bounds__(256)
-    residual_add_norm_rows_kernel(const float* __restrict__ part, int splits, int rows, int d,
+    residual_add_norm_rows_kernel(const float* __restrict__ part, Planes splits, int rows, int d,
                                   float* __restrict__ h, const float* __restrict__ w, float eps,
                                   bf16* __restrict__ out, int ld_out, RowIo io) {
   pdl_wait();
@@ -359,26 +359,29 @@ __global__ void __launch_bounds__(256)
   float* x = h + static_cast<size_t>(r) * d;
   const float* xin = io.row_src(h, r, d);
   float* put = io.row_put(r, d);
-  const bool write = splits > 0 || xin != x;
+  const bool write = splits.n > 0 || xin != x;
   const size_t plane = static_cast<size_t>(rows) * d;
   const float* pp = part + static_cast<size_t>(r) * d;
   // planes outer, the row's vectors inner: kRowVec loads in flight per plane
   float4 v[kRowVec];
+  int cnt[kRowVec];
 #pragma unroll
-  for (int k = 0; k < kRowVec; ++k) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int s = 0; s < splits; ++s) {
+  for (int k = 0; k < kRowVec; ++k) {
+    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int i = (threadIdx.x + k * 256) * 4;
+    cnt[k] = i < d ? splits.count(r, i) : 0;
+  }
+  for (int s = 0; s < splits.n; ++s) {
     const float* ps = pp + s * plane;
     float4 t[kRowVec];
 #pragma unroll
     for (int k = 0; k < kRowVec; ++k) {
       const int i = (threadIdx.x + k * 256) * 4;
-      if (i < d) t[k] = ld4(ps + i);
+      if (s < cnt[k]) t[k] = ld4(ps + i);
     }
 #pragma unroll
-    for (int k = 0; k < kRowVec; ++k) {
-      const int i = (threadIdx.x + k * 256) * 4;
-      if (i < d) add4(v[k], t[k]);
-    }
+    for (int k = 0; k < kRowVec; ++k)
+      if (s < cnt[k]) add4(v[k], t[k]);
   }
   // h += sum of the planes (the same association as the cluster form)
 #pragma unroll
@@ -420,10 +423,11 @@ __global__ void __launch_bounds__(256)
 // thread, every plane in flight) beats a CTA per row
 constexpr int kClusterRowsMax = 64;
 
-int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
-                      float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io) {
+int residual_add_norm(const float* part, const Planes& splits, int rows, int d, float* h,
+                      const float* w, float eps, bf16* out, int ld_out, cudaStream_t st,
+                      const RowIo& io) {
   if (rows <= 0) return HS_OK;
-  if (d % (4 * kNormCluster) || splits > kMaxSplits) return HS_E_CONFIG;
+  if (d % (4 * kNormCluster) || splits.n > kMaxSplits) return HS_E_CONFIG;
   if (rows > kClusterRowsMax && d <= 4 * 256 * kRowVec)
     return launch_pdl(residual_add_norm_rows_kernel, dim3(rows), dim3(256), 0, st, part, splits,
                       rows, d, h, w, eps, out, ld_out, io);
@@ -447,7 +451,7 @@ int residual_add_norm(const float* part, int splits, int rows, int d, float* h, 
 // two float2 loads per split plane, bf16x2 stores of both halves.  q and k
 // heads are rotated, v heads copied.
 __global__ void __launch_bounds__(256)
-    qkv_rope_scatter_kernel(const float* __restrict__ part, int splits, int rows, int n_q,
+    qkv_rope_scatter_kernel(const float* __restrict__ part, Planes splits, int rows, int n_q,
                             int n_kv, int hd, const float* __restrict__ rope_cos,
                             const float* __restrict__ rope_sin, const int* __restrict__ row_pos,
                             const int* __restrict__ row_slot, const int* __restrict__ row_mode,
@@ -496,12 +500,13 @@ __global__ void __launch_bounds__(256)
   const int slot = batch ? row_slot[r] : carry_slot[r - n_batch];
   const int mode = batch ? (row_mode ? row_mode[r] : 0) : 1;
   float a1, a2, b1, b2;  // (x1, x2) of pairs j and j+1
+  const int np = splits.count(r, base);
   if (permuted) {  // feature i of the head in row 2i, feature i + hd/2 in row 2i+1
-    const float4 v = sum_planes4_all(src + 2 * j, plane, splits);
+    const float4 v = sum_planes4_all(src + 2 * j, plane, np);
     a1 = v.x, a2 = v.y, b1 = v.z, b2 = v.w;
   } else {
-    const float2 lo = sum_planes2(src + j, plane, splits);
-    const float2 hi = sum_planes2(src + half + j, plane, splits);
+    const float2 lo = sum_planes2(src + j, plane, np);
+    const float2 hi = sum_planes2(src + half + j, plane, np);
     a1 = lo.x, b1 = lo.y, a2 = hi.x, b2 = hi.y;
   }
   float y1a = a1, y2a = a2, y1b = b1, y2b = b2;
@@ -528,14 +533,15 @@ __global__ void __launch_bounds__(256)
   *reinterpret_cast<uint32_t*>(dst + half + j) = pack_bf16x2(y2a, y2b);
 }
 
-int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv, int head_dim,
+int qkv_rope_scatter(const float* part, const Planes& splits, int rows, int n_q, int n_kv,
+                     int head_dim,
                      const float* rope_cos, const float* rope_sin, const int* row_pos,
                      const int* row_slot, const int* row_mode, int n_batch, const int* carry_pos,
                      const int* carry_slot, bf16* qbuf, int q_row_stride, bf16* kv_pool,
                      const KvGeom& g, int layer, const int* page_table, int pt_stride, bf16* ship,
                      int ship_stride, cudaStream_t st, int permuted, const RowCopy& rc) {
   if (rows + rc.n <= 0) return HS_OK;
-  if (splits > kMaxSplits || head_dim % 8 || q_row_stride % 2 || ship_stride % 2 ||
+  if (splits.n > kMaxSplits || head_dim % 8 || q_row_stride % 2 || ship_stride % 2 ||
       (rc.n && (rc.width % 8 || rc.src_stride % 8 || rc.dst_stride % 8)))
     return HS_E_CONFIG;
   const int threads = (n_q + 2 * n_kv) * head_dim / 4;
@@ -550,7 +556,7 @@ int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv,
 // grid (feature blocks, rows); each thread 4 consecutive features: float4
 // loads of gate and up from every split plane, one 8-byte bf16 store.
 __global__ void __launch_bounds__(256)
-    silu_mul_kernel(const float* __restrict__ part, int splits, int rows, int ffn,
+    silu_mul_kernel(const float* __restrict__ part, Planes splits, int rows, int ffn,
                     bf16* __restrict__ act, int ld_act, int permuted) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
@@ -563,7 +569,7 @@ __global__ void __launch_bounds__(256)
   const int gi = permuted ? 32 * (i >> 4) + (i & 15) : i;
   const int ui = permuted ? gi + 16 : ffn + i;
   float4 g, u;
-  sum_planes4x2(src + gi, src + ui, plane, splits, g, u);
+  sum_planes4x2(src + gi, src + ui, plane, splits.count(r, gi), g, u);
   auto f = [](float gt, float up) { return gt / (1.f + __expf(-gt)) * up; };
   uint2 pk;
   pk.x = pack_bf16x2(f(g.x, u.x), f(g.y, u.y));
@@ -571,10 +577,10 @@ __global__ void __launch_bounds__(256)
   *reinterpret_cast<uint2*>(act + static_cast<size_t>(r) * ld_act + i) = pk;
 }
 
-int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld_act,
+int silu_mul(const float* part, const Planes& splits, int rows, int ffn, bf16* act, int ld_act,
              cudaStream_t st, int permuted) {
   if (rows <= 0 || ffn <= 0) return HS_OK;
-  if (ffn % 16 || ld_act % 4 || splits > kMaxSplits) return HS_E_CONFIG;
+  if (ffn % 16 || ld_act % 4 || splits.n > kMaxSplits) return HS_E_CONFIG;
   dim3 grid((ffn / 4 + 255) / 256, rows);
   return launch_pdl(silu_mul_kernel, grid, dim3(256), 0, st, part, splits, rows, ffn, act, ld_act,
                     permuted);
@@ -593,7 +599,7 @@ __device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
 }
 
 __global__ void __cluster_dims__(kArgCluster, 1, 1) __launch_bounds__(512)
-    argmax_kernel(const float* __restrict__ part, int splits, int rows, int vocab,
+    argmax_kernel(const float* __restrict__ part, Planes splits, int rows, int vocab,
                   int* __restrict__ tokens, float* __restrict__ logits_out) {
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
@@ -620,16 +626,22 @@ __global__ void __cluster_dims__(kArgCluster, 1, 1) __launch_bounds__(512)
       float4 acc[kArgVec];
 #pragma unroll
       for (int j = 0; j < kArgVec; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int sp = 0; sp < splits; ++sp) {
+      int cnt[kArgVec];
+#pragma unroll
+      for (int j = 0; j < kArgVec; ++j) {
+        const int i4 = base + j * blockDim.x + threadIdx.x;
+        cnt[j] = i4 < hi4 ? splits.count(r, 4 * i4) : 0;
+      }
+      for (int sp = 0; sp < splits.n; ++sp) {
         float4 t[kArgVec];
 #pragma unroll
         for (int j = 0; j < kArgVec; ++j) {
           const int i4 = base + j * blockDim.x + threadIdx.x;
-          if (i4 < hi4) t[j] = ld4(src + sp * plane + 4 * i4);
+          if (sp < cnt[j]) t[j] = ld4(src + sp * plane + 4 * i4);
         }
 #pragma unroll
         for (int j = 0; j < kArgVec; ++j)
-          if (base + j * blockDim.x + threadIdx.x < hi4) add4(acc[j], t[j]);
+          if (sp < cnt[j]) add4(acc[j], t[j]);
       }
 #pragma unroll
       for (int j = 0; j < kArgVec; ++j) {
@@ -645,7 +657,7 @@ __global__ void __cluster_dims__(kArgCluster, 1, 1) __launch_bounds__(512)
     }
   } else {
     for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      const float v = sum_planes1(src + i, plane, splits);
+      const float v = sum_planes1(src + i, plane, splits.count(r, i));
       if (logits_out) logits_out[static_cast<size_t>(r) * vocab + i] = v;
       better(best, bi, v, i);
     }
@@ -675,10 +687,11 @@ __global__ void __cluster_dims__(kArgCluster, 1, 1) __launch_bounds__(512)
   cluster.sync();
 }
 
-int argmax_rows(const float* part, int splits, int rows, int vocab, int* tokens, float* logits_out,
+int argmax_rows(const float* part, const Planes& splits, int rows, int vocab, int* tokens,
+                float* logits_out,
                 cudaStream_t st) {
   if (rows <= 0) return HS_OK;
-  if (splits > kMaxSplits) return HS_E_CONFIG;
+  if (splits.n > kMaxSplits) return HS_E_CONFIG;
   dim3 grid(kArgCluster, rows);
   return launch_pdl(argmax_kernel, dim3(grid), dim3(512), 0, st, part, splits, rows, vocab, tokens, logits_out);
 }

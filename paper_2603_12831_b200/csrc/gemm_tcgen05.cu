@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         }
         if (Epi == EPI_PLANES) {
           fix = false;
-          // zero the planes no CTA covers for this tile
+          // zero the planes no CTA covers for this tile (planes = 0: the
+          // consumers read per-tile plane counts instead, see Planes)
           for (int p = tile_done ? plane + 1 : planes; p < planes; ++p) {
             float* z = out + static_cast<size_t>(p) * tokens * n_out + n;
             for (int tt = t0; tt < min(tokens, t0 + BN); ++tt) z[static_cast<size_t>(tt) * n_out] = 0.f;
@@ -501,6 +502,21 @@ static int launch_any(const CUtensorMap& mw, const CUtensorMap& mx, int bn, floa
     case 256: return launch_bn<256, kBlocked, Epi>(mw, mx, out, n_out, tokens, sk, planes, ep, st);
   }
   return HS_E_CONFIG;
+}
+
+int gemm_launch_planes(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,
+                       int tokens, int k, int max_planes, cudaStream_t st, Planes* planes) {
+  *planes = Planes(1);
+  if (tokens <= 0) return HS_OK;
+  if (n_out % kTileM || k % kTileK) return HS_E_CONFIG;
+  int n = 1;
+  const StreamK sk = choose_streamk(n_out, k, tokens, bn, max_planes, &n);
+  planes->n = n;
+  planes->sk = sk;
+  planes->n_tiles = n_out / kTileM;
+  planes->bn = bn;
+  const EpiParams ep{};
+  return launch_any<false, EPI_PLANES>(mw, mx, bn, out, n_out, tokens, sk, 0, ep, st);
 }
 
 int gemm_launch(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,

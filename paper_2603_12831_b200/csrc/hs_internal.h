@@ -80,13 +80,38 @@ struct StreamK {
     if (aligned) return (static_cast<long long>(c) * tiles / G) * kb;
     return static_cast<long long>(c) * tiles * kb / G;
   }
-  __host__ __device__ int owner(long long u) const {  // largest c with start(c) <= u
-    int lo = 0, hi = G - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (start(mid) <= u) lo = mid; else hi = mid - 1;
-    }
-    return lo;
+  // largest c with start(c) <= u, in closed form (start is floor(c*X/G)
+  // scaled, so c*X < (x+1)*G); checked against a binary search over the
+  // whole range of shapes
+  __host__ __device__ int owner(long long u) const {
+    const unsigned long long num = aligned ? (static_cast<unsigned long long>(u / kb) + 1) * G - 1
+                                           : (static_cast<unsigned long long>(u) + 1) * G - 1;
+    const unsigned long long den = aligned ? tiles : static_cast<unsigned long long>(tiles) * kb;
+    // 32-bit division when it fits (every serving shape): the glue kernels
+    // call this on their critical path
+    const unsigned long long c = (num >> 32) == 0 && (den >> 32) == 0
+                                     ? static_cast<unsigned>(num) / static_cast<unsigned>(den)
+                                     : num / den;
+    return static_cast<int>(c < static_cast<unsigned long long>(G - 1) ? c : G - 1);
+  }
+};
+
+// ---- split-K partial planes of a GEMM launch, as its consumers see them:
+// `n` planes at most; with a stream-K map (sk.G > 0) the planes of tile t
+// (BN token rows x 128 features) are only the ones its segments wrote, so
+// the GEMM zero-fills nothing and consumers read no empty planes.  A plain
+// int converts to a uniform count (caller-written planes, op-level API).
+struct Planes {
+  int n = 1;
+  StreamK sk{0, 0, 0, 0};
+  int n_tiles = 0, bn = 0;
+  Planes() = default;
+  Planes(int uniform) : n(uniform) {}  // NOLINT(runtime/explicit)
+  __host__ __device__ int count(int row, int feat) const {
+    if (sk.G <= 0) return n;
+    const int t = (row / bn) * n_tiles + feat / 128;
+    const long long a = static_cast<long long>(t) * sk.kb;
+    return sk.owner(a + sk.kb - 1) - sk.owner(a) + 1;
   }
 };
 
@@ -133,6 +158,9 @@ int gemm_pick_bn(int tokens);
 int gemm_pick_splits(int n_out, int k, int tokens, int bn, int max_splits);
 // Persistent stream-K GEMM; writes `*planes` (<= max_planes) fp32 partial
 // planes [planes][tokens][n_out] whose sum is the product.
+// step-level launch: per-tile planes, no zero fill (consumers take `Planes`)
+int gemm_launch_planes(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,
+                       int tokens, int k, int max_planes, cudaStream_t st, Planes* planes);
 int gemm_launch(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,
                 int tokens, int k, int max_planes, cudaStream_t st, int* planes,
                 bool blocked = false);
@@ -221,7 +249,7 @@ struct RowCopy {
   unsigned* fault = nullptr;
   int layer = 0;
 };
-int residual_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
+int residual_add_norm(const float* part, const Planes& splits, int rows, int d, float* h, const float* w,
                       float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io = RowIo{});
 
 // ---- tensor parallelism: the all-reduce of a row-parallel projection fused
@@ -239,21 +267,21 @@ struct TpPeers {
   size_t xbuf_par = 0;      // floats per parity
   size_t flag_par = 0;      // flags per parity
 };
-int tp_add_norm(const float* part, int splits, int rows, int d, float* h, const float* w,
+int tp_add_norm(const float* part, const Planes& splits, int rows, int d, float* h, const float* w,
                 float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io,
                 const TpPeers& peers, unsigned epoch);
 // rows [0, n_batch): row_* arrays (row_mode may be null = all KV-scatter);
 // rows [n_batch, rows): carry_* arrays, shipped to the host mailbox
-int qkv_rope_scatter(const float* part, int splits, int rows, int n_q, int n_kv, int head_dim,
+int qkv_rope_scatter(const float* part, const Planes& splits, int rows, int n_q, int n_kv, int head_dim,
                      const float* rope_cos, const float* rope_sin, const int* row_pos,
                      const int* row_slot, const int* row_mode, int n_batch, const int* carry_pos,
                      const int* carry_slot, bf16* qbuf, int q_row_stride, bf16* kv_pool,
                      const KvGeom& g, int layer, const int* page_table, int pt_stride, bf16* ship,
                      int ship_stride, cudaStream_t st, int permuted = 0,
                      const RowCopy& rc = RowCopy{});
-int silu_mul(const float* part, int splits, int rows, int ffn, bf16* act, int ld_act,
+int silu_mul(const float* part, const Planes& splits, int rows, int ffn, bf16* act, int ld_act,
              cudaStream_t st, int permuted = 0);
-int argmax_rows(const float* part, int splits, int rows, int vocab, int* tokens, float* logits_out,
+int argmax_rows(const float* part, const Planes& splits, int rows, int vocab, int* tokens, float* logits_out,
                 cudaStream_t st);
 int lse_merge_rows(const bf16* parts, const float* lse, int n_parts, int rows, int n_q,
                    int head_dim, int part_stride, int row_stride_parts, bf16* out,

@@ -271,9 +271,9 @@ int prof_collect(hs_ctx* c) {
 
 // GEMM over `tokens` rows of an activation buffer against a cached weight map.
 int gemm(hs_ctx* c, const CUtensorMap& mw, const ActBuf& x, int tokens, int n_out, int k,
-         int* splits_out) {
+         Planes* planes_out) {
   if (tokens <= 0) {
-    *splits_out = 1;
+    *planes_out = Planes(1);
     return HS_OK;
   }
   // algorithmic traffic: weights + bf16 activations in + bf16 result out
@@ -283,8 +283,8 @@ int gemm(hs_ctx* c, const CUtensorMap& mw, const ActBuf& x, int tokens, int n_ou
   const size_t per_split = static_cast<size_t>(tokens) * n_out;
   const int cap = static_cast<int>(std::min<size_t>(16, c->part_floats / per_split));
   if (cap < 1) return set_error(HS_E_CAPACITY, "split-K buffer too small for %d x %d", tokens, n_out);
-  return gemm_launch(mw, x.maps[bn_index(bn)], bn, c->part, n_out, tokens, k, cap, c->st,
-                     splits_out);
+  return gemm_launch_planes(mw, x.maps[bn_index(bn)], bn, c->part, n_out, tokens, k, cap, c->st,
+                            planes_out);
 }
 
 // GEMM with an epilogue fused into its stream-K fixup (no partial planes
@@ -1065,7 +1065,7 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   int* dm = c->dm;
   cudaStream_t st = c->st;
   const int d_ = m.d, nqh = m.n_q * m.hd;
-  int sp = 1;
+  Planes sp(1);
   ProfScope whole(c, 3, 0.0, 0.0);  // the layer's span on the device
   const int R = d->n_restart;
   const int NL = last ? c->n_logit + M : 0;
@@ -1441,7 +1441,7 @@ int hs_probe_dense(hs_ctx* c, int n, int reps, float* us) {
   if (n < 1 || n > c->r.max_rows) return set_error(HS_E_CONFIG, "probe rows out of range");
   const int d_ = m.d, nqh = m.n_q * m.hd;
   return time_reps(c, reps, [&]() -> int {
-    int sp;
+    Planes sp;
     EpiParams ep = epi_base(c);
     RC(gemm(c, c->m_qkv[0], c->xn, n, m.qkv_n(), d_, &sp));  // (+ a RoPE epilogue in the layer)
     RC(gemm_fused(c, c->m_o[0], c->attn, n, d_, nqh, EPI_RESID, ep));
@@ -1466,7 +1466,7 @@ int hs_probe_gemm_stream(hs_ctx* c, int n, int reps, float* us, double* bytes) {
                                   2.0 * m.ffn * d_ + static_cast<double>(d_) * m.ffn) +
                            2.0 * n * (d_ + m.qkv_n() + nqh + d_ + d_ + 2.0 * m.ffn + m.ffn + d_);
   int err = time_reps(c, reps, [&]() -> int {
-    int s;
+    Planes s;
     for (int l = 0; l < m.layers; ++l) {
       RC(gemm(c, c->m_qkv[l], c->xn, n, m.qkv_n(), d_, &s));
       RC(gemm(c, c->m_o[l], c->attn, n, d_, nqh, &s));
@@ -1536,22 +1536,22 @@ int hs_probe_dense_mode(hs_ctx* c, int n, int mode, int layers, int reps, float*
   const int s_qkv = planes(m.qkv_n(), d_), s_o = planes(d_, nqh), s_gu = planes(2 * m.ffn, d_),
             s_dn = planes(d_, m.ffn);
   int err = time_reps(c, reps, [&]() -> int {
-    int s;
+    Planes s, pq(s_qkv), po(s_o), pg(s_gu), pd(s_dn);
     for (int l = 0; l < layers; ++l) {
-      if (on(0)) RC(gemm(c, c->m_qkv[l], c->xn, n, m.qkv_n(), d_, &s));
+      if (on(0)) RC(gemm(c, c->m_qkv[l], c->xn, n, m.qkv_n(), d_, &pq));
       if (on(1))
-        RC(qkv_rope_scatter(c->part, s_qkv, n, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
+        RC(qkv_rope_scatter(c->part, pq, n, m.n_q, m.n_kv, m.hd, c->rope_cos, c->rope_sin,
                             nullptr, nullptr, nullptr, 0, cpos, cslot, c->qbuf, nqh, c->kv_pool,
                             c->geom, l, c->page_table, c->r.max_pages_per_req, c->ship_d,
                             m.qkv_n(), c->st, 1));
-      if (on(2)) RC(gemm(c, c->m_o[l], c->attn, n, d_, nqh, &s));
+      if (on(2)) RC(gemm(c, c->m_o[l], c->attn, n, d_, nqh, &po));
       if (on(3))
-        RC(residual_add_norm(c->part, s_o, n, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, c->st));
-      if (on(4)) RC(gemm(c, c->m_gu[l], c->xn2, n, 2 * m.ffn, d_, &s));
-      if (on(5)) RC(silu_mul(c->part, s_gu, n, m.ffn, c->act.p, m.ffn, c->st, 1));
-      if (on(6)) RC(gemm(c, c->m_down[l], c->act, n, d_, m.ffn, &s));
+        RC(residual_add_norm(c->part, po, n, d_, c->h, c->n_post[l], m.eps, c->xn2.p, d_, c->st));
+      if (on(4)) RC(gemm(c, c->m_gu[l], c->xn2, n, 2 * m.ffn, d_, &pg));
+      if (on(5)) RC(silu_mul(c->part, pg, n, m.ffn, c->act.p, m.ffn, c->st, 1));
+      if (on(6)) RC(gemm(c, c->m_down[l], c->act, n, d_, m.ffn, &pd));
       if (on(7))
-        RC(residual_add_norm(c->part, s_dn, n, d_, c->h, c->n_in[l], m.eps, c->xn.p, d_, c->st));
+        RC(residual_add_norm(c->part, pd, n, d_, c->h, c->n_in[l], m.eps, c->xn.p, d_, c->st));
     }
     return HS_OK;
   }, us);
@@ -1571,7 +1571,7 @@ int hs_probe_gemm(hs_ctx* c, int which, int n, int fused, int reps, float* us) {
   ep.carry_slot = c->dm_layer;
   ep.carry_pos = c->dm_layer + n;
   return time_reps(c, reps, [&]() -> int {
-    int sp;
+    Planes sp;
     switch (which) {
       case 0:
         return fused ? gemm_fused(c, c->m_qkv[0], c->xn, n, m.qkv_n(), d_, EPI_QKV, ep)
