@@ -18,6 +18,8 @@
 // instruction used for the tiny GQA tiles is irrelevant to that bound.
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "hs_common.cuh"
 #include "hs_internal.h"
 
@@ -35,8 +37,11 @@ int make_kv_map(CUtensorMap* map, const bf16* pool, const KvGeom& g) {
                           kPageTokens);
 }
 
-template <int HD>
-__global__ void __launch_bounds__(kDecThreads, 2)
+// WG warp groups of 4 warps: with WG = 2 the groups take alternate pages of
+// the chunk (one CTA per SM for small batches, where the page loop's
+// latency, not HBM, bounds the launch), with twice the stages in flight.
+template <int HD, int WG>
+__global__ void __launch_bounds__(kDecThreads * WG, WG == 1 ? 2 : 1)
     decode_attn_kernel(const __grid_constant__ CUtensorMap kv_map, KvGeom geom, int layer,
                        const bf16* __restrict__ q, int q_row_stride, int n_q,
                        const int* __restrict__ page_table, int pt_stride,
@@ -53,8 +58,11 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kDecStages];
-  __shared__ float sm_m[4][16], sm_l[4][16];
+  constexpr int kStages = kDecStages * WG;
+  constexpr int kThreads = kDecThreads * WG;
+  constexpr int kWarps = 4 * WG;
+  __shared__ uint64_t full[kStages];
+  __shared__ float sm_m[kWarps][16], sm_l[kWarps][16];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
@@ -66,13 +74,13 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&kv_map);
-    for (int s = 0; s < kDecStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
   auto issue = [&](int i) {
-    const int s = i % kDecStages;
+    const int s = i % kStages;
     const int phys = pt[i];
     uint8_t* dst = smem + s * kStageBytes;
     mbar_expect_tx(&full[s], kStageBytes);
@@ -89,7 +97,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   // epilogue just before) are safe to stream; the chunk list and the page
   // table were uploaded ahead of the iteration.
   const int safe = max(0, min(npages, (ch.ctx - 1) / kPageTokens - ch.page_begin));
-  const int first = min(kDecStages, npages);
+  const int first = min(kStages, npages);
   if (threadIdx.x == 0)
     for (int i = 0; i < min(first, safe); ++i) issue(i);
   pdl_wait();  // q and the new token's K/V are visible from here on
@@ -117,11 +125,14 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
   for (int i = 0; i < NT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
-  const int tb = warp * 16;  // this warp's 16 tokens inside every page
+  const int tb = (warp & 3) * 16;  // this warp's 16 tokens inside every page
+  const int wg = warp >> 2;         // pages wg, wg + WG, ... are this group's
 
-  for (int i = 0; i < npages; ++i) {
-    const int s = i % kDecStages;
-    mbar_wait(&full[s], (i / kDecStages) & 1);
+  for (int i0 = 0; i0 < npages; i0 += WG) {
+   const int i = i0 + wg;
+   if (i < npages) {
+    const int s = i % kStages;
+    mbar_wait(&full[s], (i / kStages) & 1);
     const int tok0 = (ch.page_begin + i) * kPageTokens + tb;
     if (tok0 < ch.ctx) {  // warp-uniform
       const uint32_t kbase = smem_u32(smem + s * kStageBytes);
@@ -199,8 +210,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         }
       }
     }
-    __syncthreads();  // every warp is done with stage s
-    if (threadIdx.x == 0 && i + kDecStages < npages) issue(i + kDecStages);
+   }
+    __syncthreads();  // every warp is done with its stage
+    if (threadIdx.x == 0)
+      for (int j = i0 + kStages; j < i0 + kStages + WG && j < npages; ++j) issue(j);
   }
 
   // quad-reduce the row sums
@@ -218,7 +231,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   // cross-warp merge: rescale each warp's O to the common max, sum in smem
   float M0 = -CUDART_INF_F, M1 = -CUDART_INF_F;
 #pragma unroll
-  for (int w = 0; w < 4; ++w) {
+  for (int w = 0; w < kWarps; ++w) {
     M0 = fmaxf(M0, sm_m[w][g]);
     M1 = fmaxf(M1, sm_m[w][g + 8]);
   }
@@ -240,15 +253,15 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   const int c_lo = out ? row_chunk_begin[ch.row] : 0;
   const int n_row_chunks = out ? row_chunk_begin[ch.row + 1] - c_lo : 0;
   if (out && n_row_chunks == 1) {  // whole row in this CTA: normalise and store
-    for (int idx = threadIdx.x; idx < G * HD; idx += kDecThreads) {
+    for (int idx = threadIdx.x; idx < G * HD; idx += kThreads) {
       const int r = idx / HD, d = idx % HD;
       float Mr = -CUDART_INF_F;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) Mr = fmaxf(Mr, sm_m[w][r]);
+      for (int w = 0; w < kWarps; ++w) Mr = fmaxf(Mr, sm_m[w][r]);
       const float Mur = Mr == -CUDART_INF_F ? 0.f : Mr;
       float L = 0.f, acc = 0.f;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
+      for (int w = 0; w < kWarps; ++w) {
         L += sm_l[w][r] * exp2f(sm_m[w][r] - Mur);
         acc += so[(w * 16 + r) * SO + d];
       }
@@ -257,15 +270,15 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     }
     return;
   }
-  for (int idx = threadIdx.x; idx < G * HD; idx += kDecThreads) {
+  for (int idx = threadIdx.x; idx < G * HD; idx += kThreads) {
     const int r = idx / HD, d = idx % HD;
     float Mr = -CUDART_INF_F;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) Mr = fmaxf(Mr, sm_m[w][r]);
+    for (int w = 0; w < kWarps; ++w) Mr = fmaxf(Mr, sm_m[w][r]);
     const float Mur = Mr == -CUDART_INF_F ? 0.f : Mr;
     float L = 0.f, acc = 0.f;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < kWarps; ++w) {
       L += sm_l[w][r] * exp2f(sm_m[w][r] - Mur);
       acc += so[(w * 16 + r) * SO + d];
     }
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   // loads, per-head weights, then the weighted sum with 4 loads in flight
   float* s_w = reinterpret_cast<float*>(smem);  // [n_row_chunks][G]
   float* s_inv = s_w + n_row_chunks * G;        // [G]
-  for (int i = threadIdx.x; i < n_row_chunks * G; i += kDecThreads) {
+  for (int i = threadIdx.x; i < n_row_chunks * G; i += kThreads) {
     const int c = c_lo + i / G, r = i % G;
     s_w[i] = __ldcg(&lse_part[(c * geom.n_kv + kvh) * G + r]);
   }
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     s_inv[r] = ws > 0.f ? 1.f / ws : 0.f;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < G * HD; idx += kDecThreads) {
+  for (int idx = threadIdx.x; idx < G * HD; idx += kThreads) {
     const int r = idx / HD, d = idx % HD;
     const float* src = o_part + (static_cast<size_t>(c_lo * geom.n_kv + kvh) * G + r) * HD + d;
     const size_t cstride = static_cast<size_t>(geom.n_kv) * G * HD;
@@ -368,26 +381,50 @@ __global__ void decode_combine_kernel(const float* __restrict__ o_part,
   if (lse_out && lane == 0) lse_out[pair] = wsum > 0.f ? mu + logf(wsum) : -CUDART_INF_F;
 }
 
+template <int HD, int WG>
+static int launch_decode_wg(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                            int q_row_stride, int n_q, const int* pt, int pt_stride,
+                            const DecodeChunk* chunks, int n_chunks, float* o_part,
+                            float* lse_part, cudaStream_t st, const int* row_chunk_begin,
+                            int* counters, bf16* out, int out_row_stride) {
+  constexpr int kStageBytes = 2 * (HD / 64) * kPageTokens * 128;
+  constexpr int kSmem = kDecStages * WG * kStageBytes + 1024;
+  static_assert(4 * WG * 16 * (HD + 8) * 4 <= kDecStages * WG * kStageBytes,
+                "merge scratch must fit");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_attn_kernel<HD, WG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmem);
+    attr = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
+  dim3 grid(n_chunks, g.n_kv);
+  return launch_pdl(decode_attn_kernel<HD, WG>, dim3(grid), dim3(kDecThreads * WG), kSmem, st,
+                    kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, chunks, o_part,
+                    lse_part, scale_log2, row_chunk_begin, counters, out, out_row_stride);
+}
+
+// Two warp groups per CTA when the launch is at most one CTA per SM (small
+// batches, latency-bound page loops); one group otherwise (HS_DEC_WG=1/2
+// forces it, tuning knob).
 template <int HD>
 static int launch_decode(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
                          int q_row_stride, int n_q, const int* pt, int pt_stride,
                          const DecodeChunk* chunks, int n_chunks, float* o_part, float* lse_part,
                          cudaStream_t st, const int* row_chunk_begin = nullptr,
                          int* counters = nullptr, bf16* out = nullptr, int out_row_stride = 0) {
-  constexpr int kStageBytes = 2 * (HD / 64) * kPageTokens * 128;
-  constexpr int kSmem = kDecStages * kStageBytes + 1024;
-  static_assert(4 * 16 * HD * 4 <= kDecStages * kStageBytes, "merge scratch must fit");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmem);
-    attr = true;
-  }
-  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
-  dim3 grid(n_chunks, g.n_kv);
-  return launch_pdl(decode_attn_kernel<HD>, dim3(grid), dim3(kDecThreads), kSmem, st, kv_map, g,
-                    layer, q, q_row_stride, n_q, pt, pt_stride, chunks, o_part, lse_part,
-                    scale_log2, row_chunk_begin, counters, out, out_row_stride);
+  static const int forced = [] {
+    const char* e = getenv("HS_DEC_WG");
+    return e ? atoi(e) : 0;
+  }();
+  const bool two = forced ? forced == 2 : n_chunks * g.n_kv <= 148;
+  if (two)
+    return launch_decode_wg<HD, 2>(kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, chunks,
+                                   n_chunks, o_part, lse_part, st, row_chunk_begin, counters, out,
+                                   out_row_stride);
+  return launch_decode_wg<HD, 1>(kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, chunks,
+                                 n_chunks, o_part, lse_part, st, row_chunk_begin, counters, out,
+                                 out_row_stride);
 }
 
 int decode_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
