@@ -282,11 +282,16 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
       __threadfence_system();
       st_release_sys(peers.flag[peers.me] + foff, epoch);
       // 2. wait for every peer's partial of the same columns
+      // a peer that never publishes fails the launch after 20 s instead of
+      // hanging the device (time-sliced peers on one GPU may take a while)
+      uint64_t t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
       for (int p = 0; p < peers.world; ++p) {
-        unsigned spins = 0;
         while (static_cast<int>(ld_acquire_sys(peers.flag[p] + foff) - epoch) < 0) {
-          __nanosleep(64);
-          if (++spins > (1u << 25)) __trap();  // a peer never published: fail, do not hang
+          __nanosleep(256);
+          uint64_t now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          if (now - t0 > 20000000000ull) __trap();
         }
       }
     }

@@ -123,10 +123,11 @@ def test_tp2_two_processes_match_full_oracle(cuda):
         out[rank] = (counters, gen, stats)
     for p in procs:
         p.join(timeout=60)
-        assert p.exitcode == 0
+    assert [p.exitcode for p in procs] == [0, 0], [p.exitcode for p in procs]
     (c0, g0, st), (c1, g1, _) = out[0], out[1]
     assert c0 == c1 and c0["merges"] > 0 and c0["injections"] > 0
-    assert g0 == g1  # bit-identical residual streams -> identical greedy tokens
+    diverged = [k for k in g0 if g0[k] != g1.get(k)]
+    assert not diverged, diverged[:5]  # bit-identical residual streams -> identical tokens
     compared, max_rel, ties, bad = st
     assert compared == c0["tokens_total"] > 0
     assert not bad, bad
