@@ -1,3 +1,4 @@
+# per-kernel in-stream cost by ablation (HS_SKIP) on whole iterations (tools/probe_step.py)
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 for a in "8 700 0" "32 700 0"; do
   for m in 0 1 2 4 8 16 29 31 32 64 128 256 480 511; do

@@ -1,3 +1,4 @@
+# decode attention: one vs two warp groups (HS_DEC_WG), parity tests first
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 timeout 600 python -m pytest tests/test_ops_gpu.py tests/test_serving.py -q -m gpu -x 2>&1 | tail -1
 HS_DEC_WG=2 timeout 600 python -m pytest tests/test_ops_gpu.py -q -m gpu -x -k decode 2>&1 | tail -1

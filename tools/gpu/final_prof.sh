@@ -1,3 +1,4 @@
+# end-of-round record: bench, reference arm, steady-state ncu launch list
 O=gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 echo "== bench"; timeout 1200 python bench.py > $O/bench_final.log 2>&1; tail -c 400 $O/bench_final.log; echo

@@ -1,3 +1,4 @@
+# shared-memory stage counts (decode attention / GEMM) under PDL co-residency
 # stage-count sweep: decode-attention smem vs GEMM co-residency under PDL
 for v in "3 6 5" "2 6 5" "2 4 4" "3 4 4" "2 5 4" "2 4 3"; do
   set -- $v
