@@ -19,10 +19,8 @@ namespace hs {
 
 constexpr int kMaxSplits = 16;
 
-// Sum of `splits` fp32 split-K planes at p (plane stride in floats), plane 0
-// first (a fixed order: results are bit-reproducible).  Runtime loop issuing
-// four planes' loads at a time: few registers, so the glue kernels keep full
-// occupancy and enough bytes in flight to stream HBM.
+// Sums of `splits` fp32 split-K planes at p (plane stride in floats), plane 0
+// first (a fixed order: results are bit-reproducible).
 __device__ __forceinline__ void add4(float4& a, const float4& v) {
   a.x += v.x;
   a.y += v.y;
@@ -34,24 +32,8 @@ __device__ __forceinline__ float4 ld4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-__device__ __forceinline__ float4 sum_planes4(const float* __restrict__ p, size_t plane,
-                                              int splits) {
-  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-  int k = 0;
-  for (; k + 4 <= splits; k += 4) {
-    const float4 v0 = ld4(p + k * plane), v1 = ld4(p + (k + 1) * plane),
-                 v2 = ld4(p + (k + 2) * plane), v3 = ld4(p + (k + 3) * plane);
-    add4(a, v0);
-    add4(a, v1);
-    add4(a, v2);
-    add4(a, v3);
-  }
-  for (; k < splits; ++k) add4(a, ld4(p + k * plane));
-  return a;
-}
-
 // Every plane's load in flight at once (one memory round trip for up to
-// kMaxSplits planes), summed plane 0 first -- the same order as sum_planes4.
+// kMaxSplits planes), summed plane 0 first.
 __device__ __forceinline__ float4 sum_planes4_all(const float* __restrict__ p, size_t plane,
                                                   int splits) {
   float4 v[kMaxSplits];
