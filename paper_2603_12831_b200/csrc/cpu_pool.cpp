@@ -61,6 +61,7 @@ class CpuService {
   // mailboxes / KV resolution provided by the context
   std::function<bf16*(int slot)> ship_row, result_row, host_kv;
   std::function<void(int slot, int ctx, int layer)> publish;
+  std::function<void(int slot)> retract;  // the slot's previous completion tag is void
   std::function<int(int slot)> host_cap;
 
   int submit(cudaStream_t st, const int* slots, const int* layers, const int* ctxs, int n) {
@@ -81,8 +82,11 @@ class CpuService {
       next_ev_ = (ev + 1) % events_.size();
       ev_refs_[ev] = n;
     }
-    if (cudaEventRecord(events_[ev], st) != cudaSuccess)
+    if (cudaEventRecord(events_[ev], st) != cudaSuccess) {
+      std::lock_guard<std::mutex> g(mu_);
+      ev_refs_[ev] = 0;  // not handed to any item
       return set_error(HS_E_CUDA, "cpu service: event record failed");
+    }
     const double now = wall();
     {
       std::lock_guard<std::mutex> g(mu_);
@@ -137,6 +141,11 @@ class CpuService {
         it = items_[t.item];
       }
       cudaEventSynchronize(events_[it.ev]);  // the shipped row has landed
+      // the slot's previous result was consumed before this item's ship
+      // launch (stream order): retract its tag so the device cannot take a
+      // stale tag for this item's result (every head does it before the
+      // item's publish below)
+      retract(it.slot);
       const auto t0 = std::chrono::steady_clock::now();
       cpu_attend_head(m_, ship_row(it.slot), host_kv(it.slot), host_cap(it.slot), it.layer - 1,
                       it.ctx, t.head, result_row(it.slot), nullptr);
@@ -180,12 +189,14 @@ CpuService* make_cpu_service(const ModelCfg& m, int threads, const std::vector<i
 void destroy_cpu_service(CpuService* s) { delete s; }
 void cpu_service_bind(CpuService* s, std::function<bf16*(int)> ship, std::function<bf16*(int)> res,
                       std::function<bf16*(int)> kv, std::function<int(int)> cap,
-                      std::function<void(int, int, int)> publish) {
+                      std::function<void(int, int, int)> publish,
+                      std::function<void(int)> retract) {
   s->ship_row = std::move(ship);
   s->result_row = std::move(res);
   s->host_kv = std::move(kv);
   s->host_cap = std::move(cap);
   s->publish = std::move(publish);
+  s->retract = std::move(retract);
 }
 int cpu_service_submit(CpuService* s, cudaStream_t st, const int* slots, const int* layers,
                        const int* ctxs, int n) {

@@ -452,17 +452,28 @@ __global__ void __launch_bounds__(256)
   const int r = blockIdx.y;
   if (r >= rows) {  // merged rows: host attention result -> attention buffer
     const int i = r - rows;
-    if (rc.expect && blockIdx.x == 0 && threadIdx.x == 0) {
-      const int slot = rc.idx[i];
-      unsigned tag;
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(tag) : "l"(rc.tags + slot) : "memory");
-      if (tag != static_cast<unsigned>(rc.expect[i])) {
-        rc.fault[1] = slot;
-        rc.fault[2] = rc.layer;
-        rc.fault[3] = tag;
-        __threadfence_system();
-        atomicExch(rc.fault, 1u);
+    // device-polled merges: candidates past the taken count are not consumed
+    if (rc.taken && i >= *rc.taken) return;
+    if (rc.expect) {
+      // every CTA copying part of the row acquires the row's completion tag
+      // itself (the acquire orders this CTA's row loads after the worker's
+      // release); a row whose tag does not match is not consumed
+      __shared__ int ok;
+      if (threadIdx.x == 0) {
+        const int slot = rc.idx[i];
+        unsigned tag;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(tag) : "l"(rc.tags + slot) : "memory");
+        ok = tag == static_cast<unsigned>(rc.expect[i]);
+        if (!ok && blockIdx.x == 0) {
+          rc.fault[1] = slot;
+          rc.fault[2] = rc.layer;
+          rc.fault[3] = tag;
+          __threadfence_system();
+          atomicExch(rc.fault, 1u);
+        }
       }
+      __syncthreads();
+      if (!ok) return;
     }
     const uint4* src = reinterpret_cast<const uint4*>(rc.src + static_cast<size_t>(rc.idx[i]) * rc.src_stride);
     uint4* dst = reinterpret_cast<uint4*>(rc.dst + static_cast<size_t>(i) * rc.dst_stride);

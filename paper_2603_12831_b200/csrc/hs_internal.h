@@ -248,6 +248,8 @@ struct RowCopy {
   const unsigned* tags = nullptr;
   unsigned* fault = nullptr;
   int layer = 0;
+  // device-polled merges: only rows i < *taken are consumed (null = all)
+  const int* taken = nullptr;
 };
 int residual_add_norm(const float* part, const Planes& splits, int rows, int d, float* h, const float* w,
                       float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io = RowIo{});

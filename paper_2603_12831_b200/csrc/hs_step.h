@@ -71,7 +71,8 @@ CpuService* make_cpu_service(const ModelCfg& m, int threads, const std::vector<i
 void destroy_cpu_service(CpuService* s);
 void cpu_service_bind(CpuService* s, std::function<bf16*(int)> ship, std::function<bf16*(int)> res,
                       std::function<bf16*(int)> kv, std::function<int(int)> cap,
-                      std::function<void(int, int, int)> publish);
+                      std::function<void(int, int, int)> publish,
+                      std::function<void(int)> retract);
 int cpu_service_submit(CpuService* s, cudaStream_t st, const int* slots, const int* layers,
                        const int* ctxs, int n);
 int cpu_service_poll(CpuService* s, int* slots, int* layers, double* t_done, int max);

@@ -467,6 +467,10 @@ int build_maps(hs_ctx* c) {
 }
 
 void free_all(hs_ctx* c) {
+  // stop and join the CPU-attention workers first: an in-flight work item
+  // reads the ship mailbox and host KV and writes the result mailbox / tags
+  if (c->cpu) destroy_cpu_service(c->cpu);
+  c->cpu = nullptr;
   auto F = [](void* p) {
     if (p) cudaFree(p);
   };
@@ -509,7 +513,6 @@ void free_all(hs_ctx* c) {
   if (c->hkv_h) cudaFreeHost(c->hkv_h);
   for (auto& e : c->stage_ev)
     if (e) cudaEventDestroy(e);
-  if (c->cpu) destroy_cpu_service(c->cpu);
   for (auto e : c->marks) cudaEventDestroy(e);
   for (auto e : c->iter_ev)
     if (e) cudaEventDestroy(e);
@@ -686,6 +689,12 @@ void publish_tag(hs_ctx* c, int slot, int ctx, int layer) {
       ->store(static_cast<unsigned>(HS_RESULT_TAG(ctx, layer)), std::memory_order_release);
 }
 
+// The slot's previous completion tag no longer stands for a result in the
+// mailbox (a new work item of the slot is being serviced).
+void retract_tag(hs_ctx* c, int slot) {
+  reinterpret_cast<std::atomic<unsigned>*>(c->tag_h + slot)->store(0xffffffffu, std::memory_order_relaxed);
+}
+
 // Integrity faults the kernels recorded (a merged result whose completion
 // tag did not match): HS_E_INTEGRITY, the reference's IntegrityFault.
 int check_device_faults(hs_ctx* c) {
@@ -707,7 +716,8 @@ int ensure_cpu_service(hs_ctx* c) {
       c->cpu, [c, qkv](int s) { return c->ship_h + static_cast<size_t>(s) * qkv; },
       [c, nqh](int s) { return c->result_h + static_cast<size_t>(s) * nqh; },
       [c](int s) { return host_region(c, s); }, [c](int s) { return c->regions[s].cap; },
-      [c](int s, int ctx, int layer) { publish_tag(c, s, ctx, layer); });
+      [c](int s, int ctx, int layer) { publish_tag(c, s, ctx, layer); },
+      [c](int s) { retract_tag(c, s); });
   return HS_OK;
 }
 
@@ -991,6 +1001,16 @@ int hs_iter_begin(hs_ctx* c, const hs_iter_desc* d) {
       d->n_chunks > r.max_chunks || d->n_logit_rows > d->n_rows || d->n_tiles > r.max_rows)
     return set_error(HS_E_CAPACITY, "iteration exceeds capacities (rows %d, chunks %d)", d->n_rows,
                      d->n_chunks);
+  // every batch row writes its K/V into the slot's pages at row_pos and is
+  // rotated with the RoPE table row row_pos
+  for (int i = 0; i < d->n_rows; ++i) {
+    if (d->row_slot[i] < 0 || d->row_slot[i] >= r.max_slots)
+      return set_error(HS_E_CONFIG, "row %d: slot %d out of range", i, d->row_slot[i]);
+    if (d->row_pos[i] < 0 || d->row_pos[i] >= r.max_pos ||
+        d->row_pos[i] / kPageTokens >= r.max_pages_per_req)
+      return set_error(HS_E_CONFIG, "row %d: position %d outside max_pos %d / page table", i,
+                       d->row_pos[i], r.max_pos);
+  }
   // switch pinned staging halves: everything staged into the current half is
   // enqueued before this event; the new half may be rewritten once the
   // copies staged into it last time have executed
@@ -1062,6 +1082,19 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   if (l < 0 || l >= m.layers) return set_error(HS_E_CONFIG, "layer %d out of range", d->layer);
   if (B + C > r.max_rows || B + M > r.max_rows || d->n_restart > M)
     return set_error(HS_E_CAPACITY, "layer rows exceed max_rows");
+  for (int i = 0; i < C; ++i)
+    if (d->carry_pos[i] < 0 || d->carry_pos[i] >= r.max_pos || d->carry_slot[i] < 0 ||
+        d->carry_slot[i] >= r.max_slots)
+      return set_error(HS_E_CONFIG, "carry row %d: slot %d / position %d out of range", i,
+                       d->carry_slot[i], d->carry_pos[i]);
+  for (int i = 0; i < M; ++i)
+    if (d->merge_slot[i] < 0 || d->merge_slot[i] >= r.max_slots)
+      return set_error(HS_E_CONFIG, "merge row %d: slot %d out of range", i, d->merge_slot[i]);
+  for (int i = 0; i < d->n_restart; ++i)
+    if (d->restart_idx[i] < 0 || d->restart_idx[i] >= M || d->restart_pos[i] < 0 ||
+        d->restart_pos[i] >= r.max_pos)
+      return set_error(HS_E_CONFIG, "restart row %d: index %d / position %d out of range", i,
+                       d->restart_idx[i], d->restart_pos[i]);
   int* dm = c->dm;
   cudaStream_t st = c->st;
   const int d_ = m.d, nqh = m.n_q * m.hd;
@@ -1383,7 +1416,10 @@ int hs_cpu_attend(hs_ctx* c, const int* slots, const int* layers, const int* ctx
       return set_error(HS_E_CAPACITY, "host KV of slot %d full (ctx %d)", slots[i], ctxs[i]);
     if (layers[i] < 1 || layers[i] > m.layers)
       return set_error(HS_E_CONFIG, "work item layer %d out of range", layers[i]);
+    if (ctxs[i] < 0 || ctxs[i] >= c->r.max_pos)
+      return set_error(HS_E_CONFIG, "work item ctx %d outside [0, max_pos)", ctxs[i]);
   }
+  for (int i = 0; i < n; ++i) retract_tag(c, slots[i]);
   c->pool->parallel_for(n * m.n_kv, [&](int task) {
     const int i = task / m.n_kv, h = task % m.n_kv;
     const int s = slots[i];
@@ -1665,6 +1701,10 @@ int hs_cpu_submit(hs_ctx* c, const int* slots, const int* layers, const int* ctx
       return set_error(HS_E_INTEGRITY, "work item for slot %d without host KV", slots[i]);
     if (ctxs[i] >= c->regions[slots[i]].cap)
       return set_error(HS_E_CAPACITY, "host KV of slot %d full (ctx %d)", slots[i], ctxs[i]);
+    if (layers[i] < 1 || layers[i] > c->m.layers)
+      return set_error(HS_E_CONFIG, "work item layer %d out of range", layers[i]);
+    if (ctxs[i] < 0 || ctxs[i] >= c->r.max_pos)
+      return set_error(HS_E_CONFIG, "work item ctx %d outside [0, max_pos)", ctxs[i]);
   }
   return cpu_service_submit(c->cpu, c->st, slots, layers, ctxs, n);
 }

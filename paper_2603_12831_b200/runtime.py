@@ -620,6 +620,10 @@ class LiveCudaStep(CudaStep):
         self.last_device_ms = 0.0
         self.swap_out_tickets: dict[int, str] = {}
         self._inflight: list[tuple[int, list[str], object]] = []  # (ticket, reqs, payload)
+        # iterations finished by a blocking drain() (a recompute rebuild
+        # needing their tokens) that the engine has not resolved yet: handed
+        # out first by the next poll_iterations()
+        self._drained: list = []
         self.anchor_wall = 0.0
 
     def set_anchor(self, wall: float) -> None:
@@ -645,11 +649,17 @@ class LiveCudaStep(CudaStep):
         self._inflight.append((ticket, self._logit_reqs + self._merge_L, payload))
         self.iterations += 1
 
-    def drain(self):
-        return self.poll_iterations(block=True)
+    def drain(self) -> None:
+        """Finish every in-flight iteration (their tokens are recorded); the
+        records stay queued for the engine's next poll_iterations()."""
+        self._drained += self._poll(block=True)
 
     def poll_iterations(self, block: bool = False):
         """Finished iterations in order: [(payload, t_done_wall, tokens)]."""
+        out, self._drained = self._drained, []
+        return out + self._poll(block)
+
+    def _poll(self, block: bool):
         out = []
         while self._inflight:
             ticket, reqs, payload = self._inflight[0]
