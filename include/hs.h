@@ -168,7 +168,17 @@ typedef struct {
      first-touched from them.  NULL / 0 = no pinning. */
   const int* cpu_list;
   int n_cpu_list;
+  /* HS_PREC_BF16: the serving datapath (bf16 weights / activations / KV, fp32
+     accumulation and residual stream, tcgen05 GEMMs).  HS_PREC_FP32: the
+     validation datapath (north star: logits within 1e-4 of the fp32 oracle,
+     greedy tokens identical over the first 64 steps) -- fp32 weights,
+     activations, KV pool, piggyback mailboxes, host KV and CPU attention,
+     SIMT kernels on the same device; probes and tensor parallelism are
+     bf16-only. */
+  int precision;
 } hs_rt_cfg;
+#define HS_PREC_BF16 0
+#define HS_PREC_FP32 1
 
 enum {
   HS_W_EMBED = 0, HS_W_LM_HEAD = 1, HS_W_FINAL_NORM = 2, HS_W_QKV = 3, HS_W_O = 4,
@@ -323,7 +333,10 @@ int hs_probe_prefill(hs_ctx* ctx, int q, int done, int reps, float* us);
 /* test taps */
 int hs_keep_logits(hs_ctx* ctx, int on);
 int hs_read_logits(hs_ctx* ctx, float* host, int rows);
+/* logits of a pipelined iteration (hs_iter_end_async ticket; hs_keep_logits on) */
+int hs_iter_logits(hs_ctx* ctx, int ticket, float* host, int rows);
 int hs_read_ship(hs_ctx* ctx, int slot, void* host, size_t bytes);
+int hs_read_result(hs_ctx* ctx, int slot, void* host, size_t bytes);
 int hs_read_residual(hs_ctx* ctx, int slot, float* host);
 
 #if defined(__GNUC__)

@@ -40,12 +40,14 @@ def from_bf16_bits(b: np.ndarray) -> np.ndarray:
 
 
 def rope_tables(max_pos: int, head_dim: int, theta: float) -> tuple[np.ndarray, np.ndarray]:
-    """cos/sin tables [max_pos, head_dim/2] (fp32 inverse frequencies as in
-    HF LlamaRotaryEmbedding, angles evaluated in float64)."""
+    """cos/sin tables [max_pos, head_dim/2]: HF LlamaRotaryEmbedding's
+    inverse frequencies theta^(-2i/hd) and angles pos * inv, both evaluated in
+    float64 and rounded to fp32 once (HF rounds the inverse frequency to fp32
+    first; at the 9k-32k positions of long BE contexts that alone moves the
+    angle by ~5e-4 rad, far above the fp32 validation bound)."""
     half = head_dim // 2
-    inv = (1.0 / (theta ** (np.arange(0, head_dim, 2, dtype=np.int64).astype(np.float32)
-                            / head_dim))).astype(np.float32)
-    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv.astype(np.float64)[None, :half]
+    inv = 1.0 / (float(theta) ** (np.arange(0, head_dim, 2, dtype=np.float64) / head_dim))
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :half]
     return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
 
 

@@ -92,9 +92,10 @@ class OracleModel:
 class OracleStep:
     """LayerStep restatement (duck-typed; see paper_2603_12831_b200.engine)."""
 
-    def __init__(self, cfg, weights: dict, prompt_fn):
+    def __init__(self, cfg, weights: dict, prompt_fn, bf16_points: bool = True):
         self.cfg = cfg
-        self.m = OracleModel(cfg, weights)
+        # bf16_points=False: the fp32 validation datapath (no bf16 roundings)
+        self.m = OracleModel(cfg, weights, bf16_points)
         self.prompt_fn = prompt_fn  # (req_id, length) -> int32 ids
         self.kv: dict[str, np.ndarray] = {}
         self.resid: dict[str, np.ndarray] = {}
@@ -105,6 +106,10 @@ class OracleStep:
         self.pending: dict[str, tuple] = {}  # chains waiting for QKV(l+1)
         self.logit_log: list[tuple[str, np.ndarray]] = []
         self.forced = 0
+        # teacher forcing known in advance (replays of a recorded run): the
+        # token to emit for a request, used instead of the oracle's argmax --
+        # also for a chain's restart, which embeds the token inside layer L
+        self.teacher: dict[str, int] = {}
 
     # -- helpers --------------------------------------------------------------
     def attach(self, engine):
@@ -195,6 +200,10 @@ class OracleStep:
                 self._ship_qkv(rid, 0, h1, self.engine.requests[rid].ctx)
 
     def _emit(self, rid, tok, lg):
+        if rid in self.teacher:
+            forced = self.teacher.pop(rid)
+            self.forced += forced != tok
+            tok = forced
         self.last_token[rid] = tok
         self.generated.setdefault(rid, []).append(tok)
         self.logit_log.append((rid, lg))
@@ -230,14 +239,16 @@ class OracleStep:
     def finish(self): ...
 
 
-def make_weights(cfg, seed: int = 0, std: float = 0.02) -> dict:
-    """Synthetic Llama weights: N(0, std) rounded to bf16; norm gains
-    1 + 0.1 N(0,1) in fp32 so the norm weights are exercised."""
+def make_weights(cfg, seed: int = 0, std: float = 0.02, bf16: bool = True) -> dict:
+    """Synthetic Llama weights: N(0, std) rounded to bf16 (or kept fp32 for
+    the fp32 validation datapath); norm gains 1 + 0.1 N(0,1) in fp32 so the
+    norm weights are exercised."""
     rng = np.random.default_rng(seed)
     d, L = cfg.d_model, cfg.n_layers
 
     def mat(n, k):
-        return O.to_bf16((rng.standard_normal((n, k)) * std).astype(np.float32))
+        m = (rng.standard_normal((n, k)) * std).astype(np.float32)
+        return O.to_bf16(m) if bf16 else m
 
     def gain():
         return (1.0 + 0.1 * rng.standard_normal(d)).astype(np.float32)
@@ -254,8 +265,11 @@ def make_weights(cfg, seed: int = 0, std: float = 0.02) -> dict:
     return w
 
 
-def device_weights(w: dict) -> dict:
-    """Same weights in libhs' host format: bf16 bit patterns, fp32 norms."""
+def device_weights(w: dict, fp32: bool = False) -> dict:
+    """Same weights in libhs' host format: bf16 bit patterns (or fp32
+    matrices for the fp32 datapath), fp32 norms."""
+    if fp32:
+        return w
     out = {}
     for k, v in w.items():
         if isinstance(v, list):

@@ -10,8 +10,10 @@
 #include <pthread.h>
 #include <sched.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "hs_step.h"
 
@@ -193,8 +195,50 @@ static void attend_dispatch(const ModelCfg& m, const uint16_t* q, const uint16_t
     attend_head(m, q, K, V, n_keys, out, lse);
 }
 
+// fp32 validation datapath: same layout in fp32 elements, exact float64 sums
+void cpu_attend_head_f32(const ModelCfg& m, const float* ship, float* host_kv, int cap, int layer,
+                         int ctx, int h, float* out_row) {
+  const int hd = m.hd, G = m.n_q / m.n_kv;
+  const float* k_new = ship + static_cast<size_t>(m.n_q) * hd + static_cast<size_t>(h) * hd;
+  const float* v_new = ship + static_cast<size_t>(m.n_q + m.n_kv) * hd + static_cast<size_t>(h) * hd;
+  float* K = host_kv + ((static_cast<size_t>(layer) * 2 + 0) * m.n_kv + h) * cap * hd;
+  float* V = host_kv + ((static_cast<size_t>(layer) * 2 + 1) * m.n_kv + h) * cap * hd;
+  std::memcpy(K + static_cast<size_t>(ctx) * hd, k_new, hd * sizeof(float));
+  std::memcpy(V + static_cast<size_t>(ctx) * hd, v_new, hd * sizeof(float));
+  const int n = ctx + 1;
+  std::vector<double> sc(n), acc(hd);
+  const double scale = 1.0 / std::sqrt(static_cast<double>(hd));
+  for (int g = 0; g < G; ++g) {
+    const float* q = ship + static_cast<size_t>(h * G + g) * hd;
+    double mx = -1e300;
+    for (int j = 0; j < n; ++j) {
+      const float* k = K + static_cast<size_t>(j) * hd;
+      double dot = 0.0;
+      for (int e = 0; e < hd; ++e) dot += static_cast<double>(q[e]) * k[e];
+      sc[j] = dot * scale;
+      mx = std::max(mx, sc[j]);
+    }
+    double l = 0.0;
+    std::fill(acc.begin(), acc.end(), 0.0);
+    for (int j = 0; j < n; ++j) {
+      const double p = std::exp(sc[j] - mx);
+      l += p;
+      const float* v = V + static_cast<size_t>(j) * hd;
+      for (int e = 0; e < hd; ++e) acc[e] += p * v[e];
+    }
+    float* o = out_row + static_cast<size_t>(h * G + g) * hd;
+    for (int e = 0; e < hd; ++e) o[e] = static_cast<float>(acc[e] / l);
+  }
+}
+
 void cpu_attend_head(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int cap, int layer,
                      int ctx, int h, bf16* out_row, float* lse_out) {
+  if (m.fp32) {
+    cpu_attend_head_f32(m, reinterpret_cast<const float*>(ship_row),
+                        reinterpret_cast<float*>(host_kv), cap, layer, ctx, h,
+                        reinterpret_cast<float*>(out_row));
+    return;
+  }
   const int hd = m.hd, G = m.n_q / m.n_kv;
   const uint16_t* ship = reinterpret_cast<const uint16_t*>(ship_row);
   const uint16_t* q = ship + static_cast<size_t>(h) * G * hd;

@@ -54,6 +54,7 @@ class ThreadPool {
 struct ModelCfg {
   int d, layers, n_q, n_kv, hd, ffn, vocab;
   float theta, eps;
+  bool fp32 = false;  // validation datapath: fp32 mailboxes, host KV and CPU attention
   int qkv_n() const { return (n_q + 2 * n_kv) * hd; }
 };
 
@@ -62,6 +63,9 @@ struct ModelCfg {
 // ([layers][2][n_kv][cap][hd] bf16) and attends q over ctx+1 entries.
 void cpu_attend_head(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int cap, int layer,
                      int ctx, int h, bf16* out_row, float* lse_out);
+// fp32 validation datapath: the same over fp32 rows / host KV (float64 sums)
+void cpu_attend_head_f32(const ModelCfg& m, const float* ship_row, float* host_kv, int cap,
+                         int layer, int ctx, int h, float* out_row);
 void cpu_attend_one(const ModelCfg& m, const bf16* ship_row, bf16* host_kv, int cap, int layer,
                     int ctx, bf16* out_row, float* lse_out);
 

@@ -34,126 +34,7 @@
 #include "hs_internal.h"
 #include "hs_step.h"
 
-namespace hs {
-
-static const int kBns[5] = {16, 32, 64, 128, 256};
-static int bn_index(int bn) {
-  for (int i = 0; i < 5; ++i)
-    if (kBns[i] == bn) return i;
-  return 4;
-}
-
-struct ActBuf {  // a bf16 activation buffer with one TMA map per token-tile width
-  bf16* p = nullptr;
-  int rows = 0, k = 0;
-  CUtensorMap maps[5];
-};
-
-struct HostRegion {
-  size_t offset = 0;  // bytes into the arena
-  int cap = 0;        // tokens
-  bool used = false;
-};
-
-}  // namespace hs
-
-using namespace hs;
-
-struct hs_ctx {
-  ModelCfg m{};
-  hs_rt_cfg r{};
-  cudaStream_t st = nullptr;
-  KvGeom geom{};
-  // weights
-  bf16 *w_embed = nullptr, *w_lm = nullptr;
-  float* w_final = nullptr;
-  std::vector<bf16*> w_qkv, w_o, w_gu, w_down;
-  std::vector<float*> n_in, n_post;
-  std::vector<CUtensorMap> m_qkv, m_o, m_gu, m_down;
-  CUtensorMap m_lm{};
-  // kv
-  bf16* kv_pool = nullptr;
-  CUtensorMap m_kv{};
-  int* page_table = nullptr;
-  // activations
-  float* h = nullptr;      // residual stream [max_rows][d]
-  float* hr = nullptr;     // restart rows [max_rows][d]
-  ActBuf xn, xn2, attn, act, lin, xr;
-  bf16* qbuf = nullptr;
-  float* part = nullptr;
-  size_t part_floats = 0;
-  float *o_part = nullptr, *lse_part = nullptr;
-  float* resid = nullptr;  // device residual store [max_slots][d]
-  int* last_token = nullptr;
-  int* tok = nullptr;
-  int* tok_out = nullptr;
-  float *rope_cos = nullptr, *rope_sin = nullptr;
-  float* logits = nullptr;  // optional debug copy of the last LM-head logits
-  bool keep_logits = false;
-  // metadata (device) and pinned staging
-  int* dm = nullptr;   // iteration + layer metadata
-  int* hm = nullptr;   // pinned staging (two halves), mapped
-  int* hm_d = nullptr;  // its device alias (zero-copy layer metadata)
-  size_t meta_ints = 0;
-  int stage_half = 0;
-  size_t stage_pos = 0;
-  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
-  // iteration state; pointers into the packed per-iteration device block
-  int B = 0, D = 0, n_chunks = 0, n_tiles = 0, n_logit = 0, n_tok_out = 0, merges_L = 0;
-  int* dm_iter = nullptr;   // packed iteration metadata (one upload per iteration)
-  int* dm_layer = nullptr;  // packed layer metadata (one upload per layer)
-  size_t iter_cap = 0, layer_cap = 0;
-  const int *it_slot = nullptr, *it_pos = nullptr, *it_tok = nullptr, *it_chunks = nullptr,
-            *it_cbeg = nullptr, *it_tiles = nullptr;
-  std::vector<int> h_logit_rows, h_logit_slots;  // host copies (layer-L gather lists)
-  int* dec_counters = nullptr;
-  int* tile_sem = nullptr;  // stream-K fixup semaphores of the fused GEMMs
-  // tensor parallelism (hs_tp_*): this rank's exchange buffer and flags, the
-  // group's pointers, the exchange counter and the IPC mappings to close
-  int tp_world = 1, tp_rank = 0;
-  float* tp_xbuf = nullptr;
-  unsigned* tp_flag = nullptr;
-  TpPeers tp{};
-  unsigned tp_epoch = 0;
-  std::vector<void*> tp_opened;
-  int* tokens_pinned = nullptr;
-  // piggyback mailboxes (pinned, mapped)
-  bf16 *ship_h = nullptr, *ship_d = nullptr, *result_h = nullptr, *result_d = nullptr;
-  // completion tags of the result mailbox (one per slot, written by the CPU
-  // workers) and the device fault record (hs_layer_desc.merge_tag checks)
-  unsigned *tag_h = nullptr, *tag_d = nullptr, *fault_h = nullptr, *fault_d = nullptr;
-  // host KV arena (pinned, mapped)
-  bf16 *hkv_h = nullptr, *hkv_d = nullptr;
-  size_t hkv_bytes = 0;
-  std::vector<HostRegion> regions;
-  std::vector<std::pair<size_t, size_t>> free_list;  // (offset, bytes)
-  ThreadPool* pool = nullptr;
-  std::vector<int> cpus;  // the replica's CPU-attention core set (empty: unpinned)
-  CpuService* cpu = nullptr;
-  // swaps: copy stream + contiguous staging for pack/unpack around one 2D DMA
-  cudaStream_t copy_st = nullptr;
-  bf16* swap_stage = nullptr;
-  size_t swap_stage_elems = 0;
-  std::map<int, cudaEvent_t> swap_ev;
-  int next_ticket = 1;
-  // asynchronous iteration completion: ring of pinned token buffers + events
-  static constexpr int kIterRing = 8;
-  int* tok_ring = nullptr;  // pinned [kIterRing][2*max_rows]
-  cudaEvent_t iter_ev[kIterRing] = {};
-  int iter_n[kIterRing] = {};
-  int next_iter = 0;
-  cudaEvent_t anchor = nullptr;
-  // marks (pacing) and timing events on the compute stream
-  std::vector<cudaEvent_t> marks, timers;
-  int next_mark = 0, next_timer = 0;
-  // per-kernel-class profiling (class, start, stop, bytes, flops)
-  bool prof_on = false;
-  struct Rec { int cls; cudaEvent_t a, b; double bytes, flops; };
-  std::vector<Rec> prof_pending;
-  std::vector<cudaEvent_t> prof_free;
-  double prof_stats[4][4] = {};
-  double dec_kv_tokens = 0, pre_units = 0, pre_kv_tokens = 0;
-};
+#include "hs_ctx.h"
 
 namespace {
 
@@ -421,6 +302,17 @@ __global__ void init_normal_kernel(bf16* w, size_t n, uint64_t seed, float std) 
   }
 }
 
+__global__ void init_normal_f32_kernel(float* w, size_t n, uint64_t seed, float std) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint64_t a = mix64(seed ^ (i * 2 + 0x1234567ull));
+    const uint64_t b = mix64(a ^ 0xA5A5A5A5DEADBEEFull);
+    const float u1 = (static_cast<float>(a >> 40) + 1.0f) * (1.0f / 16777217.0f);
+    const float u2 = static_cast<float>(b >> 40) * (1.0f / 16777216.0f);
+    w[i] = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2) * std;
+  }
+}
+
 __global__ void fill_f32_kernel(float* p, size_t n, float v) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -430,14 +322,15 @@ __global__ void fill_f32_kernel(float* p, size_t n, float v) {
 int rope_init(hs_ctx* c) {
   const int half = c->m.hd / 2;
   std::vector<float> cs(static_cast<size_t>(c->r.max_pos) * half), sn(cs.size());
-  std::vector<float> inv(half);
+  // inverse frequencies and angles in float64 (rounded to fp32 once, at the
+  // table): at the 9k-32k positions of BE contexts an fp32 inverse
+  // frequency alone would put ~5e-4 rad of error into the angle
+  std::vector<double> inv(half);
   for (int i = 0; i < half; ++i)
-    inv[i] = static_cast<float>(
-        1.0 / std::pow(static_cast<double>(c->m.theta),
-                       static_cast<double>(static_cast<float>(2 * i) / static_cast<float>(c->m.hd))));
+    inv[i] = 1.0 / std::pow(static_cast<double>(c->m.theta), 2.0 * i / c->m.hd);
   for (int p = 0; p < c->r.max_pos; ++p)
     for (int i = 0; i < half; ++i) {
-      const double a = static_cast<double>(p) * static_cast<double>(inv[i]);
+      const double a = static_cast<double>(p) * inv[i];
       cs[static_cast<size_t>(p) * half + i] = static_cast<float>(std::cos(a));
       sn[static_cast<size_t>(p) * half + i] = static_cast<float>(std::sin(a));
     }
@@ -483,7 +376,13 @@ void free_all(hs_ctx* c) {
   for (auto p : c->w_down) F(p);
   for (auto p : c->n_in) F(p);
   for (auto p : c->n_post) F(p);
-  F(c->kv_pool);
+  if (!c->fp32) F(c->kv_pool);
+  F(c->kv_f32);
+  F(c->fw_embed);
+  F(c->fw_lm);
+  for (auto* v : {&c->fw_qkv, &c->fw_o, &c->fw_gu, &c->fw_down})
+    for (auto p : *v) F(p);
+  for (float* p : {c->fx, c->fx2, c->fattn, c->fact, c->fq, c->flin, c->fxr}) F(p);
   F(c->page_table);
   F(c->h);
   F(c->hr);
@@ -518,6 +417,7 @@ void free_all(hs_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->anchor) cudaEventDestroy(c->anchor);
   if (c->tok_ring) cudaFreeHost(c->tok_ring);
+  if (c->logit_ring) cudaFreeHost(c->logit_ring);
   for (auto e : c->prof_free) cudaEventDestroy(e);
   for (auto& r : c->prof_pending) {
     cudaEventDestroy(r.a);
@@ -555,6 +455,11 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
                mc->rope_theta, mc->norm_eps};
   c->r = *rc;
   const hs_rt_cfg& r = c->r;
+  if (r.precision != HS_PREC_BF16 && r.precision != HS_PREC_FP32)
+    return set_error(HS_E_CONFIG, "precision %d unknown", r.precision);
+  c->fp32 = r.precision == HS_PREC_FP32;
+  c->kv_elem = c->fp32 ? 4 : 2;
+  m.fp32 = c->fp32;
   if (m.d % 128 || m.ffn % 128 || m.vocab % 128 || (m.hd != 64 && m.hd != 128) ||
       m.n_q % m.n_kv || m.n_q / m.n_kv > 16 || (m.n_q * m.hd) % 64 || m.qkv_n() % 128)
     return set_error(HS_E_CONFIG, "model dims unsupported (d/ffn/vocab %% 128, hd 64|128, G<=16)");
@@ -563,44 +468,71 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
     return set_error(HS_E_CONFIG, "runtime capacities must be >= 1");
   CK(cudaSetDevice(r.device));
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
-  // weights
+  // weights (matrices bf16 [out][in], or fp32 in the validation datapath)
   const size_t d = m.d;
-  RC(dalloc(&c->w_embed, static_cast<size_t>(m.vocab) * d));
-  RC(dalloc(&c->w_lm, static_cast<size_t>(m.vocab) * d));
   RC(dalloc(&c->w_final, d));
-  c->w_qkv.assign(m.layers, nullptr);
-  c->w_o.assign(m.layers, nullptr);
-  c->w_gu.assign(m.layers, nullptr);
-  c->w_down.assign(m.layers, nullptr);
   c->n_in.assign(m.layers, nullptr);
   c->n_post.assign(m.layers, nullptr);
   for (int l = 0; l < m.layers; ++l) {
-    RC(dalloc(&c->w_qkv[l], static_cast<size_t>(m.qkv_n()) * d));
-    RC(dalloc(&c->w_o[l], d * m.n_q * m.hd));
-    RC(dalloc(&c->w_gu[l], 2 * static_cast<size_t>(m.ffn) * d));
-    RC(dalloc(&c->w_down[l], d * m.ffn));
     RC(dalloc(&c->n_in[l], d));
     RC(dalloc(&c->n_post[l], d));
   }
-  RC(build_maps(c));
+  if (c->fp32) {
+    RC(dalloc(&c->fw_embed, static_cast<size_t>(m.vocab) * d));
+    RC(dalloc(&c->fw_lm, static_cast<size_t>(m.vocab) * d));
+    for (auto* v : {&c->fw_qkv, &c->fw_o, &c->fw_gu, &c->fw_down}) v->assign(m.layers, nullptr);
+    for (int l = 0; l < m.layers; ++l) {
+      RC(dalloc(&c->fw_qkv[l], static_cast<size_t>(m.qkv_n()) * d));
+      RC(dalloc(&c->fw_o[l], d * m.n_q * m.hd));
+      RC(dalloc(&c->fw_gu[l], 2 * static_cast<size_t>(m.ffn) * d));
+      RC(dalloc(&c->fw_down[l], d * m.ffn));
+    }
+  } else {
+    RC(dalloc(&c->w_embed, static_cast<size_t>(m.vocab) * d));
+    RC(dalloc(&c->w_lm, static_cast<size_t>(m.vocab) * d));
+    c->w_qkv.assign(m.layers, nullptr);
+    c->w_o.assign(m.layers, nullptr);
+    c->w_gu.assign(m.layers, nullptr);
+    c->w_down.assign(m.layers, nullptr);
+    for (int l = 0; l < m.layers; ++l) {
+      RC(dalloc(&c->w_qkv[l], static_cast<size_t>(m.qkv_n()) * d));
+      RC(dalloc(&c->w_o[l], d * m.n_q * m.hd));
+      RC(dalloc(&c->w_gu[l], 2 * static_cast<size_t>(m.ffn) * d));
+      RC(dalloc(&c->w_down[l], d * m.ffn));
+    }
+    RC(build_maps(c));
+  }
   // kv pool
   c->geom = KvGeom{m.layers, r.kv_pages, m.n_kv, m.hd};
-  RC(dalloc(&c->kv_pool, static_cast<size_t>(m.layers) * r.kv_pages * 2 * m.n_kv * kPageTokens *
-                             m.hd));
-  if (make_kv_map(&c->m_kv, c->kv_pool, c->geom)) return set_error(HS_E_CUDA, "kv map failed");
+  const size_t pool_elems =
+      static_cast<size_t>(m.layers) * r.kv_pages * 2 * m.n_kv * kPageTokens * m.hd;
+  if (c->fp32) {
+    RC(dalloc(&c->kv_f32, pool_elems));
+    c->kv_pool = reinterpret_cast<bf16*>(c->kv_f32);  // swaps move it as bytes
+  } else {
+    RC(dalloc(&c->kv_pool, pool_elems));
+    if (make_kv_map(&c->m_kv, c->kv_pool, c->geom)) return set_error(HS_E_CUDA, "kv map failed");
+  }
   RC(dalloc(&c->page_table, static_cast<size_t>(r.max_slots) * r.max_pages_per_req));
   CK(cudaMemset(c->page_table, 0, static_cast<size_t>(r.max_slots) * r.max_pages_per_req * 4));
   // activations
   const size_t R = r.max_rows;
   RC(dalloc(&c->h, R * d));
   RC(dalloc(&c->hr, R * d));
-  RC(make_act(c->xn, r.max_rows, m.d));
-  RC(make_act(c->xn2, r.max_rows, m.d));
-  RC(make_act(c->attn, r.max_rows, m.n_q * m.hd));
-  RC(make_act(c->act, r.max_rows, m.ffn));
-  RC(make_act(c->lin, r.max_rows, m.d));
-  RC(make_act(c->xr, r.max_rows, m.d));
-  RC(dalloc(&c->qbuf, R * m.n_q * m.hd));
+  if (c->fp32) {
+    for (float** p : {&c->fx, &c->fx2, &c->flin, &c->fxr}) RC(dalloc(p, R * d));
+    RC(dalloc(&c->fattn, R * m.n_q * m.hd));
+    RC(dalloc(&c->fq, R * m.n_q * m.hd));
+    RC(dalloc(&c->fact, R * m.ffn));
+  } else {
+    RC(make_act(c->xn, r.max_rows, m.d));
+    RC(make_act(c->xn2, r.max_rows, m.d));
+    RC(make_act(c->attn, r.max_rows, m.n_q * m.hd));
+    RC(make_act(c->act, r.max_rows, m.ffn));
+    RC(make_act(c->lin, r.max_rows, m.d));
+    RC(make_act(c->xr, r.max_rows, m.d));
+    RC(dalloc(&c->qbuf, R * m.n_q * m.hd));
+  }
   const size_t widest = std::max<size_t>(std::max<size_t>(2 * m.ffn, m.vocab), m.qkv_n());
   c->part_floats = std::max<size_t>(R * widest, static_cast<size_t>(16) * 64 * widest);
   RC(dalloc(&c->part, c->part_floats));
@@ -643,8 +575,10 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
   // piggyback mailboxes: pinned host memory mapped into the device space
   const size_t ship_elems = static_cast<size_t>(r.max_slots) * m.qkv_n();
   const size_t res_elems = static_cast<size_t>(r.max_slots) * m.n_q * m.hd;
-  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->ship_h), ship_elems * 2, cudaHostAllocMapped));
-  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->result_h), res_elems * 2, cudaHostAllocMapped));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->ship_h), ship_elems * c->kv_elem,
+                   cudaHostAllocMapped));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->result_h), res_elems * c->kv_elem,
+                   cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->ship_d), c->ship_h, 0));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->result_d), c->result_h, 0));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->tag_h), r.max_slots * sizeof(unsigned),
@@ -682,6 +616,26 @@ bf16* host_region(hs_ctx* c, int slot) {
   return reinterpret_cast<bf16*>(reinterpret_cast<uint8_t*>(c->hkv_h) + c->regions[slot].offset);
 }
 
+// mailbox rows of a slot (bf16 rows, or fp32 rows in the validation datapath)
+bf16* ship_row(hs_ctx* c, int slot) {
+  return reinterpret_cast<bf16*>(reinterpret_cast<uint8_t*>(c->ship_h) +
+                                 static_cast<size_t>(slot) * c->m.qkv_n() * c->kv_elem);
+}
+bf16* result_row(hs_ctx* c, int slot) {
+  return reinterpret_cast<bf16*>(reinterpret_cast<uint8_t*>(c->result_h) +
+                                 static_cast<size_t>(slot) * c->m.n_q * c->m.hd * c->kv_elem);
+}
+size_t region_bytes(const hs_ctx* c, int cap_tokens) {
+  return static_cast<size_t>(cap_tokens) * c->m.layers * 2 * c->m.n_kv * c->m.hd * c->kv_elem;
+}
+// the pool / host-region geometry in bf16 units (an fp32 head row is two
+// bf16-sized halves per element: the swap kernels move bytes)
+KvGeom swap_geom(const hs_ctx* c) {
+  KvGeom g = c->geom;
+  g.head_dim = g.head_dim * c->kv_elem / 2;
+  return g;
+}
+
 // A result row is complete: publish its tag (release: the row's bytes are
 // visible to a reader that acquires the tag, the device included).
 void publish_tag(hs_ctx* c, int slot, int ctx, int layer) {
@@ -711,10 +665,8 @@ int ensure_cpu_service(hs_ctx* c) {
   if (c->cpu) return HS_OK;
   if (c->r.cpu_threads <= 0) return set_error(HS_E_CONFIG, "no CPU attention threads configured");
   c->cpu = make_cpu_service(c->m, c->r.cpu_threads, c->cpus);
-  const int qkv = c->m.qkv_n(), nqh = c->m.n_q * c->m.hd;
   cpu_service_bind(
-      c->cpu, [c, qkv](int s) { return c->ship_h + static_cast<size_t>(s) * qkv; },
-      [c, nqh](int s) { return c->result_h + static_cast<size_t>(s) * nqh; },
+      c->cpu, [c](int s) { return ship_row(c, s); }, [c](int s) { return result_row(c, s); },
       [c](int s) { return host_region(c, s); }, [c](int s) { return c->regions[s].cap; },
       [c](int s, int ctx, int layer) { publish_tag(c, s, ctx, layer); },
       [c](int s) { retract_tag(c, s); });
@@ -731,8 +683,9 @@ int swap_async(hs_ctx* c, int slot, int tokens, bool to_host, int* ticket) {
   if (!hr.used) return set_error(HS_E_INTEGRITY, "slot %d has no host KV region", slot);
   if (tokens > hr.cap) return set_error(HS_E_CAPACITY, "swap of %d tokens exceeds region", tokens);
   const ModelCfg& m = c->m;
+  const KvGeom sg = swap_geom(c);
   const size_t rows = static_cast<size_t>(m.layers) * 2 * m.n_kv;
-  const size_t need = rows * tokens * m.hd;
+  const size_t need = rows * tokens * sg.head_dim;
   if (need > c->swap_stage_elems) {
     CK(cudaStreamSynchronize(c->copy_st));
     if (c->swap_stage) CK(cudaFree(c->swap_stage));
@@ -748,10 +701,10 @@ int swap_async(hs_ctx* c, int slot, int tokens, bool to_host, int* ticket) {
   CK(cudaEventDestroy(dep));
   const int* pages = c->page_table + static_cast<size_t>(slot) * c->r.max_pages_per_req;
   bf16* host = host_region(c, slot);
-  const size_t w = static_cast<size_t>(tokens) * m.hd * 2;
-  const size_t host_pitch = static_cast<size_t>(hr.cap) * m.hd * 2;
+  const size_t w = static_cast<size_t>(tokens) * sg.head_dim * 2;
+  const size_t host_pitch = static_cast<size_t>(hr.cap) * sg.head_dim * 2;
   if (to_host) {
-    RC(kv_swap(true, c->kv_pool, c->geom, pages, tokens, c->swap_stage, tokens, c->copy_st));
+    RC(kv_swap(true, c->kv_pool, sg, pages, tokens, c->swap_stage, tokens, c->copy_st));
     if (tokens > 0)
       CK(cudaMemcpy2DAsync(host, host_pitch, c->swap_stage, w, w, rows, cudaMemcpyDeviceToHost,
                            c->copy_st));
@@ -759,7 +712,7 @@ int swap_async(hs_ctx* c, int slot, int tokens, bool to_host, int* ticket) {
     if (tokens > 0)
       CK(cudaMemcpy2DAsync(c->swap_stage, w, host, host_pitch, w, rows, cudaMemcpyHostToDevice,
                            c->copy_st));
-    RC(kv_swap(false, c->kv_pool, c->geom, pages, tokens, c->swap_stage, tokens, c->copy_st));
+    RC(kv_swap(false, c->kv_pool, sg, pages, tokens, c->swap_stage, tokens, c->copy_st));
   }
   CK(cudaEventRecord(done, c->copy_st));
   *ticket = c->next_ticket++;
@@ -774,7 +727,7 @@ int kv_swap_pages(hs_ctx* c, int slot, int tokens, bool to_host) {
   if (tokens > hr.cap) return set_error(HS_E_CAPACITY, "swap of %d tokens exceeds region", tokens);
   const int* pages = c->page_table + static_cast<size_t>(slot) * c->r.max_pages_per_req;
   bf16* host = reinterpret_cast<bf16*>(reinterpret_cast<uint8_t*>(c->hkv_d) + hr.offset);
-  RC(kv_swap(to_host, c->kv_pool, c->geom, pages, tokens, host, hr.cap, c->st));
+  RC(kv_swap(to_host, c->kv_pool, swap_geom(c), pages, tokens, host, hr.cap, c->st));
   CK(cudaStreamSynchronize(c->st));
   return HS_OK;
 }
@@ -784,6 +737,7 @@ int kv_swap_pages(hs_ctx* c, int slot, int tokens, bool to_host) {
 namespace {
 template <typename F>
 int time_reps(hs_ctx* c, int reps, F&& body, float* us) {
+  if (c->fp32) return set_error(HS_E_CONFIG, "probes time the bf16 serving datapath only");
   std::vector<float> ts;
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
@@ -871,6 +825,22 @@ int hs_set_weight(hs_ctx* c, int kind, int layer, const void* host, size_t bytes
     case HS_W_NORM_POST: dst = c->n_post[layer]; want = d * 4; break;
     default: return set_error(HS_E_CONFIG, "unknown weight kind %d", kind);
   }
+  if (c->fp32 && kind != HS_W_FINAL_NORM && kind != HS_W_NORM_IN && kind != HS_W_NORM_POST) {
+    // validation datapath: fp32 matrices in the caller's [out][in] order
+    float* fdst = nullptr;
+    switch (kind) {
+      case HS_W_EMBED: fdst = c->fw_embed; break;
+      case HS_W_LM_HEAD: fdst = c->fw_lm; break;
+      case HS_W_QKV: fdst = c->fw_qkv[layer]; break;
+      case HS_W_O: fdst = c->fw_o[layer]; break;
+      case HS_W_GATE_UP: fdst = c->fw_gu[layer]; break;
+      default: fdst = c->fw_down[layer]; break;
+    }
+    if (bytes != 2 * want)
+      return set_error(HS_E_CONFIG, "fp32 weight %d: %zu bytes, want %zu", kind, bytes, 2 * want);
+    CK(cudaMemcpy(fdst, host, bytes, cudaMemcpyHostToDevice));
+    return HS_OK;
+  }
   if (bytes != want) return set_error(HS_E_CONFIG, "weight %d: %zu bytes, want %zu", kind, bytes, want);
   if (kind == HS_W_QKV || kind == HS_W_GATE_UP) {
     // rows reordered for the fused epilogues (see permute_rows)
@@ -898,6 +868,26 @@ int hs_init_weights(hs_ctx* c, uint64_t seed, float std) {
     s = s * 6364136223846793005ull + 1442695040888963407ull;
   };
   auto ones = [&](float* p, size_t n) { fill_f32_kernel<<<64, 256, 0, c->st>>>(p, n, 1.0f); };
+  if (c->fp32) {
+    auto initf = [&](float* p, size_t n) {
+      init_normal_f32_kernel<<<148 * 8, 256, 0, c->st>>>(p, n, s, std);
+      s = s * 6364136223846793005ull + 1442695040888963407ull;
+    };
+    initf(c->fw_embed, static_cast<size_t>(m.vocab) * d);
+    initf(c->fw_lm, static_cast<size_t>(m.vocab) * d);
+    ones(c->w_final, d);
+    for (int l = 0; l < m.layers; ++l) {
+      initf(c->fw_qkv[l], static_cast<size_t>(m.qkv_n()) * d);
+      initf(c->fw_o[l], d * m.n_q * m.hd);
+      initf(c->fw_gu[l], 2 * static_cast<size_t>(m.ffn) * d);
+      initf(c->fw_down[l], d * m.ffn);
+      ones(c->n_in[l], d);
+      ones(c->n_post[l], d);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->st));
+    return HS_OK;
+  }
   init(c->w_embed, static_cast<size_t>(m.vocab) * d);
   init(c->w_lm, static_cast<size_t>(m.vocab) * d);
   ones(c->w_final, d);
@@ -930,8 +920,23 @@ int hs_set_page_table(hs_ctx* c, int slot, const int* pages, int n) {
 
 int hs_keep_logits(hs_ctx* c, int on) {
   c->keep_logits = on != 0;
-  if (c->keep_logits && !c->logits)
-    RC(dalloc(&c->logits, static_cast<size_t>(2 * c->r.max_rows) * c->m.vocab));
+  const size_t per_iter = static_cast<size_t>(2 * c->r.max_rows) * c->m.vocab;
+  if (c->keep_logits && !c->logits) RC(dalloc(&c->logits, per_iter));
+  if (c->keep_logits && !c->logit_ring)
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&c->logit_ring),
+                     sizeof(float) * hs_ctx::kIterRing * per_iter, cudaHostAllocDefault));
+  return HS_OK;
+}
+
+int hs_iter_logits(hs_ctx* c, int ticket, float* host, int rows) {
+  if (!c->logit_ring) return set_error(HS_E_CONFIG, "logits not kept (hs_keep_logits)");
+  if (ticket < c->next_iter - hs_ctx::kIterRing || ticket >= c->next_iter)
+    return set_error(HS_E_CONFIG, "iteration ticket %d out of window", ticket);
+  const int slot = ticket % hs_ctx::kIterRing;
+  if (rows > c->iter_n[slot]) return set_error(HS_E_CONFIG, "only %d logit rows", c->iter_n[slot]);
+  CK(cudaEventSynchronize(c->iter_ev[slot]));
+  const size_t per_iter = static_cast<size_t>(2 * c->r.max_rows) * c->m.vocab;
+  std::memcpy(host, c->logit_ring + slot * per_iter, sizeof(float) * rows * c->m.vocab);
   return HS_OK;
 }
 
@@ -948,7 +953,7 @@ int hs_host_kv_reserve(hs_ctx* c, int slot, int cap_tokens) {
   if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
   HostRegion& hr = c->regions[slot];
   if (hr.used) return set_error(HS_E_INTEGRITY, "slot %d already holds a host KV region", slot);
-  const size_t bytes = static_cast<size_t>(cap_tokens) * c->m.layers * 2 * c->m.n_kv * c->m.hd * 2;
+  const size_t bytes = region_bytes(c, cap_tokens);
   for (size_t i = 0; i < c->free_list.size(); ++i) {
     auto& f = c->free_list[i];
     if (f.second >= bytes) {
@@ -968,7 +973,7 @@ int hs_host_kv_release(hs_ctx* c, int slot) {
   if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
   HostRegion& hr = c->regions[slot];
   if (!hr.used) return HS_OK;
-  const size_t bytes = static_cast<size_t>(hr.cap) * c->m.layers * 2 * c->m.n_kv * c->m.hd * 2;
+  const size_t bytes = region_bytes(c, hr.cap);
   c->free_list.push_back({hr.offset, bytes});
   std::sort(c->free_list.begin(), c->free_list.end());
   std::vector<std::pair<size_t, size_t>> merged;
@@ -1130,6 +1135,9 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
     HProf hp(HP_PACK);
     RC(pk.flush(st));
   }
+  if (c->fp32)
+    return layer_f32(c, d, LayerRows{carry_slot, carry_pos, merge_slot, restart_slot, restart_pos,
+                                      logit_rows, logit_slots, merge_tag});
   if (l == 0) {
     // embed batch rows (+ injected chains: fresh token from last_token)
     RC(select_tokens(c->it_tok, c->it_slot, B, carry_slot, c->last_token, B + C, c->tok, st));
@@ -1309,6 +1317,7 @@ int hs_tp_export(hs_ctx* c, void* handles) {
 }
 
 int hs_tp_open(hs_ctx* c, int rank, int world, const void* all_handles) {
+  if (c->fp32) return set_error(HS_E_CONFIG, "tensor parallelism runs the bf16 datapath only");
   if (world < 1 || world > kMaxTp || rank < 0 || rank >= world)
     return set_error(HS_E_CONFIG, "tensor-parallel rank %d of %d out of range", rank, world);
   RC(tp_alloc(c));
@@ -1372,6 +1381,10 @@ int hs_iter_end_async(hs_ctx* c, int* ticket) {
   if (c->n_tok_out > 0)
     CK(cudaMemcpyAsync(dst, c->tok_out, c->n_tok_out * sizeof(int), cudaMemcpyDeviceToHost,
                        c->st));
+  if (c->keep_logits && c->logit_ring && c->n_tok_out > 0)
+    CK(cudaMemcpyAsync(c->logit_ring + slot * static_cast<size_t>(2 * c->r.max_rows) * c->m.vocab,
+                       c->logits, sizeof(float) * c->n_tok_out * c->m.vocab,
+                       cudaMemcpyDeviceToHost, c->st));
   CK(cudaEventRecord(c->iter_ev[slot], c->st));
   c->iter_n[slot] = c->n_tok_out;
   *ticket = id;
@@ -1423,11 +1436,8 @@ int hs_cpu_attend(hs_ctx* c, const int* slots, const int* layers, const int* ctx
   c->pool->parallel_for(n * m.n_kv, [&](int task) {
     const int i = task / m.n_kv, h = task % m.n_kv;
     const int s = slots[i];
-    const HostRegion& hr = c->regions[s];
-    bf16* hkv = reinterpret_cast<bf16*>(reinterpret_cast<uint8_t*>(c->hkv_h) + hr.offset);
-    cpu_attend_head(m, c->ship_h + static_cast<size_t>(s) * m.qkv_n(), hkv, hr.cap,
-                    layers[i] - 1, ctxs[i], h, c->result_h + static_cast<size_t>(s) * m.n_q * m.hd,
-                    nullptr);
+    cpu_attend_head(m, ship_row(c, s), host_region(c, s), c->regions[s].cap, layers[i] - 1,
+                    ctxs[i], h, result_row(c, s), nullptr);
   });
   for (int i = 0; i < n; ++i) publish_tag(c, slots[i], ctxs[i], layers[i]);
   return HS_OK;
@@ -1727,8 +1737,18 @@ int hs_sync(hs_ctx* c) {
 
 int hs_read_ship(hs_ctx* c, int slot, void* host, size_t bytes) {
   CK(cudaStreamSynchronize(c->st));
-  if (bytes != static_cast<size_t>(c->m.qkv_n()) * 2) return set_error(HS_E_CONFIG, "size");
-  std::memcpy(host, c->ship_h + static_cast<size_t>(slot) * c->m.qkv_n(), bytes);
+  if (slot < 0 || slot >= c->r.max_slots || bytes != static_cast<size_t>(c->m.qkv_n()) * c->kv_elem)
+    return set_error(HS_E_CONFIG, "ship row: slot %d / %zu bytes", slot, bytes);
+  std::memcpy(host, ship_row(c, slot), bytes);
+  return HS_OK;
+}
+
+int hs_read_result(hs_ctx* c, int slot, void* host, size_t bytes) {
+  CK(cudaStreamSynchronize(c->st));
+  if (slot < 0 || slot >= c->r.max_slots ||
+      bytes != static_cast<size_t>(c->m.n_q) * c->m.hd * c->kv_elem)
+    return set_error(HS_E_CONFIG, "result row: slot %d / %zu bytes", slot, bytes);
+  std::memcpy(host, result_row(c, slot), bytes);
   return HS_OK;
 }
 

@@ -40,8 +40,13 @@ from .workload import build_requests
 
 class LiveEngine(Engine):
     def __init__(self, scenario, models=None, step=None, pace_layers: int = 1,
-                 pace_tail: int = 0):
+                 pace_tail: int = 0, batch_trace: bool = False):
         super().__init__(scenario, models=models, step=step)
+        # realised batch composition, per iteration: the plan's rows, every
+        # layer's merges with their outcomes, and the request state each call
+        # saw (the replay input of the oracle; cf. the reference's decision
+        # audit and module traces, engine.py:305-319, 975-980)
+        self.batch_trace: Optional[list[dict]] = [] if batch_trace else None
         self.t0 = time.perf_counter()
         self.pace_layers = pace_layers
         # the last `pace_tail` layers of an iteration are launched without
@@ -97,6 +102,14 @@ class LiveEngine(Engine):
         super()._complete(req, t)
         if self._collect is not None:
             self._collect.append((req, -1))
+
+    def _snap(self, rids) -> dict:
+        out = {}
+        for rid in rids:
+            r = self.requests[rid]
+            out[rid] = (r.ctx, r.prompt_len, r.output_len, r.prefill_done, r.rebuild_tokens,
+                        r.phase)
+        return out
 
     # -- async completions ---------------------------------------------------------
 
@@ -159,6 +172,16 @@ class LiveEngine(Engine):
                             merge_layers={})
         self._iter = it
         self._collect = []
+        trace = None
+        if self.batch_trace is not None:
+            rows = [r for r in plan.ls_decode + plan.be_decode_gpu] + \
+                   [r for r, _ in plan.ls_prefill_chunks + plan.be_prefill_chunks]
+            trace = {"plan": {"ls_decode": list(plan.ls_decode),
+                              "be_decode_gpu": list(plan.be_decode_gpu),
+                              "ls_prefill_chunks": list(plan.ls_prefill_chunks),
+                              "be_prefill_chunks": list(plan.be_prefill_chunks)},
+                     "snap": self._snap(rows), "layers": []}
+            self.batch_trace.append(trace)
         self.step.begin_iteration(plan)
         for layer in range(1, self.layers + 1):
             it.layer = layer
@@ -176,6 +199,9 @@ class LiveEngine(Engine):
                 self.counters["merges"] += len(merged)
             outcomes = [(item, self._process_merge(item, layer, start, start))
                         for item in merged]
+            if trace is not None:
+                trace["layers"].append((layer, [(i.req_id, o) for i, o in outcomes],
+                                        self._snap([i.req_id for i in merged])))
             self._submit_shipped(self.step.layer(layer, outcomes))
             self.host_s["issue"] += time.perf_counter() - t_i
             if self.opts.record_layer_times:

@@ -51,7 +51,9 @@ class HsRtCfg(C.Structure):
     _fields_ = [("max_rows", C.c_int), ("max_slots", C.c_int), ("kv_pages", C.c_int),
                 ("max_pages_per_req", C.c_int), ("max_pos", C.c_int), ("max_chunks", C.c_int),
                 ("cpu_threads", C.c_int), ("host_kv_bytes", C.c_int64), ("device", C.c_int),
-                ("cpu_list", _IP), ("n_cpu_list", C.c_int)]
+                ("cpu_list", _IP), ("n_cpu_list", C.c_int), ("precision", C.c_int)]
+
+PRECISIONS = {"bf16": 0, "fp32": 1}  # HS_PREC_BF16 / HS_PREC_FP32 (include/hs.h)
 
 
 class HsIterDesc(C.Structure):
@@ -95,7 +97,9 @@ _CTX_SIGS = {
     "hs_sync": [C.c_void_p],
     "hs_keep_logits": [C.c_void_p, C.c_int],
     "hs_read_logits": [C.c_void_p, C.c_void_p, C.c_int],
+    "hs_iter_logits": [C.c_void_p, C.c_int, C.c_void_p, C.c_int],
     "hs_read_ship": [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t],
+    "hs_read_result": [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t],
     "hs_read_residual": [C.c_void_p, C.c_int, C.c_void_p],
     "hs_cpu_submit": [C.c_void_p, _IP, _IP, _IP, C.c_int],
     "hs_cpu_poll": [C.c_void_p, _IP, _IP, C.c_void_p, C.c_int],
@@ -137,6 +141,9 @@ class RuntimeConfig:
     host_kv_bytes: int = 1 << 30
     device: int = 0
     cpu_list: tuple = ()  # the replica's CPU-attention cores (replicas.core_set)
+    # "bf16" serving datapath, or "fp32" validation datapath (fp32 weights,
+    # activations, KV, piggyback mailboxes and host attention; SIMT kernels)
+    precision: str = "bf16"
 
 
 class HsContext:
@@ -167,9 +174,14 @@ class HsContext:
         mc = HsModelCfg(model.d_model, model.n_layers, model.n_q, model.n_kv, model.head_dim,
                         model.ffn, model.vocab, model.rope_theta, model.norm_eps)
         cpus = np.asarray(rt.cpu_list or [], np.int32)
+        if rt.precision not in PRECISIONS:
+            from .errors import ConfigError
+
+            raise ConfigError(f"precision {rt.precision!r} (choose from {sorted(PRECISIONS)})")
         rc = HsRtCfg(rt.max_rows, rt.max_slots, rt.kv_pages, rt.max_pages_per_req, rt.max_pos,
                      rt.max_chunks, rt.cpu_threads, rt.host_kv_bytes, rt.device,
-                     cpus.ctypes.data_as(_IP) if len(cpus) else None, len(cpus))
+                     cpus.ctypes.data_as(_IP) if len(cpus) else None, len(cpus),
+                     PRECISIONS[rt.precision])
         h = C.c_void_p()
         _lib.check(lib.hs_create(C.byref(mc), C.byref(rc), C.byref(h)), "hs_create")
         self.h = h
@@ -207,9 +219,9 @@ class HsContext:
         self._call("hs_init_weights", seed, std)
 
     def load_weights(self, w: dict) -> None:
-        """w: numpy weights (bf16 bit patterns as uint16 for matrices, fp32
-        norms) in the layout of oracle/weights (embed, lm_head, final_norm,
-        and per-layer lists)."""
+        """w: numpy weights (bf16 bit patterns as uint16 for matrices, or
+        fp32 matrices for the fp32 datapath; fp32 norms): embed, lm_head,
+        final_norm, and per-layer lists."""
         self.set_weight(W_EMBED, 0, w["embed"])
         self.set_weight(W_LM_HEAD, 0, w["lm_head"])
         self.set_weight(W_FINAL_NORM, 0, w["final_norm"])
@@ -328,6 +340,12 @@ class HsContext:
     def read_logits(self, rows: int) -> np.ndarray:
         out = np.zeros((rows, self.model.vocab), np.float32)
         self._call("hs_read_logits", out.ctypes.data_as(C.c_void_p), rows)
+        return out
+
+    def iter_logits(self, ticket: int, rows: int) -> np.ndarray:
+        out = np.zeros((rows, self.model.vocab), np.float32)
+        if rows:
+            self._call("hs_iter_logits", ticket, out.ctypes.data_as(C.c_void_p), rows)
         return out
 
 
@@ -625,6 +643,10 @@ class LiveCudaStep(CudaStep):
         # out first by the next poll_iterations()
         self._drained: list = []
         self.anchor_wall = 0.0
+        # per finished iteration, in order: (request ids, greedy tokens, logits
+        # or None) -- the realised token stream, kept when trace_tokens is set
+        self.trace_tokens = False
+        self.token_log: list[tuple[list[str], np.ndarray, Optional[np.ndarray]]] = []
 
     def set_anchor(self, wall: float) -> None:
         """Device events are reported relative to this host time."""
@@ -673,6 +695,9 @@ class LiveCudaStep(CudaStep):
             self._inflight.pop(0)
             if len(toks) != len(reqs):
                 raise RuntimeError(f"libhs returned {len(toks)} tokens for {len(reqs)} rows")
+            if self.trace_tokens:
+                lg = self.ctx.iter_logits(ticket, len(toks)) if self.keep else None
+                self.token_log.append((list(reqs), toks.copy(), lg))
             self.d2h_bytes += 4 * len(toks)
             for rid, t in zip(reqs, toks):
                 self.generated.setdefault(rid, []).append(int(t))

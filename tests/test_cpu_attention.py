@@ -75,3 +75,22 @@ def test_host_attention_without_amx_matches_oracle():
                          env={**os.environ, "HS_CPU_AMX": "0"}, timeout=120)
     assert out.returncode == 0, out.stderr
     assert float(out.stdout.strip().splitlines()[-1]) < 1.5e-2
+
+
+@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("keys", [9000, 32769])
+def test_host_attention_long_context(impl, keys):
+    """C1 at the bench's BE context (~9k keys, AMX QK^T + prefetch path) and at
+    config 5's 32k-token prompts, Llama-3-8B geometry."""
+    if impl == 1 and not _has_avx512bf16():
+        pytest.skip("no AVX-512-BF16 on this host")
+    n_q, n_kv, hd = 32, 8, 128
+    rng = np.random.default_rng(keys + impl)
+    q = O.to_bf16((rng.standard_normal((n_q, hd)) * 0.3).astype(np.float32))
+    k = O.to_bf16(rng.standard_normal((n_kv, keys, hd)).astype(np.float32))
+    v = O.to_bf16(rng.standard_normal((n_kv, keys, hd)).astype(np.float32))
+    got, lse = _run(q, k, v, n_q, n_kv, hd, impl)
+    ref, ref_lse = O.decode_attention(q, k.transpose(1, 0, 2), v.transpose(1, 0, 2), n_kv)
+    err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-6)
+    assert err < 1.5e-2, err
+    assert np.abs(lse - ref_lse).max() < 1e-2

@@ -1,0 +1,142 @@
+"""Parity of the live serving path — the path `bench.py` measures.
+
+`LiveEngine` + `LiveCudaStep` run config 1 (tiny Llama, the Appendix-B
+workload: 8 LS + 32 BE, BE KV pushed to host DRAM by the 1000-token GPU KV
+budget) on the wall clock with everything the bench uses: the asynchronous
+CPU-attention pool (hs_cpu_submit/poll), asynchronous swaps on the copy
+stream, pipelined iterations (hs_iter_end_async) and launch pacing.  The
+engine records the realised schedule (per-iteration rows, per-layer merges
+with outcomes); the GPU records its tokens and logits.  The oracle then
+replays exactly that schedule (oracle/replay.py) and every token is compared:
+logits within 2e-2 relative (north star), greedy tokens equal except at
+near-ties of the oracle's logits.  Reference: engine.py:879-1047 (iteration),
+902-919 (merges), 512-560 (CPU service), 402-508 (swaps).
+"""
+
+import copy
+
+import numpy as np
+import pytest
+
+from oracle.replay import replay
+from oracle.scenarios import APPENDIX_B
+from oracle.serve_oracle import device_weights, make_weights
+
+LOGIT_REL_TOL = 2e-2
+
+
+def _live_run(pace_layers=1, pace_tail=0, cpu_threads=4):
+    from paper_2603_12831_b200.live import LiveEngine
+    from paper_2603_12831_b200.models import TRANSFORMERS
+    from paper_2603_12831_b200.runtime import LiveCudaStep, RuntimeConfig
+    from paper_2603_12831_b200.scenario import scenario_from_dict
+
+    cfg = TRANSFORMERS["tiny"]
+    w = make_weights(cfg, 0)
+    rt = RuntimeConfig(max_rows=1024, max_slots=64, kv_pages=256, max_pages_per_req=16,
+                       max_pos=2048, max_chunks=1024, cpu_threads=cpu_threads,
+                       host_kv_bytes=256 << 20)
+    step = LiveCudaStep(cfg, rt, weights=device_weights(w), keep_logits=True)
+    step.trace_tokens = True
+    doc = copy.deepcopy(APPENDIX_B)
+    eng = LiveEngine(scenario_from_dict(doc, "live_b"), step=step, pace_layers=pace_layers,
+                     pace_tail=pace_tail, batch_trace=True)
+    n = eng.run_live(horizon_s=30.0)
+    step.finish()
+    return cfg, w, eng, step, n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pace_layers,pace_tail", [(1, 0), (2, 1)])
+def test_live_engine_matches_oracle_replay(cuda, pace_layers, pace_tail):
+    from paper_2603_12831_b200.runtime import prompt_tokens
+
+    cfg, w, eng, step, n = _live_run(pace_layers, pace_tail)
+    c = eng.counters
+    assert n > 100 and c["tokens_total"] > 1000, (n, c)
+    # the async machinery the bench relies on was exercised
+    assert c["swap_out_done"] > 0 and c["injections"] > 0, c
+    assert c["merges"] > 0 and c["be_tokens_cpu"] > 0, c
+    st = replay(eng.batch_trace, step.token_log, cfg, w,
+                lambda rid, k: prompt_tokens(rid, k, cfg.vocab, 0))
+    assert st.merges == c["merges"]
+    assert st.compared == c["tokens_total"], (st.compared, c["tokens_total"])
+    assert st.logits_compared == st.compared
+    assert not st.bad, st.bad[:5]
+    assert st.max_rel < LOGIT_REL_TOL, st.max_rel
+    assert st.ties <= 0.05 * st.compared
+    print(f"live: iterations={n} tokens={st.compared} merges={st.merges} "
+          f"cpu_tokens={c['be_tokens_cpu']} swaps={c['swap_out_done']} "
+          f"max_rel={st.max_rel:.2e} ties={st.ties}")
+
+
+class _TraceOracle:
+    """Virtual-clock stand-in for LiveEngine(batch_trace)+LiveCudaStep(trace_tokens):
+    an OracleStep whose schedule and tokens are recorded in the same format."""
+
+    def __init__(self, ora):
+        self.ora = ora
+        self.trace, self.token_log = [], []
+
+    def attach(self, engine):
+        self.engine = engine
+        self.ora.attach(engine)
+
+    def _snap(self, rids):
+        out = {}
+        for rid in rids:
+            r = self.engine.requests[rid]
+            out[rid] = (r.ctx, r.prompt_len, r.output_len, r.prefill_done, r.rebuild_tokens,
+                        r.phase)
+        return out
+
+    def begin_iteration(self, plan):
+        rows = plan.ls_decode + plan.be_decode_gpu + [
+            r for r, _ in plan.ls_prefill_chunks + plan.be_prefill_chunks]
+        self.trace.append({"plan": {k: list(getattr(plan, k)) for k in (
+            "ls_decode", "be_decode_gpu", "ls_prefill_chunks", "be_prefill_chunks")},
+            "snap": self._snap(rows), "layers": []})
+        self._n = len(self.ora.logit_log)
+        self.ora.begin_iteration(plan)
+
+    def layer(self, layer, merges):
+        self.trace[-1]["layers"].append((layer, [(i.req_id, o) for i, o in merges],
+                                         self._snap([i.req_id for i, _ in merges])))
+        self.ora.layer(layer, merges)
+
+    def end_iteration(self, plan):
+        self.ora.end_iteration(plan)
+        em = self.ora.logit_log[self._n:]
+        self.token_log.append(([r for r, _ in em],
+                               np.array([self.ora.generated[r][-1] for r, _ in em]),
+                               np.stack([lg for _, lg in em]) if em else None))
+
+    def cpu_service(self, host_id, items):
+        self.ora.cpu_service(host_id, items)
+
+    def __getattr__(self, name):  # swaps / release: no numerics
+        return lambda *a, **k: None
+
+
+@pytest.mark.parametrize("horizon", [1.35])
+def test_replay_reproduces_a_recorded_oracle_run(horizon):
+    """CPU-only check of the replay itself: an oracle run recorded in the live
+    trace format replays bit-exactly (same tokens, zero logit error)."""
+    from oracle.serve_oracle import OracleStep
+    from paper_2603_12831_b200.engine import Engine
+    from paper_2603_12831_b200.models import TRANSFORMERS
+    from paper_2603_12831_b200.runtime import prompt_tokens
+    from paper_2603_12831_b200.scenario import scenario_from_dict
+
+    cfg = TRANSFORMERS["tiny"]
+    w = make_weights(cfg, 0)
+    pf = lambda rid, k: prompt_tokens(rid, k, cfg.vocab, 0)  # noqa: E731
+    rec = _TraceOracle(OracleStep(cfg, w, pf))
+    doc = copy.deepcopy(APPENDIX_B)
+    doc["horizon_s"] = horizon
+    report = Engine(scenario_from_dict(doc, "b"), step=rec).run()
+    c = report.counters
+    assert c["merges"] > 0 and c["be_tokens_cpu"] > 0
+    st = replay(rec.trace, rec.token_log, cfg, w, pf)
+    assert st.compared == c["tokens_total"] and st.merges == c["merges"]
+    assert st.max_rel == 0.0 and st.ties == 0 and not st.bad

@@ -369,3 +369,41 @@ def test_silu_mul_shapes(cuda, rows, ffn, splits):
     _lib.call("hs_op_silu_mul", _p(_t(gu, cuda)), splits, rows, ffn, _p(act), ffn, None)
     torch.cuda.synchronize()
     assert _rel(act.float().cpu().numpy(), O.silu_mul(gu.sum(0), ffn)) < 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ctxs", [[9000, 700, 9001], [32768, 1]])
+def test_decode_attention_long_context(cuda, ctxs):
+    """K1+K2 at the bench's and config 5's context lengths, split exactly as
+    the runtime splits them (runtime.decode_chunks).  Logical pages map onto
+    a small physical pool with repeats, so 32k-token rows stay cheap to build
+    while every page load goes through the page table."""
+    import torch
+    from paper_2603_12831_b200 import _lib
+    from paper_2603_12831_b200.runtime import decode_chunks
+
+    n_q, n_kv, hd = 32, 8, 128
+    rng = np.random.default_rng(sum(ctxs))
+    pages = 96
+    pool = _make_pool(rng, 1, pages, n_kv, hd)
+    max_pages = max((c + 63) // 64 for c in ctxs)
+    pt = rng.integers(0, pages, size=(len(ctxs), max_pages)).astype(np.int32)
+    q = _bf16_np(rng, (len(ctxs), n_q, hd))
+    chunks, begin = decode_chunks(ctxs, n_kv)
+    chunks = np.array([(r, r, p0, p1, c) for r, _, p0, p1, c in chunks], np.int32)
+    dpool, dq = _t(pool, cuda, torch.bfloat16), _t(q, cuda, torch.bfloat16)
+    dpt, dch = _t(pt, cuda), _t(chunks, cuda)
+    dbeg = _t(np.array(begin, np.int32), cuda)
+    cnt = torch.zeros(len(ctxs) * n_kv, dtype=torch.int32, device=cuda)
+    opart = torch.zeros(len(chunks) * n_q * hd, dtype=torch.float32, device=cuda)
+    lpart = torch.zeros(len(chunks) * n_q, dtype=torch.float32, device=cuda)
+    out = torch.zeros(len(ctxs), n_q * hd, dtype=torch.bfloat16, device=cuda)
+    _lib.call("hs_op_decode_attention_fused", _p(dpool), 1, pages, n_kv, hd, 0, _p(dq),
+              n_q * hd, n_q, _p(dpt), max_pages, _p(dch), len(chunks), _p(dbeg), _p(opart),
+              _p(lpart), _p(cnt), _p(out), n_q * hd, None)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy().reshape(len(ctxs), n_q, hd)
+    for r, c in enumerate(ctxs):
+        k, v = _gather_kv(pool, 0, pt[r, :(c + 63) // 64], c)
+        ref, _ = O.decode_attention(q[r], k, v, n_kv)
+        assert _rel(got[r], ref) < 1.5e-2, (r, c, _rel(got[r], ref))
