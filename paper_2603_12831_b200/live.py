@@ -71,6 +71,7 @@ class LiveEngine(Engine):
         # host-time accounting (seconds): planning, layer issue, waiting on
         # the GPU in pace(); the bench reports it to tell host- from GPU-bound
         self.host_s = {"plan": 0.0, "issue": 0.0, "pace_wait": 0.0}
+        self.stalled = False
 
     def clock(self) -> float:
         return time.perf_counter() - self.t0
@@ -280,8 +281,17 @@ class LiveEngine(Engine):
                     if on_iteration:
                         on_iteration(n)
                     continue
-            if idle_exit and not arrivals and not self._submitted and not self._swaps \
-                    and not self._swapin_wait and not self._runnable():
+            quiet = (not arrivals and not self._submitted and not self._swaps
+                     and not self._swapin_wait)
+            if idle_exit and quiet and not self._runnable():
+                break
+            if quiet and not self._dirty and not self.step.iterations_in_flight():
+                # the last plan had no work and nothing can change the state
+                # any more (no arrival, CPU item, swap or iteration pending):
+                # the policy is wedged, e.g. GPU KV held by partial prefills
+                # (the reference's event loop simply runs out of events here,
+                # engine.py:1065-1088)
+                self.stalled = True
                 break
             time.sleep(2e-5)
         self._resolve_iterations(block=True)

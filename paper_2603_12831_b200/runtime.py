@@ -416,10 +416,13 @@ class CudaStep(LayerStep):
 
     def __init__(self, model: TransformerConfig, rt: Optional[RuntimeConfig] = None,
                  weights: Optional[dict] = None, weight_seed: int = 0, prompt_seed: int = 0,
-                 keep_logits: bool = False):
+                 keep_logits: bool = False, ctx=None):
         self.model = model
         self.rt = rt or RuntimeConfig()
-        self.ctx = HsContext(model, self.rt)
+        # `ctx` lets the CPU test suite drive the host logic against a
+        # recording stand-in (tests/fake_device.py); serving always builds
+        # the libhs context
+        self.ctx = ctx if ctx is not None else HsContext(model, self.rt)
         if weights is not None:
             self.ctx.load_weights(weights)
         else:
@@ -670,6 +673,9 @@ class LiveCudaStep(CudaStep):
         ticket = self.ctx.iter_end_async()
         self._inflight.append((ticket, self._logit_reqs + self._merge_L, payload))
         self.iterations += 1
+
+    def iterations_in_flight(self) -> int:
+        return len(self._inflight) + len(self._drained)
 
     def drain(self) -> None:
         """Finish every in-flight iteration (their tokens are recorded); the

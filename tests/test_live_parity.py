@@ -23,6 +23,7 @@ from oracle.scenarios import APPENDIX_B
 from oracle.serve_oracle import device_weights, make_weights
 
 LOGIT_REL_TOL = 2e-2
+LIVE_KV_TOKENS = 1600
 
 
 def _live_run(pace_layers=1, pace_tail=0, cpu_threads=4):
@@ -39,6 +40,11 @@ def _live_run(pace_layers=1, pace_tail=0, cpu_threads=4):
     step = LiveCudaStep(cfg, rt, weights=device_weights(w), keep_logits=True)
     step.trace_tokens = True
     doc = copy.deepcopy(APPENDIX_B)
+    # 1600 GPU KV tokens (Appendix B: 1000): still forces BE swap-outs next to
+    # the LS load, but two long LS requests plus a partial LS prefill can no
+    # longer fill the budget -- on the wall clock that wedges the reference
+    # policy (no BE left on the GPU to swap out; tests/test_live_host.py)
+    doc["profiles"]["cluster"]["gpu_kv_capacity"] = LIVE_KV_TOKENS
     eng = LiveEngine(scenario_from_dict(doc, "live_b"), step=step, pace_layers=pace_layers,
                      pace_tail=pace_tail, batch_trace=True)
     n = eng.run_live(horizon_s=30.0)
@@ -53,7 +59,7 @@ def test_live_engine_matches_oracle_replay(cuda, pace_layers, pace_tail):
 
     cfg, w, eng, step, n = _live_run(pace_layers, pace_tail)
     c = eng.counters
-    assert n > 100 and c["tokens_total"] > 1000, (n, c)
+    assert not eng.stalled and c["tokens_total"] == 6280, (n, c)
     # the async machinery the bench relies on was exercised
     assert c["swap_out_done"] > 0 and c["injections"] > 0, c
     assert c["merges"] > 0 and c["be_tokens_cpu"] > 0, c
