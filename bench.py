@@ -12,15 +12,24 @@ contents are synthetic.  A "step" is one serving iteration of the live
 engine (all 32 layers of the planned LS+BE batch plus the piggyback
 exchange); the scheduler, merges, CPU service and swaps run live.
 
-value   = BE decode tokens emitted in the K timed iterations / device time of
-          those iterations (CUDA events on the compute stream, GPU idle gaps
-          between iterations included), summed over replicas / max over ranks.
+A step is one piggyback chain cycle: n_layers (32) serving iterations, the
+iterations a host-resident BE request needs per token (its chain advances one
+layer per iteration, reference engine.py:982-1022).  Warm-up runs W steps and
+then continues until the run is stationary (>= --warmup-s of serving, chains
+have completed tokens); the iterations actually used are reported.
+
+value   = BE decode tokens emitted in the K timed steps / device time of those
+          steps (CUDA events on the compute stream, GPU idle gaps between
+          iterations included), summed over replicas / max over ranks.
 e2e     = the same through the public API on the wall clock (host<->device
           metadata, token readback and PCIe piggyback traffic included).
 roofline: the Dense GEMMs (dominant kernel class), algorithmic bytes per
           launch / CUDA-event time, against MEASURED_PEAKS.json HBM GB/s.
-cpu_baseline: the numpy oracle port of the same step on the host cores, on a
-          bounded 2-layer sample of the representative batch (scaled x16).
+slo_sweep: the same workload at LS rates 1/2/4/8/16 per second (short
+          windows): BE tokens/s, TPOT attainment and p99 at each rate.
+cpu_baseline / --impl reference: the same serving iteration in torch bf16 on
+          the host cores (oracle/torch_cpu_step.py; oneDNN/AMX GEMMs), on the
+          GPU arm's mean batch composition, every layer timed.
 """
 
 from __future__ import annotations
@@ -28,6 +37,10 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# load every kernel at context creation: a lazily loaded module costs its
+# first launch milliseconds inside the serving loop
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 import statistics
 import subprocess
 import sys
@@ -224,97 +237,290 @@ def window_metrics(engine, t0: float, t1: float) -> dict:
             "tpot_p99_ms": p99 * 1e3 if p99 is not None else None}
 
 
-# ----------------------------------------------------------------- CPU reference
-def cpu_reference_sample(model, n_ls: int, ls_ctx: int, n_merge: int, be_ctx: int,
-                         sample_layers: int = 2, steps: int = 1, warmup: int = 0) -> dict:
-    """The oracle port of the serving step on the host cores (numpy fp32,
-    BLAS threads = all cores): Dense over the batch + LS decode attention +
-    BE piggyback attention, on `sample_layers` Llama-shaped layers, scaled to
-    the full depth.  Returns per-step seconds and BE tokens/s."""
-    import numpy as np
+# ----------------------------------------------------------------- CPU baseline
+BATCH_FILE = ROOT / "profiles" / "bench_batch.json"
+DEFAULT_BATCH = {"ls_decodes": 8, "ls_ctx": 700, "be_gpu_decodes": 0, "be_gpu_ctx": 9000,
+                 "merges_per_layer": 16, "merge_ctx": 9000, "chunk_tokens": 0,
+                 "source": "default (no GPU-arm measurement committed)"}
 
-    from oracle import llama_ops as O
 
-    rng = np.random.default_rng(0)
-    d, hd, nq, nkv, ffn = model.d_model, model.head_dim, model.n_q, model.n_kv, model.ffn
-    layers = []
-    for _ in range(sample_layers):
-        # stored [in, out] (pre-transposed) so BLAS streams each weight once
-        layers.append({k: np.ascontiguousarray(
-            (rng.standard_normal(shape, dtype=np.float32) * np.float32(0.02)).T)
-            for k, shape in (("qkv", (model.qkv_dim, d)), ("o", (d, nq * hd)),
-                             ("gu", (2 * ffn, d)), ("down", (d, ffn)))})
-    # per-KV-head contiguous [2][n_kv][keys][hd] (the host layout of libhs)
-    def kv_of(n):
-        k = rng.standard_normal((nkv, n, hd), dtype=np.float32)
-        v = rng.standard_normal((nkv, n, hd), dtype=np.float32)
-        return (k, v, np.ascontiguousarray(k.transpose(0, 2, 1)))  # K^T kept for QK^T
+def mean_batch(iters: list, n_layers: int) -> dict:
+    """Mean per-iteration composition of a measured window (for the CPU
+    step and the reference arm)."""
+    n = max(1, len(iters))
+    ls = sum(i["ls_decodes"] for i in iters)
+    be = sum(i["be_gpu_decodes"] for i in iters)
+    mg = sum(i["merges"] for i in iters)
+    return {"ls_decodes": round(ls / n, 2), "ls_ctx": round(sum(i["ls_ctx"] for i in iters) / max(ls, 1)),
+            "be_gpu_decodes": round(be / n, 2),
+            "be_gpu_ctx": round(sum(i["be_gpu_ctx"] for i in iters) / max(be, 1)),
+            "merges_per_layer": round(mg / n / n_layers, 2),
+            "merge_ctx": round(sum(i["merge_ctx"] for i in iters) / max(mg, 1)),
+            "chunk_tokens": round(sum(i["chunk_tokens"] for i in iters) / n, 1)}
 
-    kv_ls = kv_of(ls_ctx)
-    kv_be = kv_of(be_ctx)
-    rows = n_ls + n_merge
-    h = rng.standard_normal((rows, d), dtype=np.float32)
 
-    def attend(q, kv):
-        g = nq // nkv
-        qh = q.reshape(nkv, g, hd)
-        s = np.matmul(qh, kv[2]) / np.sqrt(hd)  # [nkv, g, keys]
-        s = np.exp(s - s.max(-1, keepdims=True))
-        s /= s.sum(-1, keepdims=True)
-        return np.matmul(s, kv[1]).reshape(-1)
+def cpu_step_sample(model, batch: dict, threads: int, steps: int, warmup: int) -> dict:
+    """The serving iteration on the host cores in torch bf16
+    (oracle/torch_cpu_step.py) at the batch composition `batch`; every layer
+    and the LM head timed.  Returns per-iteration seconds and BE tokens/s."""
+    import torch
 
-    def one_step():
-        x = h
-        for w in layers:
-            xn = x / np.sqrt((x * x).mean(-1, keepdims=True) + 1e-5)
-            qkv = xn @ w["qkv"]
-            att = np.stack([attend(qkv[i, :nq * hd], kv_ls if i < n_ls else kv_be)
-                            for i in range(rows)])
-            x = x + att @ w["o"]
-            xn = x / np.sqrt((x * x).mean(-1, keepdims=True) + 1e-5)
-            gu = xn @ w["gu"]
-            a = gu[:, :ffn] / (1 + np.exp(-gu[:, :ffn])) * gu[:, ffn:]
-            x = x + a @ w["down"]
-        return x
+    from oracle.torch_cpu_step import TorchCpuStep
 
+    r = lambda x: max(0, int(round(x)))  # noqa: E731
+    cpu = TorchCpuStep(model, max(1, r(batch["ls_decodes"])), max(1, batch["ls_ctx"]),
+                       r(batch["be_gpu_decodes"]), max(1, r(batch["merges_per_layer"])),
+                       max(1, batch["merge_ctx"]), threads=threads,
+                       n_prefill=r(batch.get("chunk_tokens", 0)))
     for _ in range(warmup):
-        one_step()
-    ts = []
-    for _ in range(steps):
-        t = time.perf_counter()
-        one_step()
-        ts.append((time.perf_counter() - t) * model.n_layers / sample_layers)
-    sec = statistics.median(ts)
-    del O
-    return {"step_s": sec, "steps": ts, "be_tokens_per_step": n_merge,
-            "be_tok_s": n_merge / sec, "cores": os.cpu_count()}
+        cpu.iteration()
+    runs = [cpu.iteration() for _ in range(steps)]
+    s = [x["s"] for x in runs]
+    out = {"step_s": statistics.median(s), "steps_s": s, "be_tokens_per_step": runs[0]["be_tokens"],
+           "weight_gbs": statistics.median(x["weight_gbs"] for x in runs),
+           "kv_gbs": statistics.median(x["kv_gbs"] for x in runs), "threads": threads,
+           "bytes_per_iteration": cpu.weight_bytes + cpu.kv_bytes}
+    out["be_tok_s"] = out["be_tokens_per_step"] * len(s) / sum(s)
+    del cpu, torch
+    return out
+
+
+def simulator_cost(args, model) -> dict:
+    """The reference simulator's own cost: the virtual-time
+    engine (engine.py, the bit-exact restatement of the reference's event
+    loop) on this workload for a short horizon; wall seconds per simulated
+    second, one core."""
+    from paper_2603_12831_b200 import profiler
+    from paper_2603_12831_b200.engine import Engine
+    from paper_2603_12831_b200.scenario import scenario_from_dict
+
+    doc = scenario_doc(args, 16)
+    doc["horizon_s"] = 2.0
+    doc["workload"]["be"] = {"rate": 4.0, "lengths": {"source": "longbench"}}
+    path = ROOT / "profiles" / f"b200_{args.config}_models.json"
+    models = profiler.load(path) if path.exists() else None
+    t = time.perf_counter()
+    rep = Engine(scenario_from_dict(doc, "sim"), models=models).run()
+    wall = time.perf_counter() - t
+    return {"wall_s_per_sim_s": wall / doc["horizon_s"], "horizon_s": doc["horizon_s"],
+            "iterations": rep.counters["iterations"], "cores": 1,
+            "what": "virtual-time engine (reference event loop restated bit-exactly) on this "
+                    "workload (Poisson LS + longbench BE at 4/s), B200 latency models"}
+
+
+def bench_config(args, model, cpu_threads: int, world: int) -> dict:
+    """The workload descriptor both arms print (identical by construction)."""
+    longctx = args.workload == "longctx"
+    return {"workload": ("llama3-8b live serving: Poisson LS (sharegpt, TPOT SLO 50 ms) + "
+                         f"{args.be_chains} host-resident BE decodes kept live ("
+                         + ("32768-token prompts, 136 outputs; config 5" if longctx
+                            else "longbench") +
+                         "; completed ones replaced by new prefilled requests); a step is "
+                         f"{model.n_layers} iterations (one piggyback chain cycle)"),
+            "model": args.config, "ls_rate_per_s": args.ls_rate,
+            "iterations_per_step": model.n_layers,
+            "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
+            "cpu_threads_per_replica": cpu_threads, "parallelism": f"replicas x{world}",
+            "l2": "working set (16 GB weights/iteration) > 126 MB L2"}
+
+
+def replica_workers(cpus: list) -> list:
+    """CPU-attention workers of a replica: its cores minus two for the
+    engine thread."""
+    return cpus[:-2] if len(cpus) > 3 else cpus[:1]
+
+
+def be_cap(args) -> int:
+    """Host KV tokens reserved per BE request."""
+    return 32768 + 136 + 64 if args.workload == "longctx" else 13000 + 400
+
+
+def fit_be_chains(args, model, local_world: int, verbose: bool = False) -> None:
+    """The pinned host KV arena of all replicas on this node must fit in RAM:
+    at most half of the available memory, split among the local replicas."""
+    from paper_2603_12831_b200 import replicas
+
+    per_req = be_cap(args) * model.kv_bytes_per_token_layer * model.n_layers
+    fit = int(0.5 * replicas.mem_available_bytes() / max(local_world, 1) // per_req) - 4
+    if fit < args.be_chains:
+        if verbose:
+            print(f"bench: host RAM holds {max(fit, 1)} BE requests per replica "
+                  f"(asked {args.be_chains})", file=sys.stderr)
+        args.be_chains = max(fit, 1)
 
 
 # ----------------------------------------------------------------- arms
 def run_reference(args) -> None:
+    """The reference arm: the serving iteration on the host cores (torch bf16,
+    all threads), at the GPU arm's measured mean batch; a step is one
+    iteration, all layers timed; exactly --steps steps after --warmup."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import torch
+
+    from paper_2603_12831_b200 import replicas
     from paper_2603_12831_b200.models import get_transformer
 
     model = get_transformer(args.config)
-    ref = cpu_reference_sample(model, args.ref_ls_rows, 700, args.ref_merge_rows, 9000,
-                               steps=args.steps, warmup=min(args.warmup, 1))
-    sample = (f"numpy oracle port, {args.ref_ls_rows} LS decodes (ctx 700) + "
-              f"{args.ref_merge_rows} BE piggyback merges (ctx 9000) per layer, 2 of "
-              f"{model.n_layers} layers timed and scaled")
+    batch = json.loads(BATCH_FILE.read_text()) if BATCH_FILE.exists() else dict(DEFAULT_BATCH)
+    threads = os.cpu_count() or 1
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    cpus = replicas.core_set(0, local_world)
+    fit_be_chains(args, model, local_world)
+    ref = cpu_step_sample(model, batch, threads, steps=args.steps, warmup=max(1, args.warmup))
+    sim = simulator_cost(args, model)
+    sample = (f"torch bf16 serving iteration ({threads} threads) at the GPU arm's mean batch: "
+              f"{batch['ls_decodes']} LS decodes (ctx {batch['ls_ctx']}), "
+              f"{batch['be_gpu_decodes']} GPU BE decodes, {batch['merges_per_layer']} piggyback "
+              f"merges/layer (ctx {batch['merge_ctx']}), {batch['chunk_tokens']} prefill tokens; "
+              f"all {model.n_layers} layers + LM head timed; {ref['step_s']:.2f} s/iteration, "
+              f"weights {ref['weight_gbs']:.1f} GB/s, KV {ref['kv_gbs']:.1f} GB/s")
     line = {
         "impl": "reference", "metric": METRIC, "value": ref["be_tok_s"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ref["step_s"] * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "llama3-8b serving step, CPU oracle port", "model": args.config},
-        "cpu_baseline": {"value": ref["be_tok_s"], "unit": UNIT, "cores": ref["cores"],
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": bench_config(args, model, len(replica_workers(cpus)), args.gpus),
+        "step": "one serving iteration on the host cores (a bounded sample of the workload)",
+        "cpu_baseline": {"value": ref["be_tok_s"], "unit": UNIT, "cores": threads,
                          "kind": "port", "sample": sample},
+        "batch": batch, "steps_s": ref["steps_s"],
+        "simulator": sim,
         "e2e": {"value": ref["be_tok_s"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    del torch
+
+
+class Replica:
+    """One GPU replica: context, engine, BE backlog and trace."""
+
+    def __init__(self, args, world: int, rank: int, local: int, local_world: int):
+        from paper_2603_12831_b200 import profiler, replicas
+        from paper_2603_12831_b200.models import get_transformer
+        from paper_2603_12831_b200.runtime import LiveCudaStep, RuntimeConfig
+
+        self.args, self.world, self.rank = args, world, rank
+        model = self.model = get_transformer(args.config)
+        # the replica's CPU-attention cores: its GPU's NUMA node, split among the
+        # GPUs on that node; two cores stay free for the engine thread
+        cpus = replicas.core_set(local, local_world)
+        workers = replica_workers(cpus)
+        self.cores = len(cpus)
+        self.be_fixed = (32768, 136) if args.workload == "longctx" else None
+        be_cap_tokens = be_cap(args)
+        fit_be_chains(args, model, local_world, verbose=rank == 0)
+        rt = self.rt = RuntimeConfig(
+            max_rows=args.max_rows, max_slots=512,
+            kv_pages=args.gpu_kv_tokens // 64 + 512 + 64, max_pages_per_req=256,
+            max_pos=max(16384, be_cap_tokens + 64), max_chunks=8192, cpu_threads=len(workers),
+            host_kv_bytes=(args.be_chains + 4) * be_cap_tokens
+            * model.kv_bytes_per_token_layer * model.n_layers, device=local,
+            cpu_list=tuple(workers) if args.pin else ())
+        self.step = LiveCudaStep(model, rt, weight_seed=args.seed)
+        models_path = ROOT / "profiles" / f"b200_{args.config}_models.json"
+        scen = self.scenario(args.ls_rate)
+        if args.calibrate or not models_path.exists():
+            self.models = profiler.calibrate(
+                self.step.ctx, scen.cluster, max_batch=args.max_rows,
+                log=(lambda m: print(m, file=sys.stderr)) if rank == 0 else None)
+            if rank == 0 and args.calibrate:
+                out = Path(args.calibrate_out) if args.calibrate_out else models_path
+                out.parent.mkdir(parents=True, exist_ok=True)
+                profiler.save(self.models, out, {"config": args.config, "how": "hs_probe_* on B200"})
+        else:
+            self.models = profiler.load(models_path)
+
+    def scenario(self, ls_rate: float):
+        from paper_2603_12831_b200 import replicas
+        from paper_2603_12831_b200.scenario import scenario_from_dict
+
+        args = self.args
+        if args.route == "round_robin":
+            # one global trace (world x the per-GPU LS rate) split over replicas
+            doc = scenario_doc(args, self.cores, ls_rate=ls_rate * self.world)
+        else:
+            # independent per-replica traces (config 3: replica r uses seed + r)
+            doc = scenario_doc(args, self.cores, ls_rate=ls_rate)
+            doc["seed"] = doc["workload"]["seed"] = replicas.replica_seed(args.seed, self.rank)
+        return scenario_from_dict(doc, "bench")
+
+    def start(self, ls_rate: float):
+        """A fresh engine on the (reset) context: BE backlog + LS trace."""
+        from paper_2603_12831_b200 import replicas
+        from paper_2603_12831_b200.live import LiveEngine
+        from paper_2603_12831_b200.workload import build_requests
+
+        args = self.args
+        scen = self.scenario(ls_rate)
+        eng = self.engine = LiveEngine(scen, models=self.models, step=self.step,
+                                       pace_layers=args.pace, pace_tail=args.pace_tail)
+        self.backlog = BeBacklog(eng, self.step, args.be_chains, args.seed + self.rank,
+                                 fixed=self.be_fixed)
+        if args.ls_decodes:
+            prepopulate_ls(eng, self.step, args.ls_decodes, args.seed + self.rank)
+        trace = build_requests(scen.workload, 600.0)
+        if args.route == "round_robin":
+            trace = replicas.route(trace, self.world)[self.rank]
+        self.arrivals = eng.admit_specs(trace)
+        eng.t0 = time.perf_counter()
+        self.step.set_anchor(eng.clock())
+        return eng
+
+    def run(self, iterations: int) -> int:
+        return self.engine.run_live(max_iterations=iterations, arrivals=self.arrivals,
+                                    idle_exit=False, on_iteration=self.backlog)
+
+    def warm(self, min_iters: int, min_s: float, max_iters: int) -> int:
+        """Warm-up to a stationary state: at least `min_iters` iterations and
+        `min_s` seconds of serving, and at least one BE token completed
+        through Attention Piggybacking (chains in flight everywhere)."""
+        eng, L = self.engine, self.model.n_layers
+        n = self.run(min_iters)
+        while n < max_iters and (eng.clock() < min_s or eng.counters["be_tokens_cpu"] == 0):
+            n += self.run(L)
+        self.step.ctx.sync()
+        eng.drain()
+        return n
+
+
+def timed_window(rep, iterations: int, dist) -> dict:
+    """Run `iterations` serving iterations between two device events on the
+    compute stream; per-replica measurements of the window."""
+    eng, step = rep.engine, rep.step
+    if dist:
+        dist.barrier()
+    launches0 = step.ctx.lib.hs_launch_count()
+    h2d0, d2h0 = step.h2d_bytes, step.d2h_bytes
+    cpu0, be_cpu0 = step.ctx.cpu_busy_seconds(), eng.counters["be_tokens_cpu"]
+    host0 = dict(eng.host_s)
+    step.ctx.sync()
+    tm0 = step.ctx.timer()
+    w0 = eng.clock()
+    it0 = len(eng.iteration_log)
+    rep.run(iterations)
+    tm1 = step.ctx.timer()
+    step.ctx.sync()
+    eng.drain()
+    w1 = eng.clock()
+    if dist:
+        dist.barrier()
+    iters = eng.iteration_log[it0:]
+    # the window in engine time: from the completion of the last warm-up
+    # iteration to the completion of the last timed one
+    e0 = eng.iteration_log[it0 - 1]["end"] if it0 > 0 else w0
+    e1 = iters[-1]["end"] if iters else w1
+    m = window_metrics(eng, e0, e1)
+    m.update({"device_s": step.ctx.elapsed_ms(tm0, tm1) / 1e3, "wall_s": w1 - w0,
+              "launches": step.ctx.lib.hs_launch_count() - launches0,
+              "h2d": step.h2d_bytes - h2d0, "d2h": step.d2h_bytes - d2h0,
+              "cpu_busy": step.ctx.cpu_busy_seconds() - cpu0,
+              "be_cpu": eng.counters["be_tokens_cpu"] - be_cpu0,
+              "host_s": {k: eng.host_s[k] - host0[k] for k in host0}, "iters": iters})
+    return m
 
 
 def run_ours(args) -> None:
@@ -330,110 +536,26 @@ def run_ours(args) -> None:
 
         torch.cuda.set_device(local)
         dist.init_process_group("gloo")
+        if world != args.gpus:
+            raise SystemExit(f"bench: WORLD_SIZE {world} != --gpus {args.gpus}")
 
-    from paper_2603_12831_b200 import profiler, replicas
-    from paper_2603_12831_b200.live import LiveEngine
-    from paper_2603_12831_b200.models import get_transformer
-    from paper_2603_12831_b200.runtime import LiveCudaStep, RuntimeConfig
-    from paper_2603_12831_b200.scenario import scenario_from_dict
+    from paper_2603_12831_b200 import replicas
 
-    model = get_transformer(args.config)
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
-    # the replica's CPU-attention cores: its GPU's NUMA node, split among the
-    # GPUs on that node; two cores stay free for the engine thread
-    cpus = replicas.core_set(local, local_world)
-    workers = cpus[:-2] if len(cpus) > 3 else cpus[:1]
-    cores = len(cpus)
-    if args.route == "round_robin":
-        # one global trace (world x the per-GPU LS rate) split over replicas
-        doc = scenario_doc(args, cores, ls_rate=args.ls_rate * world)
-    else:
-        # independent per-replica traces (config 3: replica r uses seed + r)
-        doc = scenario_doc(args, cores)
-        doc["seed"] = doc["workload"]["seed"] = replicas.replica_seed(args.seed, rank)
-    scenario = scenario_from_dict(doc, "bench")
-    # config 5 (--workload longctx): every BE request a 32768-token prompt with
-    # 136 output tokens, KV in host DRAM (4.3 GB each for Llama-3-8B)
-    be_fixed = (32768, 136) if args.workload == "longctx" else None
-    be_cap_tokens = (be_fixed[0] + be_fixed[1] + 64) if be_fixed else 13000 + 400
-    # the pinned host KV arena of all replicas on this node must fit in RAM:
-    # at most half of the available memory, split among the local replicas
-    per_req = be_cap_tokens * model.kv_bytes_per_token_layer * model.n_layers
-    fit = int(0.5 * replicas.mem_available_bytes() / max(local_world, 1) // per_req) - 4
-    if fit < args.be_chains:
-        if rank == 0:
-            print(f"bench: host RAM holds {max(fit, 1)} BE requests per replica "
-                  f"(asked {args.be_chains})", file=sys.stderr)
-        args.be_chains = max(fit, 1)
-    rt = RuntimeConfig(max_rows=args.max_rows, max_slots=512,
-                       kv_pages=args.gpu_kv_tokens // 64 + 512 + 64, max_pages_per_req=256,
-                       max_pos=max(16384, be_cap_tokens + 64), max_chunks=8192,
-                       cpu_threads=len(workers),
-                       host_kv_bytes=(args.be_chains + 4) * be_cap_tokens
-                       * model.kv_bytes_per_token_layer * model.n_layers, device=local,
-                       cpu_list=tuple(workers) if args.pin else ())
     t_setup = time.perf_counter()
-    step = LiveCudaStep(model, rt, weight_seed=args.seed)
-    models_path = ROOT / "profiles" / f"b200_{args.config}_models.json"
-    if args.calibrate or not models_path.exists():
-        models = profiler.calibrate(step.ctx, scenario.cluster, max_batch=args.max_rows,
-                                    log=(lambda m: print(m, file=sys.stderr)) if rank == 0
-                                    else None)
-        if rank == 0 and args.calibrate:
-            out = Path(args.calibrate_out) if args.calibrate_out else models_path
-            out.parent.mkdir(parents=True, exist_ok=True)
-            profiler.save(models, out, {"config": args.config, "how": "hs_probe_* on B200"})
-    else:
-        models = profiler.load(models_path)
-    engine = LiveEngine(scenario, models=models, step=step, pace_layers=args.pace,
-                        pace_tail=args.pace_tail)
-    backlog = BeBacklog(engine, step, args.be_chains, args.seed + rank, fixed=be_fixed)
-    if args.ls_decodes:
-        prepopulate_ls(engine, step, args.ls_decodes, args.seed + rank)
-    from paper_2603_12831_b200.workload import build_requests
-
-    trace = build_requests(scenario.workload, 600.0)
-    if args.route == "round_robin":
-        trace = replicas.route(trace, world)[rank]
-    arrivals = engine.admit_specs(trace)
+    rep = Replica(args, world, rank, local, local_world)
+    model, step = rep.model, rep.step
+    L = model.n_layers
+    rep.start(args.ls_rate)
     setup_s = time.perf_counter() - t_setup
-    engine.t0 = time.perf_counter()
-    step.set_anchor(engine.clock())
-    engine.run_live(max_iterations=args.warmup, arrivals=arrivals, idle_exit=False,
-                    on_iteration=backlog)
-    step.ctx.sync()
-    engine.drain()
-    if dist:
-        dist.barrier()
-    launches0 = step.ctx.lib.hs_launch_count()
-    h2d0, d2h0 = step.h2d_bytes, step.d2h_bytes
-    cpu0, be_cpu0 = step.ctx.cpu_busy_seconds(), engine.counters["be_tokens_cpu"]
-    host0 = dict(engine.host_s)
-    # timed region: no per-kernel events (an event between two PDL launches
-    # serialises them; measured +2.6 ms/step on llama3-8b)
+    warm_iters = rep.warm(args.warmup * L, args.warmup_s, max(args.warmup, 40) * L)
     with ClockSampler(local) as clocks:
-        step.ctx.sync()
-        tm0 = step.ctx.timer()
-        w0 = host_w0 = engine.clock()
-        it0 = len(engine.iteration_log)
-        engine.run_live(max_iterations=args.steps, arrivals=arrivals, idle_exit=False,
-                        on_iteration=backlog)
-        tm1 = step.ctx.timer()
-        step.ctx.sync()
-        engine.drain()
-        w1 = host_w1 = engine.clock()
-    if dist:
-        dist.barrier()
-    device_s = step.ctx.elapsed_ms(tm0, tm1) / 1e3
-    launches = step.ctx.lib.hs_launch_count() - launches0
-    h2d1, d2h1 = step.h2d_bytes, step.d2h_bytes
-    cpu_busy = step.ctx.cpu_busy_seconds() - cpu0
-    host_ms = {k: (engine.host_s[k] - host0[k]) * 1e3 / max(args.steps, 1) for k in host0}
-    be_cpu = engine.counters["be_tokens_cpu"] - be_cpu0
-    it1 = len(engine.iteration_log)
+        m = timed_window(rep, args.steps * L, dist)
+    eng = rep.engine
+    iters = m["iters"]
     # profiled window: the same workload continued for --profile-steps more
-    # iterations with per-kernel-class CUDA events on the launch stream; the
-    # roofline and the device breakdown come from here
+    # iterations with per-kernel-class CUDA events on the launch stream (the
+    # device breakdown; events serialise the PDL chain there)
     prof = (C_double * 16)()
     prof_s = 0.0
     if args.profile_steps > 0:
@@ -441,41 +563,118 @@ def run_ours(args) -> None:
         step.ctx.lib.hs_profile_read(step.ctx.h, prof, 1)
         step.ctx.sync()
         tp0 = step.ctx.timer()
-        engine.run_live(max_iterations=args.profile_steps, arrivals=arrivals, idle_exit=False,
-                        on_iteration=backlog)
+        rep.run(args.profile_steps)
         tp1 = step.ctx.timer()
         step.ctx.sync()
-        engine.drain()
+        eng.drain()
         prof_s = step.ctx.elapsed_ms(tp0, tp1) / 1e3
         step.ctx.lib.hs_profile_read(step.ctx.h, prof, 1)
         step.ctx.lib.hs_profile(step.ctx.h, 0)
-    iters = engine.iteration_log[it0:it1]
-    # the window in engine time: from the completion of the last warm-up
-    # iteration to the completion of the last timed one
-    w0 = engine.iteration_log[it0 - 1]["end"] if it0 > 0 else w0
-    w1 = iters[-1]["end"] if iters else w1
-    m = window_metrics(engine, w0, w1)
-    wall_s = host_w1 - host_w0
     stats = np.array(list(prof), dtype=np.float64).reshape(4, 4)
     # whole job: tokens, LS gaps and launches summed over replicas; device and
     # wall windows and the LS p99 maxed (the slowest replica bounds the job)
     tot, mx = replicas.aggregate(
-        [m["be_tokens"], m["ls_tokens"], launches, m["ls_gaps"],
-         m["tpot_attainment"] * m["ls_gaps"]],
-        [device_s, wall_s, m["tpot_p99_ms"] or 0.0], dist)
+        [m["be_tokens"], m["ls_tokens"], m["launches"], m["ls_gaps"],
+         m["tpot_attainment"] * m["ls_gaps"], m["be_cpu"], 1.0],
+        [m["device_s"], m["wall_s"], m["tpot_p99_ms"] or 0.0], dist)
     device_max, wall_max = float(mx[0]), float(mx[1])
     attain = float(tot[4] / tot[3]) if tot[3] else 1.0
+    roof, pcie = roofline_and_link(args, rep, iters, stats, prof_s)
+    batch = mean_batch(iters, L)
+    # LS-rate sweep (short windows on the same context)
+    sweep = []
+    if args.sweep:
+        for lam in args.sweep:
+            step.reset()
+            rep.start(lam)
+            rep.warm(args.sweep_warmup * L, args.warmup_s, max(args.sweep_warmup, 20) * L)
+            ms = timed_window(rep, args.sweep_steps * L, dist)
+            t2, m2 = replicas.aggregate([ms["be_tokens"], ms["ls_gaps"],
+                                         ms["tpot_attainment"] * ms["ls_gaps"]],
+                                        [ms["device_s"], ms["tpot_p99_ms"] or 0.0], dist)
+            att = float(t2[2] / t2[1]) if t2[1] else 1.0
+            sweep.append({"ls_rate_per_s": lam, "be_tok_s": float(t2[0] / m2[0]) if m2[0] else 0.0,
+                          "tpot_attainment": att, "tpot_p99_ms": float(m2[1]),
+                          "ls_gaps": int(t2[1]), "slo_met": bool(att >= 0.99),
+                          "ms_per_iteration": float(m2[0]) * 1e3 / max(1, len(ms["iters"]))})
     if rank != 0:
+        step.finish()
         return
+    value = tot[0] / device_max if device_max > 0 else 0.0
+    e2e_val = tot[0] / wall_max if wall_max > 0 else 0.0
+    ms_step = device_max * 1e3 / max(args.steps, 1)
+    n_merges = sum(i["merges"] for i in iters)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, synthetic KV, Poisson LS trace)",
+        "config": bench_config(args, model, rep.rt.cpu_threads, world),
+        "iterations_timed": len(iters), "warmup_iterations": warm_iters,
+        "gpus_active": int(tot[6]),
+        "ls_tpot_attainment": attain, "ls_tpot_p99_ms": float(mx[2]),
+        "ls_tokens": int(tot[1]), "be_tokens": int(tot[0]), "ls_gaps": int(tot[3]),
+        "slo_met": bool(attain >= 0.99),
+        "merges": n_merges, "avg_batch_tokens": statistics.mean(i["batch_tokens"] for i in iters)
+        if iters else 0,
+        "batch_tokens_p90": sorted(i["batch_tokens"] for i in iters)[int(0.9 * len(iters))]
+        if iters else 0,
+        "batch": batch,
+        "be_tokens_via_cpu_attention": int(tot[5]),
+        "cpu_pool_busy_frac": m["cpu_busy"] / max(m["wall_s"] * rep.rt.cpu_threads, 1e-9),
+        "host_ms_per_iteration": {k: v * 1e3 / max(1, len(iters)) for k, v in m["host_s"].items()},
+        "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters
+                                              if i.get("device_ms")) if iters else None,
+        "device_breakdown_ms": {"window": f"{args.profile_steps} profiled iterations after the "
+                                          "timed region (events serialise PDL launches there)",
+                                "total": prof_s * 1e3, "layers": stats[3, 1],
+                                "gemm": stats[0, 1], "decode_attn": stats[1, 1],
+                                "prefill_attn": stats[2, 1],
+                                "other_kernels": stats[3, 1] - stats[0, 1] - stats[1, 1] - stats[2, 1],
+                                "between_layers": prof_s * 1e3 - stats[3, 1]},
+        "roofline": roof,
+        "piggyback": {
+            "ship_bytes_per_iteration": m["d2h"] / max(1, len(iters)),
+            "result_bytes_per_iteration": m["h2d"] / max(1, len(iters)),
+            "items_per_iteration": n_merges / max(1, len(iters)),
+            "pcie_probe_64_items": pcie},
+        "e2e": {"value": e2e_val, "unit": UNIT,
+                "h2d_bytes_per_step": m["h2d"] / max(args.steps, 1),
+                "d2h_bytes_per_step": m["d2h"] / max(args.steps, 1)},
+        "gpu_launches": int(tot[2]),
+        "clocks": clocks.summary(),
+        "setup_s": setup_s,
+    }
+    if sweep:
+        ok = [s_ for s_ in sweep if s_["slo_met"]]
+        line["slo_sweep"] = sweep
+        line["slo_sweep_window"] = (f"{args.sweep_steps} steps per rate after >= {args.warmup_s} s "
+                                    "of warm-up, same context")
+        line["max_be_tok_s_at_slo"] = max((s_["be_tok_s"] for s_ in ok), default=None)
+    step.finish()
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        ref = cpu_step_sample(model, batch, threads, steps=1, warmup=1)
+        line["cpu_baseline"] = {
+            "value": ref["be_tok_s"], "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"torch bf16 serving iteration on the host cores at this run's mean batch "
+                      f"({batch['ls_decodes']} LS decodes, {batch['merges_per_layer']} piggyback "
+                      f"merges/layer, {batch['chunk_tokens']} prefill tokens), every layer timed; "
+                      f"{ref['step_s']:.2f} s/iteration, weights {ref['weight_gbs']:.1f} GB/s"}
+    print(json.dumps(line), flush=True)
+    if args.write_batch:
+        BATCH_FILE.write_text(json.dumps({**batch, "source": f"bench.py GPU arm, {len(iters)} "
+                                          "timed iterations"}, indent=1) + "\n")
+
+
+def roofline_and_link(args, rep, iters, stats, prof_s):
+    """Dense-GEMM roofline at the run's mean batch (in-stream, PDL chain
+    intact) and the PCIe rate of the piggyback mailboxes."""
+    step, model = rep.step, rep.model
     pk = peaks()
-    gemm_ms, gemm_bytes, gemm_launches, gemm_flops = stats[0, 1], stats[0, 2], stats[0, 0], stats[0, 3]
+    gemm_ms, gemm_bytes, gemm_launches = stats[0, 1], stats[0, 2], stats[0, 0]
     serial_gbs = gemm_bytes / (gemm_ms / 1e3) / 1e9 if gemm_ms > 0 else 0.0
-    intensity = gemm_flops / gemm_bytes if gemm_bytes else 0.0
     ridge = pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
-    # the roofline's launch duration: the four Dense GEMMs of all 32 layers at
-    # this run's mean batch, back to back on the step stream (PDL chain intact,
-    # 16 GB of weights per pass >> L2) between one CUDA event pair; per-launch
-    # events (the profiled window) serialise the PDL chain and overstate it
     rows_mean = max(1, round(statistics.mean(i["batch_tokens"] for i in iters))) if iters else 1
     us_l, by_l = C_float(), C_double()
     step.ctx.lib.hs_probe_gemm_stream.argtypes = [C_void_p, C_int, C_int, C_POINTER(C_float),
@@ -515,83 +714,31 @@ def run_ours(args) -> None:
                  "window": f"4 x {model.n_layers} Dense GEMM launches at the run's mean batch "
                            f"({rows_mean} rows) back to back between one event pair (median of 5)",
                  "serialised_window": {
-                     "what": f"{args.profile_steps} profiled steps after the timed region, events "
-                             "around every GEMM launch (serialises PDL; includes the LM head)",
+                     "what": f"{args.profile_steps} profiled iterations after the timed region, "
+                             "events around every GEMM launch (serialises PDL; includes the LM head)",
                      "launches": int(gemm_launches), "ms_per_launch": gemm_ms / max(gemm_launches, 1),
                      "gbs": serial_gbs, "frac": serial_gbs / pk["hbm_gbs"],
                      "share_of_device_time": gemm_ms / 1e3 / max(prof_s, 1e-9)},
                  "peak_source": pk["source"],
                  "decode_attn": {"ms": stats[1, 1], "gbs": stats[1, 2] / max(stats[1, 1], 1e-9) / 1e6,
                                  "frac": stats[1, 2] / max(stats[1, 1], 1e-9) / 1e6 / pk["hbm_gbs"]}})
-    value = tot[0] / device_max if device_max > 0 else 0.0
-    e2e_val = tot[0] / wall_max if wall_max > 0 else 0.0
-    ms_step = device_max * 1e3 / max(args.steps, 1)
-    n_merges = sum(i["merges"] for i in iters)
-    avg_rows = statistics.mean(i["batch_tokens"] for i in iters) if iters else 0
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init weights, synthetic KV, Poisson LS trace)",
-        "config": {"workload": ("llama3-8b live serving: Poisson LS (sharegpt, TPOT SLO 50 ms) + "
-                                f"{args.be_chains} host-resident BE decodes kept live ("
-                                + ("32768-token prompts, 136 outputs; config 5" if be_fixed
-                                   else "longbench") +
-                                "; completed ones replaced by new prefilled requests)"),
-                   "model": args.config, "ls_rate_per_s": args.ls_rate,
-                   "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
-                   "cpu_threads_per_replica": rt.cpu_threads, "parallelism": f"replicas x{world}",
-                   "pace_layers": args.pace, "pace_tail": args.pace_tail,
-                   "l2": "working set (16 GB weights/iteration) > 126 MB L2"},
-        "ls_tpot_attainment": attain, "ls_tpot_p99_ms": float(mx[2]),
-        "ls_tokens": int(tot[1]), "be_tokens": int(tot[0]), "ls_gaps": int(tot[3]),
-        "slo_met": bool(attain >= 0.99),
-        "merges": n_merges, "avg_batch_tokens": avg_rows,
-        "batch_tokens_p90": sorted(i["batch_tokens"] for i in iters)[int(0.9 * len(iters))]
-        if iters else 0,
-        "be_tokens_via_cpu_attention": be_cpu,
-        "cpu_pool_busy_frac": cpu_busy / max(wall_s * rt.cpu_threads, 1e-9),
-        "host_ms_per_step": host_ms,
-        "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters
-                                              if i.get("device_ms")) if iters else None,
-        "device_breakdown_ms": {"window": f"{args.profile_steps} profiled steps after the timed "
-                                          "region (events serialise PDL launches there)",
-                                "total": prof_s * 1e3, "layers": stats[3, 1],
-                                "gemm": stats[0, 1], "decode_attn": stats[1, 1],
-                                "prefill_attn": stats[2, 1],
-                                "other_kernels": stats[3, 1] - stats[0, 1] - stats[1, 1] - stats[2, 1],
-                                "between_layers": prof_s * 1e3 - stats[3, 1]},
-        "roofline": roof,
-        "piggyback": {
-            "ship_bytes_per_step": (d2h1 - d2h0) / max(args.steps, 1),
-            "result_bytes_per_step": (h2d1 - h2d0) / max(args.steps, 1),
-            "items_per_step": n_merges / max(1, len(iters)),
-            "pcie_probe_64_items": pcie,
-            "link_us_per_step": ((d2h1 - d2h0) / max(args.steps, 1) / (pcie["ship_sm_store_gbs"] or 1)
-                                 + (h2d1 - h2d0) / max(args.steps, 1)
-                                 / (pcie["result_sm_load_gbs"] or 1)) / 1e3},
-        "e2e": {"value": e2e_val, "unit": UNIT,
-                "h2d_bytes_per_step": (h2d1 - h2d0) / max(args.steps, 1),
-                "d2h_bytes_per_step": (d2h1 - d2h0) / max(args.steps, 1)},
-        "gpu_launches": int(tot[2]),
-        "clocks": clocks.summary(),
-        "setup_s": setup_s,
-    }
-    if world == 1 and not args.no_cpu_baseline:
-        avg_ls = statistics.mean(i["ls_decodes"] for i in iters) if iters else 1
-        avg_merge = n_merges / max(1, len(iters)) / model.n_layers
-        ref = cpu_reference_sample(model, max(1, round(avg_ls)), 700, max(1, round(avg_merge)),
-                                   9000, steps=1)
-        line["cpu_baseline"] = {
-            "value": ref["be_tok_s"], "unit": UNIT, "cores": ref["cores"], "kind": "port",
-            "sample": f"numpy oracle port of this run's mean batch ({round(avg_ls)} LS decodes, "
-                      f"{max(1, round(avg_merge))} piggyback merges/layer), 2 of 32 layers timed, "
-                      f"scaled; {ref['step_s']:.2f} s/iteration"}
-    print(json.dumps(line), flush=True)
-    step.finish()
+    return roof, pcie
 
 
 C_double = C_float = C_int = C_void_p = C_POINTER = C_byref = None
+
+
+def spawn_replicas(n: int) -> int:
+    """`--gpus N` outside torchrun: one replica process per GPU via
+    torch.distributed.run (rank 0 prints the line)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())]
+    return subprocess.call(cmd + sys.argv[1:])
 
 
 def main() -> None:
@@ -602,14 +749,21 @@ def main() -> None:
     C_void_p, C_POINTER, C_byref = ctypes.c_void_p, ctypes.POINTER, ctypes.byref
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1500)
-    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=40, help="timed steps (chain cycles)")
+    ap.add_argument("--warmup", type=int, default=8, help="warm-up steps (at least)")
+    ap.add_argument("--warmup-s", type=float, default=2.0,
+                    help="minimum seconds of serving before the timed region (LS ramp)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama3-8b")
     ap.add_argument("--workload", default="saturating", choices=["saturating", "longctx"],
                     help="BE backlog: longbench-like (config 2) or 32k-token prompts (config 5)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ls-rate", type=float, default=8.0)
+    ap.add_argument("--sweep", type=lambda s: [float(x) for x in s.split(",") if x],
+                    default=[1.0, 2.0, 4.0, 8.0, 16.0],
+                    help="LS rates of the SLO sweep (empty string: none)")
+    ap.add_argument("--sweep-steps", type=int, default=4)
+    ap.add_argument("--sweep-warmup", type=int, default=2)
     ap.add_argument("--be-chains", type=int, default=None,
                     help="host-resident BE requests kept live (default 32; 8 for --workload longctx)")
     ap.add_argument("--ls-decodes", type=int, default=0)
@@ -623,21 +777,19 @@ def main() -> None:
     ap.add_argument("--calibrate", action="store_true")
     ap.add_argument("--calibrate-out", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--write-batch", action="store_true",
+                    help="record the measured mean batch for the reference arm")
     ap.add_argument("--route", default="seeded", choices=["seeded", "round_robin"],
                     help="N>1: per-replica seeded traces, or one global trace routed")
     ap.add_argument("--pin", type=int, default=1, help="pin CPU-attention workers")
     ap.add_argument("--profile-steps", type=int, default=160,
-                    help="profiled iterations after the timed region (roofline, breakdown)")
-    ap.add_argument("--ref-ls-rows", type=int, default=8)
-    ap.add_argument("--ref-merge-rows", type=int, default=16)
+                    help="profiled iterations after the timed region (device breakdown)")
     args = ap.parse_args()
     if args.be_chains is None:
         args.be_chains = 8 if args.workload == "longctx" else 32
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_replicas(args.gpus))
     if args.impl == "reference":
-        # each CPU step is a seconds-long bounded sample: cap the count so the
-        # arm finishes within minutes (the line reports the steps actually run)
-        args.steps = max(1, min(args.steps, 10))
-        args.warmup = min(args.warmup, 1)
         run_reference(args)
     else:
         run_ours(args)

@@ -268,6 +268,7 @@ int hs_iter_end(hs_ctx* ctx, int* tokens_out, int n);
  * appends each item's new k/v to the host KV and writes the attention
  * result row into the slot's result mailbox (engine.py:529-560). */
 int hs_cpu_attend(hs_ctx* ctx, const int* slots, const int* layers, const int* ctxs, int n);
+/* Waits for the compute stream and the swap copy stream. */
 int hs_sync(hs_ctx* ctx);
 
 /* ------------------------------------------------------------ live mode

@@ -1732,6 +1732,7 @@ double hs_wall_seconds(void) { return wall_seconds(); }
 
 int hs_sync(hs_ctx* c) {
   CK(cudaStreamSynchronize(c->st));
+  if (c->copy_st) CK(cudaStreamSynchronize(c->copy_st));
   return HS_OK;
 }
 

@@ -184,6 +184,9 @@ class LiveEngine(Engine):
                      "snap": self._snap(rows), "layers": []}
             self.batch_trace.append(trace)
         self.step.begin_iteration(plan)
+        ctx_sum = {"ls_ctx": sum(self.requests[r].ctx for r in plan.ls_decode),
+                   "be_gpu_ctx": sum(self.requests[r].ctx for r in plan.be_decode_gpu),
+                   "merge_ctx": 0}
         for layer in range(1, self.layers + 1):
             it.layer = layer
             tail = layer > self.layers - self.pace_tail
@@ -195,6 +198,7 @@ class LiveEngine(Engine):
             self.now = start = self.clock()
             merged = self._consume_merges(layer, cap)
             if merged:
+                ctx_sum["merge_ctx"] += sum(self.requests[i.req_id].ctx for i in merged)
                 it.merges_total += len(merged)
                 it.merge_layers[layer] = len(merged)
                 self.counters["merges"] += len(merged)
@@ -214,7 +218,7 @@ class LiveEngine(Engine):
                "ls_decodes": len(plan.ls_decode), "be_gpu_decodes": len(plan.be_decode_gpu),
                "chunk_tokens": sum(q for _, q in plan.ls_prefill_chunks + plan.be_prefill_chunks),
                "merges": it.merges_total, "batch_tokens": plan.loads.batch_tokens,
-               "marks": self._collect}
+               "marks": self._collect, **ctx_sum}
         self.step.end_iteration(plan, payload=rec)
         self._iter = None
         self.gpu_busy = False

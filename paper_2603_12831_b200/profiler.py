@@ -24,13 +24,18 @@ from pathlib import Path
 import numpy as np
 
 from .latency import (
+    DecodeAttnModel,
     LatencyModelSet,
+    PrefillAttnModel,
     build_dense_table,
     comm_models_for,
     fit_decode_attn,
     fit_prefill_attn,
     model_set_from_dict,
     model_set_to_dict,
+    predict_decode_attn,
+    predict_dense,
+    predict_prefill_attn,
 )
 from .profiles import DeviceClass
 from .scheduling import pairwise_units
@@ -79,27 +84,95 @@ def calibrate(ctx, cluster, max_batch: int = 8192, max_ctx: int = 16384,
             f"d(1)={dense(1):.1f}us d({max_batch})={dense(max_batch):.1f}us")
 
     rng = np.random.default_rng(seed)
-    da = []
-    for _ in range(24):
+    da = decode_samples(ctx, rng, 24, max_ctx)
+    da_model = fit_decode_attn_nonneg(da)
+    pa = prefill_samples(ctx, rng, 16, max_ctx)
+    pa_model = fit_prefill_attn_nonneg(pa)
+    if log:
+        log(f"decode attn: {da_model}; prefill attn: {pa_model}")
+    return LatencyModelSet(DeviceClass.GPU, pa_model, da_model, table, comm_models_for(cluster))
+
+
+def decode_samples(ctx, rng, n: int, max_ctx: int) -> list[tuple[float, int, float]]:
+    """(context tokens, requests, us) of the decode-attention kernel at
+    random batch shapes (Eq. 3's regressors)."""
+    out = []
+    for _ in range(n):
         g = int(rng.integers(1, 65))
         c = int(rng.integers(64, max_ctx // 2))
         c = min(c, (ctx.rt.max_pages_per_req * 64) - 1, (ctx.rt.kv_pages * 64) // g - 1)
         if c < 2:
             continue
-        da.append((float(g * c), g, _probe(ctx, "hs_probe_decode", g, c)))
-    da_model, _ = fit_decode_attn(da)
-    pa = []
-    for _ in range(16):
+        out.append((float(g * c), g, _probe(ctx, "hs_probe_decode", g, c)))
+    return out
+
+
+def prefill_samples(ctx, rng, n: int, max_ctx: int) -> list[tuple[float, float]]:
+    """(pairwise units, us) of the chunked-prefill kernel (Eq. 2)."""
+    out = []
+    for _ in range(n):
         q = int(rng.integers(16, min(4096, ctx.rt.max_rows)))
         done = int(rng.integers(0, max_ctx // 2))
         done = min(done, ctx.rt.max_pages_per_req * 64 - q - 1)
-        pa.append((pairwise_units(done, q), _probe(ctx, "hs_probe_prefill", q, done)))
-    pa_model, _ = fit_prefill_attn(pa)
-    if pa_model.per_unit < 0:
-        pa_model = type(pa_model)(0.0, pa_model.base)
-    if log:
-        log(f"decode attn: {da_model}; prefill attn: {pa_model}")
-    return LatencyModelSet(DeviceClass.GPU, pa_model, da_model, table, comm_models_for(cluster))
+        out.append((pairwise_units(done, q), _probe(ctx, "hs_probe_prefill", q, done)))
+    return out
+
+
+def nnls(design: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Least squares with non-negative coefficients, exact for the 2-3
+    regressors of Eq. 2/3: the best unconstrained solution over every
+    support subset whose coefficients are all >= 0.  A latency model must not
+    credit a request or a token with negative time (the reference's plain
+    lstsq, latency.py:162-186, can: on B200 the fitted per-request decode
+    term came out at -0.035 us)."""
+    k = design.shape[1]
+    best, best_err = np.zeros(k), float(np.sum(y * y))
+    for mask in range(1, 1 << k):
+        cols = [j for j in range(k) if mask >> j & 1]
+        coef, *_ = np.linalg.lstsq(design[:, cols], y, rcond=None)
+        if np.any(coef < 0):
+            continue
+        err = float(np.sum((design[:, cols] @ coef - y) ** 2))
+        if err < best_err:
+            best = np.zeros(k)
+            best[cols] = coef
+            best_err = err
+    return best
+
+
+def fit_decode_attn_nonneg(samples) -> DecodeAttnModel:
+    fit_decode_attn(samples)  # the reference's degeneracy checks
+    a = np.asarray(samples, dtype=float)
+    c = nnls(np.column_stack([a[:, 0], a[:, 1], np.ones(len(a))]), a[:, 2])
+    return DecodeAttnModel(float(c[0]), float(c[1]), float(c[2]))
+
+
+def fit_prefill_attn_nonneg(samples) -> PrefillAttnModel:
+    fit_prefill_attn(samples)
+    a = np.asarray(samples, dtype=float)
+    c = nnls(np.column_stack([a[:, 0], np.ones(len(a))]), a[:, 1])
+    return PrefillAttnModel(float(c[0]), float(c[1]))
+
+
+def accuracy(ctx, models: LatencyModelSet, seed: int = 1, n: int = 12,
+             max_ctx: int = 16384, max_batch: int = 4096) -> dict:
+    """Held-out accuracy of the fitted models against fresh kernel timings,
+    in the paper's form: mean and 90th-percentile
+    accuracy, 1 - |predicted - measured| / measured, per model family."""
+    rng = np.random.default_rng(seed)
+    fam = {}
+    dn = [int(x) for x in rng.integers(1, min(max_batch, ctx.rt.max_rows), n)]
+    fam["dense"] = [(predict_dense(models.dense, x), _probe(ctx, "hs_probe_dense", x)) for x in dn]
+    fam["decode_attn"] = [(predict_decode_attn(models.decode_attn, c, g), us)
+                          for c, g, us in decode_samples(ctx, rng, n, max_ctx)]
+    fam["prefill_attn"] = [(predict_prefill_attn(models.prefill_attn, u), us)
+                           for u, us in prefill_samples(ctx, rng, n, max_ctx)]
+    out = {}
+    for k, pairs in fam.items():
+        acc = np.array([1.0 - abs(p - m) / m for p, m in pairs if m > 0])
+        out[k] = {"mean": float(acc.mean()), "p90": float(np.percentile(acc, 10)),
+                  "samples": len(acc)}
+    return out
 
 
 def save(models: LatencyModelSet, path: Path, meta: dict | None = None) -> None:

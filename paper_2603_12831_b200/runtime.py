@@ -674,6 +674,34 @@ class LiveCudaStep(CudaStep):
         self._inflight.append((ticket, self._logit_reqs + self._merge_L, payload))
         self.iterations += 1
 
+    def reset(self, timeout_s: float = 60.0) -> None:
+        """Quiesce the replica (in-flight iterations, CPU items, swaps) and
+        release every request slot, so a new engine can be attached to the
+        same context (weights and arenas are kept)."""
+        import time
+
+        self._poll(block=True)
+        self._drained = []
+        t0 = time.perf_counter()
+        while self.ctx.lib.hs_cpu_in_flight(self.ctx.h) > 0:
+            if time.perf_counter() - t0 > timeout_s:
+                raise RuntimeError("reset: CPU-attention items still in flight")
+            time.sleep(1e-3)
+        self.ctx.cpu_poll()
+        self.ctx.sync()
+        for s in list(self.slots.values()):
+            self.pages.release(s)
+            self.ctx.host_kv_release(s)
+            self._dirty.add(s)
+        self._flush_pages()
+        self.slots.clear()
+        self.free_slots = list(range(self.rt.max_slots - 1, -1, -1))
+        for d in (self.generated, self.prompts, self._tags):
+            d.clear()
+        self._pending_release.clear()
+        self._carry, self._merge_L, self._logit_reqs = [], [], []
+        self.token_log.clear()
+
     def iterations_in_flight(self) -> int:
         return len(self._inflight) + len(self._drained)
 

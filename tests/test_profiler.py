@@ -1,0 +1,66 @@
+"""Profiler on real kernels (reference latency.py:162-186 fits,
+200-259 Alg. 1, PAPER.md:760-772 accuracy table).
+
+CPU: the non-negative Eq. 2/3 fits against scipy's NNLS.  GPU: the fitted
+models predict held-out kernel timings of the B200 within 10% on average.
+"""
+
+import numpy as np
+import pytest
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_nnls_matches_scipy(seed):
+    from scipy.optimize import nnls as scipy_nnls
+
+    from paper_2603_12831_b200.profiler import nnls
+
+    rng = np.random.default_rng(seed)
+    n = 24
+    X = np.column_stack([rng.uniform(0, 1e5, n), rng.integers(1, 64, n), np.ones(n)])
+    true = np.array([1e-3, rng.uniform(-0.1, 0.1), rng.uniform(-2, 8)])
+    y = X @ true + rng.normal(0, 0.5, n)
+    ours = nnls(X, y)
+    ref, _ = scipy_nnls(X, y)
+    assert np.all(ours >= 0)
+    np.testing.assert_allclose(np.sum((X @ ours - y) ** 2), np.sum((X @ ref - y) ** 2),
+                               rtol=1e-9, atol=1e-9)
+
+
+def test_nonneg_fits_keep_reference_degeneracy_checks():
+    from paper_2603_12831_b200.errors import FitDegenerateError
+    from paper_2603_12831_b200.profiler import fit_decode_attn_nonneg, fit_prefill_attn_nonneg
+
+    with pytest.raises(FitDegenerateError):
+        fit_decode_attn_nonneg([(100.0, 1, 3.0), (200.0, 1, 4.0), (300.0, 1, 5.0)])
+    with pytest.raises(FitDegenerateError):
+        fit_prefill_attn_nonneg([(10.0, 1.0)])
+    m = fit_decode_attn_nonneg([(1e3, 1, 10.0), (2e3, 2, 10.5), (4e3, 3, 12.0), (8e3, 4, 13.0)])
+    assert m.per_token >= 0 and m.per_request >= 0 and m.base >= 0
+
+
+@pytest.mark.gpu
+def test_calibrated_models_predict_kernel_times(cuda):
+    import dataclasses
+
+    from paper_2603_12831_b200 import profiler
+    from paper_2603_12831_b200.models import get_transformer
+    from paper_2603_12831_b200.runtime import HsContext, RuntimeConfig
+    from paper_2603_12831_b200.scenario import scenario_from_dict
+
+    # the probes time one layer: two layers of the 8B geometry suffice
+    model = dataclasses.replace(get_transformer("llama3-8b"), n_layers=2)
+    rt = RuntimeConfig(max_rows=2048, max_slots=128, kv_pages=4096, max_pages_per_req=256,
+                       max_pos=16384, max_chunks=8192, cpu_threads=1, host_kv_bytes=1 << 20)
+    ctx = HsContext(model, rt)
+    ctx.init_weights(0)
+    cluster = scenario_from_dict({"model": "34B", "horizon_s": 1.0, "profiles": {
+        "cluster": {"layers": 2, "gpu_count": 1, "tp_degree": 1, "cpu_hosts": 1}}},
+        "calib").cluster
+    models = profiler.calibrate(ctx, cluster, max_batch=2048, max_ctx=16384)
+    assert models.decode_attn.per_request >= 0 and models.prefill_attn.per_unit >= 0
+    acc = profiler.accuracy(ctx, models, max_batch=2048)
+    print("latency-model accuracy", acc)
+    for fam, a in acc.items():
+        assert a["mean"] >= 0.90, (fam, a)
+    ctx.close()
