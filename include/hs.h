@@ -295,6 +295,39 @@ int hs_anchor(hs_ctx* ctx);
 int hs_iter_end_async(hs_ctx* ctx, int* ticket);
 int hs_iter_poll(hs_ctx* ctx, int ticket, int* tokens_out, int n, double* done_ms);
 int hs_iter_ntokens(hs_ctx* ctx, int ticket);
+/* ------------------------------------------------- device-polled merges
+ * The piggyback merge decision taken by the GPU (north star item 3; the
+ * reference's _consume_merges / _merge_cap, engine.py:861-919, and the chain
+ * continuation of _process_merge, engine.py:982-1022).  With hs_pg_enable(1)
+ * the output FIFO of work items lives on the device: at the head of every
+ * hs_layer a controller kernel reads the CPU workers' completion tags
+ * (ld.acquire.sys) and merges the ready head-run whose layer matches, at
+ * most `cap` rows; chains merged at layer l are carried into QKV(l+1) and
+ * shipped; at the last layer every merged chain emits its token and
+ * restarts unless it is done or stopped.  Shipped items reach the CPU pool
+ * through a work ring in mapped host memory (no host submission).  The
+ * hs_layer_desc row lists are ignored in this mode (only `layer` is read).
+ * Per iteration:
+ *   hs_iter_begin(...); hs_pg_iter(cap, merge_bound[n_layers], inject_bound);
+ *   hs_layer(l) for l = 1..L; hs_iter_end_async(&ticket);
+ *   once finished: hs_iter_poll(ticket, tokens...) -- the tokens of the
+ *   plan's logit rows, then one row per merge_bound[L] entry of which the
+ *   first (merged chains at L) are valid -- and hs_pg_log(ticket, ...).
+ * Bounds are the launch sizes (padding rows cost compute, not correctness);
+ * the device never merges more than the bound.
+ * hs_pg_log output, per layer 1..L: count n, then n records (slot, flags);
+ * flags 1 = injection taken at layer 1 (carry), 2 = chain restarted with its
+ * next token at layer L, 4 = chain ended at layer L (done or stopped), 0 =
+ * merged and carried into the next layer.  Returns the number of ints. */
+int hs_pg_enable(hs_ctx* ctx, int on);
+/* fresh chains entering at layer 1 (engine.py:437-454 _inject): context
+ * length and tokens still to generate (>= 1), in injection order */
+int hs_pg_inject(hs_ctx* ctx, const int* slots, const int* ctx_tokens, const int* tokens_left,
+                 int n);
+/* swap-in directive at the chain's next token boundary (engine.py:489-494) */
+int hs_pg_stop(hs_ctx* ctx, const int* slots, const int* stop, int n);
+int hs_pg_iter(hs_ctx* ctx, int cap, const int* merge_bound, int inject_bound);
+int hs_pg_log(hs_ctx* ctx, int ticket, int* out, int n);
 /* stream marks for launch pacing, and timing events (CUDA events on the
  * compute stream; elapsed in ms between two timer ids) */
 int hs_mark(hs_ctx* ctx);

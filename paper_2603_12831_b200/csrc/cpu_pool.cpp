@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cstring>
 #include <deque>
+#include <thread>
 
 #include "hs_step.h"
 
@@ -54,6 +55,7 @@ class CpuService {
       stop_ = true;
     }
     cv_.notify_all();
+    if (dispatcher_.joinable()) dispatcher_.join();
     for (auto& t : threads_) t.join();
     for (auto& e : events_) cudaEventDestroy(e);
   }
@@ -101,6 +103,19 @@ class CpuService {
     return HS_OK;
   }
 
+  // Device-polled merges: work items arrive through a ring the GPU publishes
+  // into (entries written, then the tail released after the rows landed);
+  // a dispatcher thread turns new entries into tasks.  No CUDA events.
+  void attach_ring(const int* ring, const int* tail, int Q) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (dispatcher_.joinable()) return;
+    ring_ = ring;
+    ring_tail_ = tail;
+    ring_q_ = Q;
+    ring_next_ = __atomic_load_n(tail, __ATOMIC_ACQUIRE);
+    dispatcher_ = std::thread([this] { dispatch(); });
+  }
+
   int poll(int* slots, int* layers, double* t_done, int max) {
     std::lock_guard<std::mutex> g(mu_);
     int k = 0;
@@ -128,6 +143,39 @@ class CpuService {
   }
 
  private:
+  void dispatch() {
+    int idle = 0;
+    for (;;) {
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (stop_) return;
+      }
+      const int tail = __atomic_load_n(ring_tail_, __ATOMIC_ACQUIRE);
+      if (tail == ring_next_) {
+        if (++idle < 256) {
+          __builtin_ia32_pause();
+        } else {
+          std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+        continue;
+      }
+      idle = 0;
+      const double now = wall();
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        for (int i = ring_next_; i != tail; ++i) {
+          const int* e = ring_ + static_cast<size_t>(i % ring_q_) * 4;
+          const int idx = static_cast<int>(items_.size());
+          items_.push_back(CpuItem{e[0], e[1], e[2], -1, m_.n_kv, now});
+          for (int h = 0; h < m_.n_kv; ++h) tasks_.push_back(CpuTask{idx, h});
+          ++in_flight_;
+        }
+      }
+      ring_next_ = tail;
+      cv_.notify_all();
+    }
+  }
+
   void loop() {
     for (;;) {
       CpuTask t;
@@ -140,7 +188,7 @@ class CpuService {
         tasks_.pop_front();
         it = items_[t.item];
       }
-      cudaEventSynchronize(events_[it.ev]);  // the shipped row has landed
+      if (it.ev >= 0) cudaEventSynchronize(events_[it.ev]);  // the shipped row has landed
       // the slot's previous result was consumed before this item's ship
       // launch (stream order): retract its tag so the device cannot take a
       // stale tag for this item's result (every head does it before the
@@ -160,7 +208,7 @@ class CpuService {
         // the device checks before merging the row
         publish(ref.slot, ref.ctx, ref.layer);
         done_.emplace_back(ref.slot, ref.layer, wall());
-        --ev_refs_[ref.ev];
+        if (ref.ev >= 0) --ev_refs_[ref.ev];
         --in_flight_;
         // compact the item table once everything queued so far is finished
         if (in_flight_ == 0 && tasks_.empty()) items_.clear();
@@ -181,6 +229,10 @@ class CpuService {
   int in_flight_ = 0;
   bool stop_ = false;
   std::atomic<int64_t> busy_ns_{0};
+  std::thread dispatcher_;
+  const int* ring_ = nullptr;
+  const int* ring_tail_ = nullptr;
+  int ring_q_ = 0, ring_next_ = 0;
 };
 
 CpuService* make_cpu_service(const ModelCfg& m, int threads, const std::vector<int>& cpus) {
@@ -206,6 +258,9 @@ int cpu_service_poll(CpuService* s, int* slots, int* layers, double* t_done, int
   return s->poll(slots, layers, t_done, max);
 }
 int cpu_service_in_flight(CpuService* s) { return s->in_flight(); }
+void cpu_service_attach_ring(CpuService* s, const int* ring, const int* tail, int Q) {
+  s->attach_ring(ring, tail, Q);
+}
 double cpu_service_busy(CpuService* s) { return s->busy_seconds(); }
 double wall_seconds() { return CpuService::wall(); }
 

@@ -452,8 +452,8 @@ __global__ void __launch_bounds__(256)
   const int r = blockIdx.y;
   if (r >= rows) {  // merged rows: host attention result -> attention buffer
     const int i = r - rows;
-    // device-polled merges: candidates past the taken count are not consumed
-    if (rc.taken && i >= *rc.taken) return;
+    // device-polled merges: padding rows (negative slot) are not consumed
+    if (rc.idx[i] < 0) return;
     if (rc.expect) {
       // every CTA copying part of the row acquires the row's completion tag
       // itself (the acquire orders this CTA's row loads after the worker's
@@ -497,6 +497,7 @@ __global__ void __launch_bounds__(256)
   const int pos = batch ? row_pos[r] : carry_pos[r - n_batch];
   const int slot = batch ? row_slot[r] : carry_slot[r - n_batch];
   const int mode = batch ? (row_mode ? row_mode[r] : 0) : 1;
+  if (slot < 0) return;  // padding carry row (device-polled merges): nothing shipped
   float a1, a2, b1, b2;  // (x1, x2) of pairs j and j+1
   const int np = splits.count(r, base);
   if (permuted) {  // feature i of the head in row 2i, feature i + hd/2 in row 2i+1

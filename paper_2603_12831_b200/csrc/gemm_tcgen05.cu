@@ -96,8 +96,9 @@ __device__ __forceinline__ void epi_apply(const EpiParams& ep, int n, int lane, 
       const int tt = t0c + j;
       if (tt >= tokens) continue;
       const bool batch = tt < ep.n_batch;
-      const int pos = batch ? ep.row_pos[tt] : ep.carry_pos[tt - ep.n_batch];
       const int slot = batch ? ep.row_slot[tt] : ep.carry_slot[tt - ep.n_batch];
+      if (slot < 0) continue;  // padding carry row (device-polled merges)
+      const int pos = batch ? ep.row_pos[tt] : ep.carry_pos[tt - ep.n_batch];
       float y = v[j];
       if (rotate) {
         const float c = ep.rope_cos[static_cast<size_t>(pos) * half + jj];

@@ -29,6 +29,32 @@ struct HostRegion {
   bool used = false;
 };
 
+// Device-polled piggyback merges (piggyback.cu): the output FIFO of work
+// items lives on the device, the merge decision of every layer is taken by
+// a controller kernel from the CPU workers' completion tags, and the shipped
+// items reach the CPU pool through a work ring in mapped host memory.
+struct PgDev {
+  int Q = 0;                  // FIFO / work-ring capacity (entries)
+  int Qi = 0;                 // injection-ring capacity
+  int* q = nullptr;           // FIFO [Q][3]: slot, layer (1-based), ctx
+  int* inj = nullptr;         // injection ring [Qi]: slot
+  int* st = nullptr;          // counters, see PG_* below
+  int* slot_ctx = nullptr;    // [max_slots] the chain's current context length
+  int* slot_left = nullptr;   // [max_slots] tokens still to generate, this one included
+  int* slot_stop = nullptr;   // [max_slots] 1 = end the chain at its next token boundary
+  int* prev = nullptr;        // [max_rows] slots merged at the previous layer
+  int* lists = nullptr;       // per-layer row lists written by the controller
+  int* it_logit_slots = nullptr;  // [max_rows] the iteration's logit-row slots
+  int* work_d = nullptr;      // work ring [Q][4] (slot, layer, ctx, seq), mapped host
+  int* work_tail_d = nullptr; // published entries (mapped host)
+  int* log_d = nullptr;       // per-iteration decision log (mapped host)
+  const unsigned* tags = nullptr;  // completion tags (mapped host)
+  int list_cap = 0;           // entries per list in `lists`
+  int log_stride = 0;         // ints per iteration in the log
+};
+enum { PG_HEAD = 0, PG_TAIL = 1, PG_PUB = 2, PG_INJ_HEAD = 3, PG_INJ_TAIL = 4, PG_PREV_N = 5,
+       PG_STATE_INTS = 8 };
+
 // device pointers of one hs_layer call's row lists (packed staging run)
 struct LayerRows {
   const int *carry_slot, *carry_pos, *merge_slot, *restart_slot, *restart_pos, *logit_rows,
@@ -144,8 +170,36 @@ struct hs_ctx {
   std::vector<cudaEvent_t> prof_free;
   double prof_stats[4][4] = {};
   double dec_kv_tokens = 0, pre_units = 0, pre_kv_tokens = 0;
+  // device-polled piggyback merges (piggyback.cu)
+  bool pg_on = false;
+  PgDev pg{};
+  int* pg_work_h = nullptr;   // host side of the work ring / tail / log
+  int* pg_tail_h = nullptr;
+  int* pg_log_h = nullptr;
+  int* pg_logit_h = nullptr;  // [kIterRing][max_rows] logit-row slots per iteration (mapped)
+  int* pg_logit_d = nullptr;
+  int* pg_ops_h = nullptr;    // admin-op staging ring (mapped)
+  int* pg_ops_d = nullptr;
+  cudaEvent_t pg_op_ev[8] = {};
+  int pg_op_next = 0;
+  int pg_cap = 0;             // this iteration's per-layer merge cap
+  int pg_inj_bound = 0;       // host bound on the layer-1 injections taken
+  std::vector<int> pg_bound;  // host bound on the merges of each layer
+  int pg_iter_slot = 0;       // ring slot of the iteration being issued
 };
 
 // the fp32 validation datapath of hs_layer (step_f32.cu); called after the
 // row lists are packed, with the same row semantics as the bf16 layer
 int layer_f32(hs_ctx* c, const hs_layer_desc* d, const hs::LayerRows& rows);
+
+namespace hs {
+// device-polled piggyback merges (piggyback.cu)
+int pg_alloc(hs_ctx* c);
+void pg_free(hs_ctx* c);
+// launches the layer's controller; fills `rows` with its device lists and
+// the host bounds of the carry / merge / restart counts
+int pg_control(hs_ctx* c, int layer, hs::LayerRows* rows, int* n_carry, int* n_merge,
+               int* n_restart);
+int pg_publish(hs_ctx* c);
+int ctx_cpu_service(hs_ctx* c);  // starts the CPU-attention pool if needed (step.cu)
+}  // namespace hs

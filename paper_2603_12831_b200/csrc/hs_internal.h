@@ -223,12 +223,13 @@ struct RowIo {
   const int* put_idx = nullptr;
   int put_from = 0;
   __device__ __forceinline__ const float* row_src(const float* h, int r, int d) const {
-    return (src_idx && r >= src_from) ? src + static_cast<size_t>(src_idx[r - src_from]) * d
-                                      : h + static_cast<size_t>(r) * d;
+    // a negative index is a padding row (device-polled merges): its own row
+    const int i = (src_idx && r >= src_from) ? src_idx[r - src_from] : -1;
+    return i >= 0 ? src + static_cast<size_t>(i) * d : h + static_cast<size_t>(r) * d;
   }
   __device__ __forceinline__ float* row_put(int r, int d) const {
-    return (put_idx && r >= put_from) ? put + static_cast<size_t>(put_idx[r - put_from]) * d
-                                      : nullptr;
+    const int i = (put_idx && r >= put_from) ? put_idx[r - put_from] : -1;
+    return i >= 0 ? put + static_cast<size_t>(i) * d : nullptr;
   }
 };
 // n rows gathered dst[i] = src[idx[i]] (bf16, width multiple of 8): the host
@@ -248,8 +249,6 @@ struct RowCopy {
   const unsigned* tags = nullptr;
   unsigned* fault = nullptr;
   int layer = 0;
-  // device-polled merges: only rows i < *taken are consumed (null = all)
-  const int* taken = nullptr;
 };
 int residual_add_norm(const float* part, const Planes& splits, int rows, int d, float* h, const float* w,
                       float eps, bf16* out, int ld_out, cudaStream_t st, const RowIo& io = RowIo{});

@@ -80,6 +80,9 @@ void cpu_service_bind(CpuService* s, std::function<bf16*(int)> ship, std::functi
 int cpu_service_submit(CpuService* s, cudaStream_t st, const int* slots, const int* layers,
                        const int* ctxs, int n);
 int cpu_service_poll(CpuService* s, int* slots, int* layers, double* t_done, int max);
+// device-polled merges: the pool takes its work items from a ring the GPU
+// publishes into (mapped host memory: [Q][4] slot, layer, ctx, seq + tail)
+void cpu_service_attach_ring(CpuService* s, const int* ring, const int* tail, int Q);
 int cpu_service_in_flight(CpuService* s);
 double cpu_service_busy(CpuService* s);
 double wall_seconds();

@@ -364,6 +364,7 @@ void free_all(hs_ctx* c) {
   // reads the ship mailbox and host KV and writes the result mailbox / tags
   if (c->cpu) destroy_cpu_service(c->cpu);
   c->cpu = nullptr;
+  pg_free(c);
   auto F = [](void* p) {
     if (p) cudaFree(p);
   };
@@ -734,6 +735,10 @@ int kv_swap_pages(hs_ctx* c, int slot, int tokens, bool to_host) {
 
 }  // namespace
 
+namespace hs {
+int ctx_cpu_service(hs_ctx* c) { return ensure_cpu_service(c); }
+}  // namespace hs
+
 namespace {
 template <typename F>
 int time_reps(hs_ctx* c, int reps, F&& body, float* us) {
@@ -1081,59 +1086,90 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   const hs_rt_cfg& r = c->r;
   const MetaLayout L = layout_of(r);
   const int l = d->layer - 1;  // 0-based
-  const int B = c->B, C = d->n_carry, M = d->n_merge;
+  const int B = c->B;
   const bool last = d->layer == m.layers;
   const bool tp = c->tp_world > 1;  // row-parallel O / down: fused all-reduce
   if (l < 0 || l >= m.layers) return set_error(HS_E_CONFIG, "layer %d out of range", d->layer);
-  if (B + C > r.max_rows || B + M > r.max_rows || d->n_restart > M)
-    return set_error(HS_E_CAPACITY, "layer rows exceed max_rows");
-  for (int i = 0; i < C; ++i)
-    if (d->carry_pos[i] < 0 || d->carry_pos[i] >= r.max_pos || d->carry_slot[i] < 0 ||
-        d->carry_slot[i] >= r.max_slots)
-      return set_error(HS_E_CONFIG, "carry row %d: slot %d / position %d out of range", i,
-                       d->carry_slot[i], d->carry_pos[i]);
-  for (int i = 0; i < M; ++i)
-    if (d->merge_slot[i] < 0 || d->merge_slot[i] >= r.max_slots)
-      return set_error(HS_E_CONFIG, "merge row %d: slot %d out of range", i, d->merge_slot[i]);
-  for (int i = 0; i < d->n_restart; ++i)
-    if (d->restart_idx[i] < 0 || d->restart_idx[i] >= M || d->restart_pos[i] < 0 ||
-        d->restart_pos[i] >= r.max_pos)
-      return set_error(HS_E_CONFIG, "restart row %d: index %d / position %d out of range", i,
-                       d->restart_idx[i], d->restart_pos[i]);
+  const bool dev_merges = c->pg_on;  // merge decision taken on the device (piggyback.cu)
+  if (dev_merges && (c->fp32 || tp))
+    return set_error(HS_E_CONFIG, "device-polled merges: bf16 single-rank datapath only");
+  int C = d->n_carry, M = d->n_merge, R = d->n_restart;
+  if (!dev_merges) {
+    if (B + C > r.max_rows || B + M > r.max_rows || d->n_restart > M)
+      return set_error(HS_E_CAPACITY, "layer rows exceed max_rows");
+    for (int i = 0; i < C; ++i)
+      if (d->carry_pos[i] < 0 || d->carry_pos[i] >= r.max_pos || d->carry_slot[i] < 0 ||
+          d->carry_slot[i] >= r.max_slots)
+        return set_error(HS_E_CONFIG, "carry row %d: slot %d / position %d out of range", i,
+                         d->carry_slot[i], d->carry_pos[i]);
+    for (int i = 0; i < M; ++i)
+      if (d->merge_slot[i] < 0 || d->merge_slot[i] >= r.max_slots)
+        return set_error(HS_E_CONFIG, "merge row %d: slot %d out of range", i, d->merge_slot[i]);
+    for (int i = 0; i < d->n_restart; ++i)
+      if (d->restart_idx[i] < 0 || d->restart_idx[i] >= M || d->restart_pos[i] < 0 ||
+          d->restart_pos[i] >= r.max_pos)
+        return set_error(HS_E_CONFIG, "restart row %d: index %d / position %d out of range", i,
+                         d->restart_idx[i], d->restart_pos[i]);
+  }
   int* dm = c->dm;
   cudaStream_t st = c->st;
   const int d_ = m.d, nqh = m.n_q * m.hd;
   Planes sp(1);
   ProfScope whole(c, 3, 0.0, 0.0);  // the layer's span on the device
-  const int R = d->n_restart;
-  const int NL = last ? c->n_logit + M : 0;
-  // one packed staging run: carry slots/pos, merge slots, restart slots/pos
-  // and, at the last layer, the LM-head gather rows and their slots; the
-  // kernels read it in place from pinned host memory (a few hundred bytes)
-  Packer pk(c, nullptr, 0);
-  const bool tagged = d->merge_tag != nullptr;
-  const size_t total = 2 * static_cast<size_t>(C) + M + 2 * static_cast<size_t>(R) + 2 * NL +
-                       (tagged ? M : 0);
-  if (total > c->layer_cap) return set_error(HS_E_CAPACITY, "layer metadata too large");
-  if (total && !pk.reserve(total)) return set_error(HS_E_CAPACITY, "metadata staging overflow");
-  std::vector<int> rslot(R), lrows(NL), lslots(NL);
-  for (int i = 0; i < R; ++i) rslot[i] = d->merge_slot[d->restart_idx[i]];
-  for (int i = 0; i < NL; ++i) {
-    const bool batch = i < c->n_logit;
-    lrows[i] = batch ? c->h_logit_rows[i] : B + (i - c->n_logit);
-    lslots[i] = batch ? c->h_logit_slots[i] : d->merge_slot[i - c->n_logit];
-  }
-  const int* carry_slot = total ? pk.add(d->carry_slot, C) : nullptr;
-  const int* carry_pos = total ? pk.add(d->carry_pos, C) : nullptr;
-  const int* merge_slot = total ? pk.add(d->merge_slot, M) : nullptr;
-  const int* restart_slot = total ? pk.add(rslot.data(), R) : nullptr;
-  const int* restart_pos = total ? pk.add(d->restart_pos, R) : nullptr;
-  const int* logit_rows = total ? pk.add(lrows.data(), NL) : nullptr;
-  const int* logit_slots = total ? pk.add(lslots.data(), NL) : nullptr;
-  const int* merge_tag = tagged && M ? pk.add(d->merge_tag, M) : nullptr;
-  if (total) {
-    HProf hp(HP_PACK);
-    RC(pk.flush(st));
+  const int *carry_slot = nullptr, *carry_pos = nullptr, *merge_slot = nullptr,
+            *restart_slot = nullptr, *restart_pos = nullptr, *logit_rows = nullptr,
+            *logit_slots = nullptr, *merge_tag = nullptr;
+  int NL = 0;
+  if (dev_merges) {
+    // the controller takes this layer's FIFO head-run from the completion
+    // tags and writes the row lists (padding rows: slot -1); C / M / R are
+    // the host bounds the launches are sized for
+    LayerRows lr{};
+    RC(pg_control(c, d->layer, &lr, &C, &M, &R));
+    if (B + C > r.max_rows || B + M > r.max_rows)
+      return set_error(HS_E_CAPACITY, "layer rows exceed max_rows (device-polled bounds)");
+    carry_slot = lr.carry_slot, carry_pos = lr.carry_pos, merge_slot = lr.merge_slot;
+    restart_slot = lr.restart_slot, restart_pos = lr.restart_pos, merge_tag = lr.merge_tag;
+    logit_slots = lr.logit_slots;
+    NL = last ? c->n_logit + M : 0;
+    if (NL) {
+      std::vector<int> lrows(NL);
+      for (int i = 0; i < NL; ++i) lrows[i] = i < c->n_logit ? c->h_logit_rows[i] : B + (i - c->n_logit);
+      Packer pk(c, nullptr, 0);
+      if (static_cast<size_t>(NL) > c->layer_cap || !pk.reserve(NL))
+        return set_error(HS_E_CAPACITY, "metadata staging overflow");
+      logit_rows = pk.add(lrows.data(), NL);
+    }
+  } else {
+    NL = last ? c->n_logit + M : 0;
+    // one packed staging run: carry slots/pos, merge slots, restart slots/pos
+    // and, at the last layer, the LM-head gather rows and their slots; the
+    // kernels read it in place from pinned host memory (a few hundred bytes)
+    Packer pk(c, nullptr, 0);
+    const bool tagged = d->merge_tag != nullptr;
+    const size_t total = 2 * static_cast<size_t>(C) + M + 2 * static_cast<size_t>(R) + 2 * NL +
+                         (tagged ? M : 0);
+    if (total > c->layer_cap) return set_error(HS_E_CAPACITY, "layer metadata too large");
+    if (total && !pk.reserve(total)) return set_error(HS_E_CAPACITY, "metadata staging overflow");
+    std::vector<int> rslot(R), lrows(NL), lslots(NL);
+    for (int i = 0; i < R; ++i) rslot[i] = d->merge_slot[d->restart_idx[i]];
+    for (int i = 0; i < NL; ++i) {
+      const bool batch = i < c->n_logit;
+      lrows[i] = batch ? c->h_logit_rows[i] : B + (i - c->n_logit);
+      lslots[i] = batch ? c->h_logit_slots[i] : d->merge_slot[i - c->n_logit];
+    }
+    carry_slot = total ? pk.add(d->carry_slot, C) : nullptr;
+    carry_pos = total ? pk.add(d->carry_pos, C) : nullptr;
+    merge_slot = total ? pk.add(d->merge_slot, M) : nullptr;
+    restart_slot = total ? pk.add(rslot.data(), R) : nullptr;
+    restart_pos = total ? pk.add(d->restart_pos, R) : nullptr;
+    logit_rows = total ? pk.add(lrows.data(), NL) : nullptr;
+    logit_slots = total ? pk.add(lslots.data(), NL) : nullptr;
+    merge_tag = tagged && M ? pk.add(d->merge_tag, M) : nullptr;
+    if (total) {
+      HProf hp(HP_PACK);
+      RC(pk.flush(st));
+    }
   }
   if (c->fp32)
     return layer_f32(c, d, LayerRows{carry_slot, carry_pos, merge_slot, restart_slot, restart_pos,
@@ -1290,6 +1326,9 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
                           m.qkv_n(), st, 1));
     }
   }
+  // device-polled merges: the work items shipped by this layer (carries and
+  // restarts) become visible to the CPU pool once their rows have landed
+  if (dev_merges) RC(pg_publish(c));
   return HS_OK;
 }
 

@@ -20,8 +20,9 @@ __global__ void select_tokens_kernel(const int* __restrict__ row_token,
   pdl_trigger();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
-  if (r >= n_batch) {
-    tok[r] = last_token[carry_slot[r - n_batch]];
+  if (r >= n_batch) {  // a negative slot is a padding row (device-polled merges)
+    const int cs = carry_slot[r - n_batch];
+    tok[r] = cs >= 0 ? last_token[cs] : 0;
     return;
   }
   const int t = row_token[r];
@@ -34,6 +35,7 @@ __global__ void gather_rows_f32_kernel(const float* __restrict__ src, const int*
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const int r = blockIdx.x;
+  if (idx[r] < 0) return;  // padding row
   const float4* s = reinterpret_cast<const float4*>(src + static_cast<size_t>(idx[r]) * d);
   float4* o = reinterpret_cast<float4*>(dst + static_cast<size_t>(r) * d);
   for (int i = threadIdx.x; i < d / 4; i += blockDim.x) o[i] = s[i];
@@ -45,6 +47,7 @@ __global__ void scatter_rows_f32_kernel(const float* __restrict__ src, const int
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const int r = blockIdx.x;
+  if (idx[r] < 0) return;  // padding row
   const float4* s = reinterpret_cast<const float4*>(src + static_cast<size_t>(r) * d);
   float4* o = reinterpret_cast<float4*>(dst + static_cast<size_t>(idx[r]) * d);
   for (int i = threadIdx.x; i < d / 4; i += blockDim.x) o[i] = s[i];
@@ -67,7 +70,7 @@ __global__ void scatter_tokens_kernel(const int* __restrict__ tok, const int* __
   pdl_wait();  // dependent data of the previous kernel is visible
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) last_token[slot[i]] = tok[i];
+  if (i < n && slot[i] >= 0) last_token[slot[i]] = tok[i];
 }
 
 // Swap: copy `tokens` KV entries of one request between its pool pages and

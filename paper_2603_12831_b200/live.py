@@ -32,9 +32,11 @@ from .engine import (
     EV_SERVICE_DONE,
     EV_SWAP_DONE,
     EV_WORKITEM,
+    MERGE_TOKEN_END,
+    MERGE_TOKEN_NEXT,
     Engine,
 )
-from .state import IterationState, ResultItem, SimRequest
+from .state import IterationState, ResultItem, SimRequest, WorkItem
 from .workload import build_requests
 
 
@@ -42,6 +44,14 @@ class LiveEngine(Engine):
     def __init__(self, scenario, models=None, step=None, pace_layers: int = 1,
                  pace_tail: int = 0, batch_trace: bool = False):
         super().__init__(scenario, models=models, step=step)
+        # device-polled merges (step.device_merges): the GPU takes every merge
+        # decision; the engine replays the bookkeeping from each finished
+        # iteration's decision log, in the device's order
+        self.device_merges = bool(getattr(step, "device_merges", False))
+        self._pg_inj: deque = deque()        # injections handed to the device, not yet taken
+        self._pg_stop: dict[str, bool] = {}  # stop flag last sent per chain
+        self._pg_enq: list = []              # work items enqueued by the merge being replayed
+        self._pg_bucket: list = []           # chain items the next layer ships
         # realised batch composition, per iteration: the plan's rows, every
         # layer's merges with their outcomes, and the request state each call
         # saw (the replay input of the oracle; cf. the reference's decision
@@ -80,6 +90,9 @@ class LiveEngine(Engine):
 
     def _push(self, t: float, kind: str, payload) -> None:
         if kind == EV_WORKITEM:
+            if self.device_merges:
+                self._pg_enq.append(payload)
+                return
             self._unshipped[payload.req_id] = payload
         elif kind == EV_SWAP_DONE:
             rid, direction = payload
@@ -116,9 +129,17 @@ class LiveEngine(Engine):
 
     def _poll_async(self) -> None:
         now = self.clock()
-        for rid, _layer in self.step.cpu_poll():
+        for rid, layer in self.step.cpu_poll():
+            if self.device_merges:
+                # a hint that the device has something to merge (the device
+                # decides from the completion tags themselves)
+                w = self._submitted.get(rid)
+                if w is not None and w.layer == layer:
+                    self._finished.add(rid)
+                    self._dirty = True
+                continue
             self._finished.add(rid)
-        while self._order and self._order[0].req_id in self._finished:
+        while not self.device_merges and self._order and self._order[0].req_id in self._finished:
             item = self._order.popleft()
             rid = item.req_id
             self._finished.discard(rid)
@@ -162,9 +183,10 @@ class LiveEngine(Engine):
 
     def _live_iteration(self, plan) -> bool:
         cap = self._merge_cap(plan.loads)
+        pending = (self.queues.output or self.pending_injections
+                   or (self.device_merges and (self._pg_inj or self._finished)))
         has_work = (plan.ls_decode or plan.ls_prefill_chunks or plan.be_prefill_chunks
-                    or plan.be_decode_gpu
-                    or (cap > 0 and (self.queues.output or self.pending_injections)))
+                    or plan.be_decode_gpu or (cap > 0 and pending))
         if not has_work:
             return False
         self.gpu_busy = True
@@ -184,6 +206,8 @@ class LiveEngine(Engine):
                      "snap": self._snap(rows), "layers": []}
             self.batch_trace.append(trace)
         self.step.begin_iteration(plan)
+        if self.device_merges:
+            self._pg_begin(cap)
         ctx_sum = {"ls_ctx": sum(self.requests[r].ctx for r in plan.ls_decode),
                    "be_gpu_ctx": sum(self.requests[r].ctx for r in plan.be_decode_gpu),
                    "merge_ctx": 0}
@@ -196,6 +220,10 @@ class LiveEngine(Engine):
             self.host_s["pace_wait"] += t_i - t_w
             self._poll_async()
             self.now = start = self.clock()
+            if self.device_merges:
+                self.step.layer(layer, [])
+                self.host_s["issue"] += time.perf_counter() - t_i
+                continue
             merged = self._consume_merges(layer, cap)
             if merged:
                 ctx_sum["merge_ctx"] += sum(self.requests[i.req_id].ctx for i in merged)
@@ -219,6 +247,8 @@ class LiveEngine(Engine):
                "chunk_tokens": sum(q for _, q in plan.ls_prefill_chunks + plan.be_prefill_chunks),
                "merges": it.merges_total, "batch_tokens": plan.loads.batch_tokens,
                "marks": self._collect, **ctx_sum}
+        if self.device_merges:
+            rec["trace"] = trace
         self.step.end_iteration(plan, payload=rec)
         self._iter = None
         self.gpu_busy = False
@@ -233,6 +263,8 @@ class LiveEngine(Engine):
 
     def _resolve_iterations(self, block: bool = False) -> None:
         for rec, t_done, _ in self.step.poll_iterations(block=block):
+            if self.device_merges:
+                self._pg_replay(rec, t_done)
             for req, idx in rec.pop("marks"):
                 if idx < 0:
                     req.completion = t_done
@@ -243,6 +275,146 @@ class LiveEngine(Engine):
             rec["end"] = t_done
             rec["device_ms"] = (t_done - self._last_done) * 1e3 if self._last_done else None
             self._last_done = t_done
+
+    # -- device-polled merges ----------------------------------------------------------
+
+    def _runnable(self) -> bool:
+        if self.device_merges and (self._pg_inj or self._finished):
+            return True
+        return super()._runnable()
+
+    def _enqueue_workitem(self, req: SimRequest, layer: int, time_: float) -> None:
+        if not self.device_merges:
+            return super()._enqueue_workitem(req, layer, time_)
+        # the device ships the item; a swap-in directive takes effect at the
+        # chain's next token boundary on the device (the stop flag), not at
+        # the ship of its last layer (engine.py:319-320)
+        item = WorkItem(req.id, layer, req.ctx, next(self._seq), time_)
+        req.chain_state = "input"
+        req.chain_layer = layer
+        self._pg_enq.append(item)
+
+    def _pg_begin(self, cap: int) -> None:
+        """Hand new chains and stop-flag changes to the device, then this
+        iteration's cap and launch bounds."""
+        inj = []
+        while self.pending_injections:
+            item = self.pending_injections.popleft()
+            r = self.requests[item.req_id]
+            inj.append((r.id, r.ctx, r.output_len - r.tokens_out))
+            r.chain_state = "device"  # owned by the device until the log says otherwise
+            self._pg_inj.append(item)
+        stops = []
+        for r in self._live():
+            if r.chain_state == "none" or not isinstance(r.kv_place, int):
+                continue
+            want = r.swap_state in ("in_pending", "in_transfer", "in_done")
+            if want != self._pg_stop.get(r.id, False):
+                stops.append((r.id, want))
+                self._pg_stop[r.id] = want
+        # every chain has one item in the host mirror (FIFO or injection):
+        # no layer can merge more than that
+        n_chains = len(self._order) + len(self._pg_inj)
+        bound = min(cap, n_chains)
+        self.step.pg_begin(cap, [bound] * self.layers, min(cap, len(self._pg_inj)), inj, stops)
+
+    def _pg_ship(self, items) -> None:
+        for w in items:
+            self._order.append(w)
+            self._submitted[w.req_id] = w
+            self.queues.input_enq += 1
+            self.queues.input_deq += 1
+
+    def _pg_boundary(self, item: ResultItem, t: float, flags: int) -> str:
+        """Layer-L merge as the device took it (engine.py:1005-1021): the
+        token is emitted; the chain restarted on the device unless it is done
+        or was stopped by a swap-in directive."""
+        req = self.requests[item.req_id]
+        self.residuals.get(req.id, self.layers)
+        req.chain_state = "none"
+        req.kv_held += 1
+        self._emit_token(req, t)
+        self.counters["be_tokens_cpu"] += 1
+        if req.tokens_out >= req.output_len:
+            if flags & 2:
+                raise AssertionError(f"device restarted finished chain {req.id}")
+            self._pg_stop.pop(req.id, None)
+            self._complete(req, t)
+            return MERGE_TOKEN_END
+        if flags & 2:
+            if req.swap_state == "in_pending":
+                # the directive reached the device after this boundary: the
+                # chain runs one more token, whose KV the swap-in must also
+                # hold on the GPU (the directive reserved ctx + 1 tokens)
+                if self.kv.alloc_gpu(1):
+                    req.gpu_reserved += 1
+                else:
+                    self._cancel_swap_in(req)
+            self._chain_qkv(req, 1, t)
+            return MERGE_TOKEN_NEXT
+        self._pg_stop.pop(req.id, None)
+        if req.swap_state == "in_pending":
+            self._start_swap_in(req, t)
+        elif req.swap_state in ("in_transfer", "in_done"):
+            self._maybe_resume_on_gpu(req)
+        else:  # the directive was withdrawn after the device stopped the chain
+            self._inject(req)
+        return MERGE_TOKEN_END
+
+    def _pg_replay(self, rec: dict, t: float) -> None:
+        """Apply one finished iteration's device decisions (hs_pg_log) to the
+        engine state, layer by layer, with the reference's merge semantics;
+        items enter the host mirror of the FIFO in the device's ship order."""
+        log = rec.pop("pg_log", None)
+        trace = rec.pop("trace", None)
+        if log is None:
+            return
+        self.now = t
+        L = self.layers
+        merges = chain_tokens = 0
+        self._pg_bucket = []
+        for layer, recs in enumerate(log, 1):
+            self._pg_ship(self._pg_bucket)  # this layer's carries (merged at layer-1)
+            self._pg_bucket = []
+            same, outcomes = [], []
+            for rid, flags in recs:
+                req = self.requests[rid]
+                if flags & 1:
+                    item = self._pg_inj.popleft()
+                    if item.req_id != rid:
+                        raise AssertionError(f"device injected {rid}, host expected {item.req_id}")
+                    self.counters["injections"] += 1
+                    req.chain_state = "inject"
+                    out = self._process_merge(item, 1, t, t)
+                else:
+                    w = self._order.popleft()
+                    if w.req_id != rid or w.layer != layer:
+                        raise AssertionError(f"device merged {rid} at layer {layer}, host FIFO "
+                                             f"head is {w.req_id} at layer {w.layer}")
+                    self._submitted.pop(rid, None)
+                    self._finished.discard(rid)
+                    self.queues.output_enq += 1
+                    self.queues.output_deq += 1
+                    req.chain_state = "output"
+                    item = ResultItem(rid, layer, t, w.enq_seq)
+                    if layer < L:
+                        out = self._process_merge(item, layer, t, t)
+                    else:
+                        out = self._pg_boundary(item, t, flags)
+                        chain_tokens += 1
+                outcomes.append((rid, out))
+                for w in self._pg_enq:
+                    (self._pg_bucket if w.layer == layer + 1 else same).append(w)
+                self._pg_enq = []
+            self._pg_ship(same)  # injections (layer 1) / restarts (layer L)
+            if recs:
+                merges += len(recs)
+                self.counters["merges"] += len(recs)
+            if trace is not None:
+                trace["layers"].append((layer, outcomes, self._snap([r for r, _ in recs])))
+        rec["merges"] = merges
+        rec["chain_tokens"] = chain_tokens
+        self._dirty = True
 
     # -- main loop ------------------------------------------------------------------------
 
@@ -286,7 +458,7 @@ class LiveEngine(Engine):
                         on_iteration(n)
                     continue
             quiet = (not arrivals and not self._submitted and not self._swaps
-                     and not self._swapin_wait)
+                     and not self._swapin_wait and not self._pg_inj)
             if idle_exit and quiet and not self._runnable():
                 break
             if quiet and not self._dirty and not self.step.iterations_in_flight():

@@ -84,9 +84,9 @@ def calibrate(ctx, cluster, max_batch: int = 8192, max_ctx: int = 16384,
             f"d(1)={dense(1):.1f}us d({max_batch})={dense(max_batch):.1f}us")
 
     rng = np.random.default_rng(seed)
-    da = decode_samples(ctx, rng, 24, max_ctx)
+    da = decode_samples(ctx, rng, 32, max_ctx)
     da_model = fit_decode_attn_nonneg(da)
-    pa = prefill_samples(ctx, rng, 16, max_ctx)
+    pa = prefill_samples(ctx, rng, 32, max_ctx)
     pa_model = fit_prefill_attn_nonneg(pa)
     if log:
         log(f"decode attn: {da_model}; prefill attn: {pa_model}")
@@ -140,17 +140,26 @@ def nnls(design: np.ndarray, y: np.ndarray) -> np.ndarray:
     return best
 
 
+def _rel_nnls(design: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """NNLS on relative residuals (rows scaled by 1/y): the scheduler's
+    budget test is relative to the SLO, and short kernels dominate the
+    sample count, so a fit in absolute microseconds would trade their
+    accuracy for the long ones'."""
+    w = 1.0 / np.maximum(y, 1e-6)
+    return nnls(design * w[:, None], y * w)
+
+
 def fit_decode_attn_nonneg(samples) -> DecodeAttnModel:
     fit_decode_attn(samples)  # the reference's degeneracy checks
     a = np.asarray(samples, dtype=float)
-    c = nnls(np.column_stack([a[:, 0], a[:, 1], np.ones(len(a))]), a[:, 2])
+    c = _rel_nnls(np.column_stack([a[:, 0], a[:, 1], np.ones(len(a))]), a[:, 2])
     return DecodeAttnModel(float(c[0]), float(c[1]), float(c[2]))
 
 
 def fit_prefill_attn_nonneg(samples) -> PrefillAttnModel:
     fit_prefill_attn(samples)
     a = np.asarray(samples, dtype=float)
-    c = nnls(np.column_stack([a[:, 0], np.ones(len(a))]), a[:, 1])
+    c = _rel_nnls(np.column_stack([a[:, 0], np.ones(len(a))]), a[:, 1])
     return PrefillAttnModel(float(c[0]), float(c[1]))
 
 

@@ -115,9 +115,15 @@ _CTX_SIGS = {
     "hs_wait_mark": [C.c_void_p, C.c_int],
     "hs_timer": [C.c_void_p],
     "hs_timer_elapsed": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)],
+    # device-polled merges
+    "hs_pg_enable": [C.c_void_p, C.c_int],
+    "hs_pg_inject": [C.c_void_p, _IP, _IP, _IP, C.c_int],
+    "hs_pg_stop": [C.c_void_p, _IP, _IP, C.c_int],
+    "hs_pg_iter": [C.c_void_p, C.c_int, _IP, C.c_int],
+    "hs_pg_log": [C.c_void_p, C.c_int, _IP, C.c_int],
 }
 _NONNEG_RETURNS = {"hs_iter_end", "hs_cpu_poll", "hs_cpu_in_flight", "hs_swap_done", "hs_mark",
-                   "hs_timer", "hs_iter_poll", "hs_iter_ntokens"}
+                   "hs_timer", "hs_iter_poll", "hs_iter_ntokens", "hs_pg_log"}
 _lib._SIGNATURES.update(_CTX_SIGS)
 
 
@@ -333,6 +339,37 @@ class HsContext:
         ms = C.c_float(0)
         self._call("hs_timer_elapsed", a, b, C.byref(ms))
         return ms.value
+
+    # device-polled merges (include/hs.h, piggyback.cu)
+    def pg_enable(self, on: bool = True) -> None:
+        self._call("hs_pg_enable", int(on))
+
+    def pg_inject(self, slots, ctxs, lefts) -> None:
+        s, c, l_ = _i32(slots), _i32(ctxs), _i32(lefts)
+        if len(s):
+            self._call("hs_pg_inject", _ip(s), _ip(c), _ip(l_), len(s))
+
+    def pg_stop(self, slots, flags) -> None:
+        s, f = _i32(slots), _i32(flags)
+        if len(s):
+            self._call("hs_pg_stop", _ip(s), _ip(f), len(s))
+
+    def pg_iter(self, cap: int, bounds, inject_bound: int) -> None:
+        b = _i32(bounds)
+        self._call("hs_pg_iter", cap, _ip(b), inject_bound)
+
+    def pg_log(self, ticket: int) -> list[list[tuple[int, int]]]:
+        """Per layer (1..L): [(slot, flags)] decided by the device."""
+        if not hasattr(self, "_pg_buf"):
+            self._pg_buf = np.zeros(self.model.n_layers * (1 + 2 * 1024), np.int32)
+        n = self._call("hs_pg_log", ticket, _ip(self._pg_buf), len(self._pg_buf))
+        out, k = [], 0
+        buf = self._pg_buf[:n].tolist()
+        for _ in range(self.model.n_layers):
+            cnt = buf[k]
+            out.append([(buf[k + 1 + 2 * i], buf[k + 2 + 2 * i]) for i in range(cnt)])
+            k += 1 + 2 * cnt
+        return out
 
     def keep_logits(self, on: bool = True) -> None:
         self._call("hs_keep_logits", int(on))
@@ -633,10 +670,19 @@ class CudaStep(LayerStep):
 
 class LiveCudaStep(CudaStep):
     """CudaStep for LiveEngine: asynchronous CPU service and swaps, launch
-    pacing and per-iteration device timing (CUDA events)."""
+    pacing and per-iteration device timing (CUDA events).
 
-    def __init__(self, *args, **kw):
+    device_merges=True: the piggyback merge decisions are taken by the GPU
+    (hs_pg_*, include/hs.h): layers are launched without row lists, shipped
+    work items reach the CPU pool through the device's work ring, and each
+    finished iteration hands its decision log to the engine (payload
+    "pg_log": per layer [(request id, flags)])."""
+
+    def __init__(self, *args, device_merges: bool = False, **kw):
         super().__init__(*args, **kw)
+        self.device_merges = device_merges
+        if device_merges:
+            self.ctx.pg_enable(True)
         self._marks: list[int] = []
         self.last_device_ms = 0.0
         self.swap_out_tickets: dict[int, str] = {}
@@ -656,8 +702,24 @@ class LiveCudaStep(CudaStep):
         self.ctx.anchor()
         self.anchor_wall = wall
 
+    def pg_begin(self, cap: int, bounds, inject_bound: int, injections=(), stops=()) -> None:
+        """Device-polled merges, per iteration after begin_iteration: new
+        chains [(request id, ctx, tokens left)], stop-flag changes [(request
+        id, flag)], this iteration's cap and the launch bounds."""
+        if injections:
+            self.ctx.pg_inject([self.slot_of(r) for r, _, _ in injections],
+                               [c for _, c, _ in injections], [n for _, _, n in injections])
+        if stops:
+            self.ctx.pg_stop([self.slot_of(r) for r, _ in stops], [int(f) for _, f in stops])
+        self.h2d_bytes += 16 * (len(injections) + len(stops)) + 4 * len(bounds)
+        self.ctx.pg_iter(cap, bounds, inject_bound)
+
     def layer(self, layer: int, merges):
-        shipped = super().layer(layer, merges)
+        if self.device_merges:
+            self.ctx.layer(layer, [], [], [], [], [])
+            shipped = []
+        else:
+            shipped = super().layer(layer, merges)
         self._marks.append(self.ctx.mark())
         if len(self._marks) > 64:
             del self._marks[:-16]
@@ -671,7 +733,8 @@ class LiveCudaStep(CudaStep):
     def end_iteration(self, plan, payload=None) -> None:
         """Queue the token readback; the iteration completes asynchronously."""
         ticket = self.ctx.iter_end_async()
-        self._inflight.append((ticket, self._logit_reqs + self._merge_L, payload))
+        reqs = list(self._logit_reqs) if self.device_merges else self._logit_reqs + self._merge_L
+        self._inflight.append((ticket, reqs, payload))
         self.iterations += 1
 
     def reset(self, timeout_s: float = 60.0) -> None:
@@ -727,7 +790,19 @@ class LiveCudaStep(CudaStep):
                 continue
             toks, ms = res
             self._inflight.pop(0)
-            if len(toks) != len(reqs):
+            if self.device_merges:
+                # the device's decisions; the chains merged at the last layer
+                # own the token rows after the plan's logit rows (the rest of
+                # the launch bound is padding)
+                by_slot = {s: rid for rid, s in self.slots.items()}
+                log = [[(by_slot[s], f) for s, f in recs] for recs in self.ctx.pg_log(ticket)]
+                reqs = list(reqs) + [rid for rid, _ in log[-1]]
+                if len(toks) < len(reqs):
+                    raise RuntimeError(f"libhs returned {len(toks)} tokens for {len(reqs)} rows")
+                toks = toks[:len(reqs)]
+                if payload is not None:
+                    payload["pg_log"] = log
+            elif len(toks) != len(reqs):
                 raise RuntimeError(f"libhs returned {len(toks)} tokens for {len(reqs)} rows")
             if self.trace_tokens:
                 lg = self.ctx.iter_logits(ticket, len(toks)) if self.keep else None

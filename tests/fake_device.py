@@ -172,3 +172,112 @@ class FakeHsContext:
 
     def close(self):
         pass
+
+
+class FakePgContext(FakeHsContext):
+    """FakeHsContext with device-polled merges: a Python model of the
+    controller kernel of csrc/piggyback.cu (FIFO head-run from completion
+    times, layer-1 injections, carries, restarts, stop flags, decision log)
+    executed when each layer is launched."""
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        self.pg_on = False
+        self.fifo: list[list[int]] = []      # [slot, layer, ctx, ready_time]
+        self.inj: list[int] = []
+        self.slot_ctx: dict[int, int] = {}
+        self.slot_left: dict[int, int] = {}
+        self.slot_stop: dict[int, int] = {}
+        self.prev: list[int] = []
+        self.cap = 0
+        self.bounds: list[int] = []
+        self.inj_bound = 0
+        self.logs: dict[int, list] = {}
+        self._log: list = []
+        self._n_logit = 0
+        self.merged_total = 0
+
+    def pg_enable(self, on=True):
+        self.pg_on = bool(on)
+
+    def pg_inject(self, slots, ctxs, lefts):
+        for s, c, l_ in zip(slots, ctxs, lefts):
+            assert l_ >= 1 and s in self.host_kv and c + l_ <= self.host_kv[s]
+            self.inj.append(int(s))
+            self.slot_ctx[int(s)] = int(c)
+            self.slot_left[int(s)] = int(l_)
+            self.slot_stop[int(s)] = 0
+
+    def pg_stop(self, slots, flags):
+        for s, f in zip(slots, flags):
+            self.slot_stop[int(s)] = int(f)
+
+    def pg_iter(self, cap, bounds, inject_bound):
+        self.cap, self.bounds, self.inj_bound = cap, [min(b, cap) for b in bounds], min(inject_bound, cap)
+        self._log = []
+
+    def iter_begin(self, *a, **kw):
+        super().iter_begin(*a, **kw)
+        self._n_logit = self._rows_logit
+
+    def layer(self, layer, carry_slot, carry_pos, merge_slot, restart_idx, restart_pos,
+              merge_tag=None):
+        if not self.pg_on:
+            return super().layer(layer, carry_slot, carry_pos, merge_slot, restart_idx,
+                                 restart_pos, merge_tag)
+        L = self.model.n_layers
+        now = time.perf_counter()
+        m_max = self.bounds[layer - 1]
+        c_max = self.inj_bound if layer == 1 else self.bounds[layer - 2]
+        k = 0
+        while k < min(self.cap, m_max) and k < len(self.fifo):
+            e = self.fifo[k]
+            if e[1] != layer or e[3] > now:
+                break
+            k += 1
+        taken, self.fifo = self.fifo[:k], self.fifo[k:]
+        n_inj = min(len(self.inj), self.cap - k, c_max) if layer == 1 else 0
+        inj, self.inj = self.inj[:n_inj], self.inj[n_inj:]
+        carries = inj if layer == 1 else self.prev[:c_max]
+        ship_t = self._enqueue(self.iter_s / L)
+        for s in carries:
+            self._push_item(s, layer, ship_t)
+        recs = []
+        restarts = 0
+        if layer < L:
+            self.prev = [e[0] for e in taken]
+            recs = [(e[0], 0) for e in taken]
+        else:
+            self.prev = []
+            for e in taken:
+                s = e[0]
+                self.slot_left[s] -= 1
+                self.slot_ctx[s] += 1
+                if self.slot_left[s] > 0 and not self.slot_stop.get(s, 0):
+                    self._push_item(s, 1, ship_t)
+                    recs.append((s, 2))
+                    restarts += 1
+                else:
+                    recs.append((s, 4))
+            self._merge_last = m_max
+        recs += [(s, 1) for s in inj]
+        self.merged_total += len(taken)
+        self._log.append(recs)
+        self.calls["layer"] += 1
+        self.lib.launches += 10
+
+    def _push_item(self, s, layer, ship_t):
+        """A shipped work item: FIFO entry + its CPU completion time."""
+        ready = ship_t + self.cpu_s * self.rng.uniform(0.5, 1.5)
+        assert s in self.host_kv and self.slot_ctx[s] + 1 <= self.host_kv[s]
+        self.fifo.append([s, layer, self.slot_ctx[s], ready])
+        self.cpu.append((ready, s, layer))
+        self.cpu_in_flight += 1
+
+    def iter_end_async(self):
+        t = super().iter_end_async()
+        self.logs[t] = self._log
+        return t
+
+    def pg_log(self, ticket):
+        return self.logs.pop(ticket)

@@ -16,12 +16,12 @@ import pytest
 
 sys.path.insert(0, str(Path(__file__).resolve().parent))
 
-from fake_device import FakeHsContext  # noqa: E402
+from fake_device import FakeHsContext, FakePgContext  # noqa: E402
 
 from oracle.scenarios import APPENDIX_B  # noqa: E402
 
 
-def _run(kv_tokens, seed, pace_layers=1, pace_tail=0, cpu_ms=0.5):
+def _run(kv_tokens, seed, pace_layers=1, pace_tail=0, cpu_ms=0.5, device_merges=False):
     from paper_2603_12831_b200.live import LiveEngine
     from paper_2603_12831_b200.models import TRANSFORMERS
     from paper_2603_12831_b200.runtime import LiveCudaStep, RuntimeConfig
@@ -30,8 +30,9 @@ def _run(kv_tokens, seed, pace_layers=1, pace_tail=0, cpu_ms=0.5):
     cfg = TRANSFORMERS["tiny"]
     rt = RuntimeConfig(max_rows=1024, max_slots=64, kv_pages=256, max_pages_per_req=16,
                        max_pos=2048, max_chunks=1024, cpu_threads=4, host_kv_bytes=256 << 20)
-    fake = FakeHsContext(cfg, rt, iter_ms=0.25, cpu_ms=cpu_ms, rng_seed=seed)
-    step = LiveCudaStep(cfg, rt, ctx=fake)
+    fake = (FakePgContext if device_merges else FakeHsContext)(cfg, rt, iter_ms=0.25,
+                                                               cpu_ms=cpu_ms, rng_seed=seed)
+    step = LiveCudaStep(cfg, rt, ctx=fake, device_merges=device_merges)
     doc = copy.deepcopy(APPENDIX_B)
     doc["profiles"]["cluster"]["gpu_kv_capacity"] = kv_tokens
     eng = LiveEngine(scenario_from_dict(doc, "live"), step=step, pace_layers=pace_layers,
@@ -41,9 +42,10 @@ def _run(kv_tokens, seed, pace_layers=1, pace_tail=0, cpu_ms=0.5):
     return eng, step, fake, n
 
 
+@pytest.mark.parametrize("device_merges", [False, True])
 @pytest.mark.parametrize("seed,pace", [(0, (1, 0)), (1, (2, 1)), (2, (1, 0))])
-def test_live_engine_serves_every_request(seed, pace):
-    eng, step, fake, n = _run(1600, seed, *pace)
+def test_live_engine_serves_every_request(seed, pace, device_merges):
+    eng, step, fake, n = _run(1600, seed, *pace, device_merges=device_merges)
     c = eng.counters
     assert not eng.stalled
     assert c["tokens_total"] == sum(r.output_len for r in eng.requests.values())
@@ -57,6 +59,8 @@ def test_live_engine_serves_every_request(seed, pace):
     assert not any(eng.residuals.outstanding(r) for r in eng.requests)
     assert not step.slots and len(step.free_slots) == step.rt.max_slots
     assert not fake.host_kv
+    if device_merges:  # the device's FIFO drained in step with the host mirror
+        assert not fake.fifo and not fake.inj and fake.merged_total == c["merges"] - c["injections"]
     # every token time was patched to its iteration's device completion
     for r in eng.requests.values():
         assert r.token_times == sorted(r.token_times)

@@ -26,7 +26,7 @@ LOGIT_REL_TOL = 2e-2
 LIVE_KV_TOKENS = 1600
 
 
-def _live_run(pace_layers=1, pace_tail=0, cpu_threads=4):
+def _live_run(pace_layers=1, pace_tail=0, cpu_threads=4, device_merges=False):
     from paper_2603_12831_b200.live import LiveEngine
     from paper_2603_12831_b200.models import TRANSFORMERS
     from paper_2603_12831_b200.runtime import LiveCudaStep, RuntimeConfig
@@ -37,7 +37,8 @@ def _live_run(pace_layers=1, pace_tail=0, cpu_threads=4):
     rt = RuntimeConfig(max_rows=1024, max_slots=64, kv_pages=256, max_pages_per_req=16,
                        max_pos=2048, max_chunks=1024, cpu_threads=cpu_threads,
                        host_kv_bytes=256 << 20)
-    step = LiveCudaStep(cfg, rt, weights=device_weights(w), keep_logits=True)
+    step = LiveCudaStep(cfg, rt, weights=device_weights(w), keep_logits=True,
+                        device_merges=device_merges)
     step.trace_tokens = True
     doc = copy.deepcopy(APPENDIX_B)
     # 1600 GPU KV tokens (Appendix B: 1000): still forces BE swap-outs next to
@@ -53,11 +54,15 @@ def _live_run(pace_layers=1, pace_tail=0, cpu_threads=4):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("pace_layers,pace_tail", [(1, 0), (2, 1)])
-def test_live_engine_matches_oracle_replay(cuda, pace_layers, pace_tail):
+@pytest.mark.parametrize("pace_layers,pace_tail,device_merges",
+                         [(1, 0, False), (2, 1, False), (1, 0, True), (2, 1, True)])
+def test_live_engine_matches_oracle_replay(cuda, pace_layers, pace_tail, device_merges):
+    """device_merges: the merge decisions taken by the GPU controller
+    (csrc/piggyback.cu); the engine's replay of its log is what the oracle
+    replays in turn."""
     from paper_2603_12831_b200.runtime import prompt_tokens
 
-    cfg, w, eng, step, n = _live_run(pace_layers, pace_tail)
+    cfg, w, eng, step, n = _live_run(pace_layers, pace_tail, device_merges=device_merges)
     c = eng.counters
     assert not eng.stalled and c["tokens_total"] == 6280, (n, c)
     # the async machinery the bench relies on was exercised
