@@ -320,6 +320,7 @@ def bench_config(args, model, cpu_threads: int, world: int) -> dict:
             "model": args.config, "ls_rate_per_s": args.ls_rate,
             "iterations_per_step": model.n_layers,
             "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
+            "merge_decision": args.merges,
             "cpu_threads_per_replica": cpu_threads, "parallelism": f"replicas x{world}",
             "l2": "working set (16 GB weights/iteration) > 126 MB L2"}
 
@@ -420,7 +421,8 @@ class Replica:
             host_kv_bytes=(args.be_chains + 4) * be_cap_tokens
             * model.kv_bytes_per_token_layer * model.n_layers, device=local,
             cpu_list=tuple(workers) if args.pin else ())
-        self.step = LiveCudaStep(model, rt, weight_seed=args.seed)
+        self.step = LiveCudaStep(model, rt, weight_seed=args.seed,
+                                 device_merges=args.merges == "device")
         models_path = ROOT / "profiles" / f"b200_{args.config}_models.json"
         scen = self.scenario(args.ls_rate)
         if args.calibrate or not models_path.exists():
@@ -774,6 +776,9 @@ def main() -> None:
     ap.add_argument("--pace", type=int, default=2, help="layers the host may run ahead")
     ap.add_argument("--pace-tail", type=int, default=12,
                     help="final layers of an iteration launched unpaced (covers host planning)")
+    ap.add_argument("--merges", default="device", choices=["device", "host"],
+                    help="piggyback merge decision: GPU controller polling the completion "
+                         "tags (csrc/piggyback.cu), or the host at each layer launch")
     ap.add_argument("--calibrate", action="store_true")
     ap.add_argument("--calibrate-out", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -319,6 +319,8 @@ int hs_iter_ntokens(hs_ctx* ctx, int ticket);
  * flags 1 = injection taken at layer 1 (carry), 2 = chain restarted with its
  * next token at layer L, 4 = chain ended at layer L (done or stopped), 0 =
  * merged and carried into the next layer.  Returns the number of ints. */
+/* on = 1 on an enabled context drops every queued item and injection (a new
+ * engine takes over the replica) */
 int hs_pg_enable(hs_ctx* ctx, int on);
 /* fresh chains entering at layer 1 (engine.py:437-454 _inject): context
  * length and tokens still to generate (>= 1), in injection order */

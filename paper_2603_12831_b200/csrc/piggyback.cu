@@ -111,7 +111,8 @@ __global__ void pg_publish_kernel(PgDev p) {
 }
 
 // admin ops staged by the host, in stream order: {0, slot, ctx, left} =
-// inject a fresh chain (layer-1 entry); {1, slot, stop, 0} = stop flag
+// inject a fresh chain (layer-1 entry); {1, slot, stop, 0} = stop flag;
+// {2, 0, 0, 0} = drop everything queued
 __global__ void pg_admin_kernel(PgDev p, const int* ops, int n) {
   pdl_wait();
   pdl_trigger();
@@ -126,8 +127,12 @@ __global__ void pg_admin_kernel(PgDev p, const int* ops, int n) {
       p.slot_ctx[slot] = o[2];
       p.slot_left[slot] = o[3];
       p.slot_stop[slot] = 0;
-    } else {
+    } else if (o[0] == 1) {
       p.slot_stop[slot] = o[2];
+    } else {  // flush: every queued item and injection is dropped (a new engine)
+      p.st[PG_HEAD] = p.st[PG_TAIL];
+      p.st[PG_INJ_HEAD] = tail;
+      p.st[PG_PREV_N] = 0;
     }
   }
   p.st[PG_INJ_TAIL] = tail;
@@ -384,6 +389,7 @@ int hs_pg_enable(hs_ctx* c, int on) {
   }
   if (c->fp32 || c->tp_world > 1)
     return set_error(HS_E_CONFIG, "device-polled merges: bf16 single-rank datapath only");
+  if (c->pg_on) return stage_ops(c, {2, 0, 0, 0});  // re-enable: drop the queued items
   if (int rc = pg_alloc(c)) return rc;
   if (int rc = ctx_cpu_service(c)) return rc;
   cpu_service_attach_ring(c->cpu, c->pg_work_h, c->pg_tail_h, c->pg.Q);

@@ -978,6 +978,9 @@ int hs_host_kv_release(hs_ctx* c, int slot) {
   if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
   HostRegion& hr = c->regions[slot];
   if (!hr.used) return HS_OK;
+  // the slot's last completion tag stands for nothing any more: a later
+  // occupant's item with the same (ctx, layer) must not read as complete
+  retract_tag(c, slot);
   const size_t bytes = region_bytes(c, hr.cap);
   c->free_list.push_back({hr.offset, bytes});
   std::sort(c->free_list.begin(), c->free_list.end());

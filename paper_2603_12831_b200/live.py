@@ -312,11 +312,26 @@ class LiveEngine(Engine):
             if want != self._pg_stop.get(r.id, False):
                 stops.append((r.id, want))
                 self._pg_stop[r.id] = want
-        # every chain has one item in the host mirror (FIFO or injection):
-        # no layer can merge more than that
-        n_chains = len(self._order) + len(self._pg_inj)
-        bound = min(cap, n_chains)
-        self.step.pg_begin(cap, [bound] * self.layers, min(cap, len(self._pg_inj)), inj, stops)
+        bounds = self._pg_bounds(cap, len(self._pg_inj) - len(inj))
+        self.step.pg_begin(cap, bounds, min(cap, len(self._pg_inj)), inj, stops)
+
+    def _pg_bounds(self, cap: int, injected_before: int) -> list[int]:
+        """Launch bound of each layer's merges: the chains that can be at that
+        layer.  A chain advances at most one layer per iteration (its item
+        merged at layer x ships at x+1 and needs another iteration), so one
+        whose item the host mirror shows at layer m can be merged this
+        iteration only at m .. m+lag, lag = iterations launched but not yet
+        replayed; chains injected in those iterations at 2 .. 1+lag."""
+        L = self.layers
+        lag = self.step.iterations_in_flight()
+        cnt = [0] * (L + 1)
+        for w in self._order:
+            for k in range(min(lag, L - 1) + 1):
+                cnt[(w.layer - 1 + k) % L + 1] += 1
+        for _ in range(injected_before):
+            for k in range(1, min(lag, L - 1) + 1):
+                cnt[k % L + 1] += 1
+        return [min(cap, c) for c in cnt[1:]]
 
     def _pg_ship(self, items) -> None:
         for w in items:

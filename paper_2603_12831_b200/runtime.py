@@ -752,6 +752,8 @@ class LiveCudaStep(CudaStep):
             time.sleep(1e-3)
         self.ctx.cpu_poll()
         self.ctx.sync()
+        if getattr(self, "device_merges", False):
+            self.ctx.pg_enable(True)  # drop the device's queued items
         for s in list(self.slots.values()):
             self.pages.release(s)
             self.ctx.host_kv_release(s)

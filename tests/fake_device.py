@@ -196,6 +196,7 @@ class FakePgContext(FakeHsContext):
         self._log: list = []
         self._n_logit = 0
         self.merged_total = 0
+        self.bound_binding = 0
 
     def pg_enable(self, on=True):
         self.pg_on = bool(on)
@@ -235,6 +236,11 @@ class FakePgContext(FakeHsContext):
             if e[1] != layer or e[3] > now:
                 break
             k += 1
+        # the host's launch bound must never be what stops the head-run
+        ku = 0
+        while ku < min(self.cap, len(self.fifo)) and self.fifo[ku][1] == layer and self.fifo[ku][3] <= now:
+            ku += 1
+        self.bound_binding += ku > k
         taken, self.fifo = self.fifo[:k], self.fifo[k:]
         n_inj = min(len(self.inj), self.cap - k, c_max) if layer == 1 else 0
         inj, self.inj = self.inj[:n_inj], self.inj[n_inj:]

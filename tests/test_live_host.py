@@ -61,6 +61,7 @@ def test_live_engine_serves_every_request(seed, pace, device_merges):
     assert not fake.host_kv
     if device_merges:  # the device's FIFO drained in step with the host mirror
         assert not fake.fifo and not fake.inj and fake.merged_total == c["merges"] - c["injections"]
+        assert fake.bound_binding == 0
     # every token time was patched to its iteration's device completion
     for r in eng.requests.values():
         assert r.token_times == sorted(r.token_times)
