@@ -132,9 +132,21 @@ def scenario_doc(args, cores: int, ls_rate: float = None) -> dict:
         "slo": {"ttft_s": TTFT_SLO_S, "tpot_s": TPOT_SLO_S,
                 "piggyback_reserve_us": args.piggyback_reserve_us},
         "engine": {"events": False},
-        "workload": {"seed": args.seed, "ls": {"rate": ls_rate,
-                                               "lengths": {"source": "sharegpt"}}},
+        "workload": {"seed": args.seed, "ls": ls_stream(args, ls_rate)},
     }
+
+
+def ls_stream(args, ls_rate: float) -> dict:
+    """Poisson LS at `ls_rate`, or (config 3) the bursty schedule of the
+    reference's make_random_rate_schedule: a rate redrawn uniformly in
+    [1, 8]/s every 5 s (workload.py:159-172), scaled by ls_rate / 8."""
+    if args.ls_trace == "poisson":
+        return {"rate": ls_rate, "lengths": {"source": "sharegpt"}}
+    from paper_2603_12831_b200.workload import make_random_rate_schedule
+
+    sched = make_random_rate_schedule(5.0, 1.0, 8.0, 600.0, args.seed)
+    return {"schedule": [[t, r * ls_rate / 8.0] for t, r in sched],
+            "lengths": {"source": "sharegpt"}}
 
 
 def prepopulate_be(engine, step, n: int, seed: int, start: int = 0, fixed=None) -> list:
@@ -311,13 +323,15 @@ def simulator_cost(args, model) -> dict:
 def bench_config(args, model, cpu_threads: int, world: int) -> dict:
     """The workload descriptor both arms print (identical by construction)."""
     longctx = args.workload == "longctx"
-    return {"workload": ("llama3-8b live serving: Poisson LS (sharegpt, TPOT SLO 50 ms) + "
+    lsw = ("Poisson LS" if args.ls_trace == "poisson"
+           else "bursty LS (rate redrawn in [1, 8]/s every 5 s)")
+    return {"workload": (f"{args.config} live serving: {lsw} (sharegpt, TPOT SLO 50 ms) + "
                          f"{args.be_chains} host-resident BE decodes kept live ("
                          + ("32768-token prompts, 136 outputs; config 5" if longctx
                             else "longbench") +
                          "; completed ones replaced by new prefilled requests); a step is "
                          f"{model.n_layers} iterations (one piggyback chain cycle)"),
-            "model": args.config, "ls_rate_per_s": args.ls_rate,
+            "model": args.config, "ls_rate_per_s": args.ls_rate, "ls_trace": args.ls_trace,
             "iterations_per_step": model.n_layers,
             "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
             "merge_decision": args.merges,
@@ -761,6 +775,9 @@ def main() -> None:
                     help="BE backlog: longbench-like (config 2) or 32k-token prompts (config 5)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ls-rate", type=float, default=8.0)
+    ap.add_argument("--ls-trace", default="poisson", choices=["poisson", "burst"],
+                    help="LS arrivals: Poisson at --ls-rate, or the bursty 5 s schedule of "
+                         "config 3 (peak --ls-rate)")
     ap.add_argument("--sweep", type=lambda s: [float(x) for x in s.split(",") if x],
                     default=[1.0, 2.0, 4.0, 8.0, 16.0],
                     help="LS rates of the SLO sweep (empty string: none)")

@@ -1,4 +1,6 @@
-// K6: causal chunked-prefill attention over the paged KV pool.
+// K6: causal chunked-prefill attention over the paged KV pool -- the
+// warp-MMA (mma.sync) version, kept as the A/B baseline of the tcgen05
+// kernel in attn_prefill_tc.cu (HS_PREFILL_MMA=1 selects it).
 //
 // One CTA per (tile of <= 64 query tokens of one request, query head); warp w
 // owns query rows 16w..16w+15.  The chunk's own K/V were scattered into the
@@ -12,6 +14,8 @@
 // pairwise_units(done, q) = q*(2*done+q+1)/2 attended pairs
 // (scheduling.py:127-133).
 #include <math_constants.h>
+
+#include <cstdlib>
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
@@ -213,11 +217,24 @@ static int launch_prefill(const CUtensorMap& kv_map, const KvGeom& g, int layer,
       scale_log2);
 }
 
+// HS_PREFILL_MMA=1 (probe knob, read once): the warp-MMA kernel below
+// instead of the tcgen05 one (attn_prefill_tc.cu), for A/B measurements.
+static bool use_warp_mma() {
+  static const bool v = [] {
+    const char* e = std::getenv("HS_PREFILL_MMA");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 int prefill_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
                       int q_row_stride, int n_q, const int* page_table, int pt_stride,
                       const PrefillTile* tiles, int n_tiles, bf16* out, int out_row_stride,
                       cudaStream_t st) {
   if (n_tiles <= 0) return HS_OK;
+  if (!use_warp_mma() && n_q % g.n_kv == 0 && n_q / g.n_kv <= 8)
+    return prefill_attention_tc(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride,
+                                tiles, n_tiles, out, out_row_stride, st);
   if (n_q % g.n_kv) return HS_E_CONFIG;
   if (g.head_dim == 128)
     return launch_prefill<128>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride,

@@ -1,0 +1,311 @@
+// K6 on the 5th-generation tensor cores: causal chunked-prefill attention
+// over the paged KV pool with tcgen05.mma, TMEM accumulators and TMA-staged
+// KV pages.
+//
+// The reference charges this work as probe_attention(gpu, PREFILL,
+// prefill_units) with prefill_units = pairwise_units(done, q) =
+// q*(2*done+q+1)/2 attended (query, key) pairs
+// (pkg/src/hybridserve/engine.py:935-938, scheduling.py:127-133): 4*n_q*hd
+// flops per pair, the step's only tensor-bound attention.
+//
+// One CTA per (block of query tokens of one prefill tile, KV head).  The
+// 128 MMA rows pack every query head of the KV head's GQA group: row =
+// token * G + g (G = n_q / n_kv; 128/G tokens per block, at most the tile's
+// 64), so each KV page is read once per group instead of once per query
+// head.  Per 64-key page:
+//
+//   S    = Q K^T     tcgen05.mma M=128 N=64  K=hd   (A = Q, K-major, smem;
+//                                                   B = K page, K-major, TMA)
+//   P    = exp2(S*scale - m), online max / sum in registers (one TMEM lane =
+//          one row per thread of warps 0-3), P written to smem (SW128)
+//   Otmp = P V       tcgen05.mma M=128 N=hd K=64    (A = P, K-major;
+//                                                   B = V page, MN-major)
+//   O    = O * alpha + Otmp  in registers
+//
+// Warp 4 issues the TMA page loads (2-stage ring) and, from one thread, the
+// MMAs; S of the next page is issued as soon as the softmax threads have
+// read the current one, so it overlaps the O update.
+#include <math_constants.h>
+
+#include <algorithm>
+
+#include "hs_common.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+namespace {
+
+constexpr int kTcStages = 2;
+constexpr int kTcSoftmaxThreads = 128;  // warps 0-3: one TMEM lane (row) each
+constexpr int kTcThreads = kTcSoftmaxThreads + 32;
+constexpr int kRows = 128;              // MMA M
+constexpr int kSCol = 0;                // TMEM columns of S (64)
+constexpr int kOCol = 128;              // TMEM columns of the P.V product (hd)
+constexpr int kTmemCols = 256;
+
+// MN-major SWIZZLE_128B operand (the V page as staged by TMA: keys are
+// rows of 128 B holding 64 hd elements): LBO = byte distance between
+// 64-element chunks along N (the next TMA box), SBO = 1024 B between
+// 8-key groups along K.
+__device__ __forceinline__ uint64_t umma_desc_mn128(uint32_t smem_addr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(2u) << 61;
+  return d;
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, KvGeom geom, int layer,
+                           const bf16* __restrict__ q, int q_row_stride, int n_q,
+                           const int* __restrict__ page_table, int pt_stride,
+                           const PrefillTile* __restrict__ tiles, int blocks_per_tile,
+                           bf16* __restrict__ out, int out_row_stride, float scale_log2) {
+  constexpr int kBox = kPageTokens * 128;       // one [64 keys][64 el] SW128 box
+  constexpr int kKvBytes = (HD / 64) * kBox;    // K or V of one page
+  constexpr int kStageBytes = 2 * kKvBytes;
+  constexpr int kQBytes = (HD / 64) * kRows * 128;
+  constexpr int kPBytes = kRows * 128;          // P: 128 rows x 64 keys bf16
+  constexpr int kKSteps = HD / 16;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sP = sQ + kQBytes;
+  uint8_t* sKV = sP + kPBytes;
+  __shared__ uint64_t kv_full[kTcStages], kv_empty[kTcStages];
+  __shared__ uint64_t s_full, p_full, o_full;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const PrefillTile tile = tiles[blockIdx.x / blocks_per_tile];
+  const int kvh = blockIdx.y;
+  const int G = n_q / geom.n_kv;
+  const int T = min(kPageTokens, kRows / G);              // tokens per block
+  const int t0 = (blockIdx.x % blocks_per_tile) * T;      // first token of the block
+  const int nt = min(T, tile.nq - t0);                    // tokens of this block
+  if (nt <= 0) return;                                    // (uniform per CTA)
+  const int last_pos = tile.pos0 + t0 + nt - 1;
+  const int npages = last_pos / kPageTokens + 1;
+  const int* pt = page_table + static_cast<size_t>(tile.slot) * pt_stride;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&kv_map);
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(&s_full, 1);
+    mbar_init(&p_full, kTcSoftmaxThreads);
+    mbar_init(&o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 4) tmem_alloc<kTmemCols>(&tmem_base_sh);
+  pdl_wait();  // q (QKV epilogue) and this layer's K/V pages are written
+  pdl_trigger();
+
+  // this thread's MMA row (softmax warps): token t0 + row/G, head kvh*G + row%G
+  const int row = threadIdx.x;
+  const int tok = row / G, gh = row % G;
+  const bool valid = warp < 4 && tok < nt;
+  const int pos = tile.pos0 + t0 + tok;
+  if (warp < 4) {  // Q row -> smem, K-major SWIZZLE_128B
+    const bf16* src = q + static_cast<size_t>(tile.q_row + t0 + tok) * q_row_stride +
+                      static_cast<size_t>(kvh * G + gh) * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 8; ++c) {
+      uint4 v = valid ? reinterpret_cast<const uint4*>(src)[c] : make_uint4(0, 0, 0, 0);
+      const int kb = c >> 3, cc = c & 7;
+      *reinterpret_cast<uint4*>(sQ + kb * (kRows * 128) + row * 128 + ((cc ^ (row & 7)) << 4)) = v;
+    }
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      auto issue = [&](int i) {
+        const int s = i % kTcStages;
+        const int phys = pt[i];
+        uint8_t* dst = sKV + s * kStageBytes;
+        mbar_expect_tx(&kv_full[s], kStageBytes);
+        const int rk = static_cast<int>(kv_row(geom, layer, phys, 0, kvh));
+        const int rv = static_cast<int>(kv_row(geom, layer, phys, 1, kvh));
+#pragma unroll
+        for (int b = 0; b < HD / 64; ++b) {
+          tma_load_2d(dst + b * kBox, &kv_map, &kv_full[s], b * 64, rk);
+          tma_load_2d(dst + kKvBytes + b * kBox, &kv_map, &kv_full[s], b * 64, rv);
+        }
+      };
+      for (int i = 0; i < min(kTcStages, npages); ++i) issue(i);
+      const uint32_t id_s = umma_idesc_bf16(kRows, kPageTokens);
+      const uint32_t id_o = umma_idesc_bf16(kRows, HD) | (1u << 16);  // B (V) MN-major
+      const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
+      auto mma_s = [&](int i) {  // S = Q K_i^T
+        const int s = i % kTcStages;
+        mbar_wait(&kv_full[s], (i / kTcStages) & 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sKV + s * kStageBytes);
+#pragma unroll
+        for (int j = 0; j < kKSteps; ++j) {
+          const uint32_t off_a = (j >> 2) * (kRows * 128) + (j & 3) * 32;
+          const uint32_t off_b = (j >> 2) * kBox + (j & 3) * 32;
+          umma_bf16(tmem + kSCol, umma_desc_k128(q_base + off_a), umma_desc_k128(k_base + off_b),
+                    id_s, j > 0);
+        }
+        umma_commit(&s_full);
+      };
+      mma_s(0);
+      for (int i = 0; i < npages; ++i) {
+        const int s = i % kTcStages;
+        mbar_wait(&p_full, i & 1);  // P_i in smem, S_i and O_{i-1} read out of TMEM
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(sKV + s * kStageBytes + kKvBytes);
+#pragma unroll
+        for (int j = 0; j < kPageTokens / 16; ++j)  // Otmp = P_i V_i (16 keys per step)
+          umma_bf16(tmem + kOCol, umma_desc_k128(p_base + j * 32),
+                    umma_desc_mn128(v_base + j * 2048, kBox), id_o, j > 0);
+        umma_commit(&o_full);
+        umma_commit(&kv_empty[s]);
+        if (i + 1 < npages) mma_s(i + 1);
+        if (i + kTcStages < npages) {
+          mbar_wait(&kv_empty[s], (i / kTcStages) & 1);
+          issue(i + kTcStages);
+        }
+      }
+    }
+  } else {
+    // softmax / accumulation: thread = TMEM lane = MMA row
+    const uint32_t t_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    float o[HD];
+#pragma unroll
+    for (int d = 0; d < HD; ++d) o[d] = 0.f;
+    float m = -CUDART_INF_F, l = 0.f;
+    for (int i = 0; i < npages; ++i) {
+      mbar_wait(&s_full, i & 1);
+      tc_fence_after();
+      float sv[kPageTokens];
+#pragma unroll
+      for (int c = 0; c < kPageTokens / 16; ++c) {
+        float v[16];
+        tmem_ld16(t_row + kSCol + c * 16, v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) sv[c * 16 + e] = v[e];
+      }
+      const int kbase = i * kPageTokens;
+      float mx = -CUDART_INF_F;
+#pragma unroll
+      for (int j = 0; j < kPageTokens; ++j) {
+        sv[j] = (valid && kbase + j <= pos) ? sv[j] * scale_log2 : -CUDART_INF_F;
+        mx = fmaxf(mx, sv[j]);
+      }
+      const float mn = fmaxf(m, mx);
+      const float mu = mn == -CUDART_INF_F ? 0.f : mn;
+      const float alpha = exp2f(m - mu);
+      m = mn;
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < kPageTokens / 8; ++c) {  // P row -> smem (K-major SW128)
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float a = exp2f(sv[c * 8 + 2 * e] - mu), b = exp2f(sv[c * 8 + 2 * e + 1] - mu);
+          const uint32_t pk = pack_bf16x2(a, b);
+          // the row sum is taken over the bf16-rounded P the MMA consumes
+          const __nv_bfloat162 r2 = *reinterpret_cast<const __nv_bfloat162*>(&pk);
+          rs += __bfloat162float(r2.x) + __bfloat162float(r2.y);
+          w[e] = pk;
+        }
+        *reinterpret_cast<uint4*>(sP + row * 128 + ((c ^ (row & 7)) << 4)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      l = l * alpha + rs;
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&p_full);
+      mbar_wait(&o_full, i & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        float v[16];
+        tmem_ld16(t_row + kOCol + c * 16, v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[c * 16 + e] = o[c * 16 + e] * alpha + v[e];
+      }
+      tc_fence_before();
+    }
+    if (valid) {
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      bf16* dst = out + static_cast<size_t>(tile.q_row + t0 + tok) * out_row_stride +
+                  static_cast<size_t>(kvh * G + gh) * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 8; ++c) {
+        uint4 w;
+        w.x = pack_bf16x2(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
+        w.y = pack_bf16x2(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
+        w.z = pack_bf16x2(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
+        w.w = pack_bf16x2(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
+        reinterpret_cast<uint4*>(dst)[c] = w;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_free<kTmemCols>(tmem);
+  }
+}
+
+template <int HD>
+int launch_tc(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+              int q_row_stride, int n_q, const int* pt, int pt_stride, const PrefillTile* tiles,
+              int n_tiles, bf16* out, int out_row_stride, cudaStream_t st) {
+  constexpr int kSmem = (HD / 64) * kRows * 128 + kRows * 128 +
+                        kTcStages * 2 * (HD / 64) * kPageTokens * 128 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(prefill_attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmem);
+    attr = true;
+  }
+  const int G = n_q / g.n_kv;
+  const int T = std::min(kPageTokens, kRows / G);
+  const int blocks_per_tile = (kPageTokens + T - 1) / T;
+  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
+  return launch_pdl(prefill_attn_tc_kernel<HD>, dim3(n_tiles * blocks_per_tile, g.n_kv),
+                    dim3(kTcThreads), kSmem, st, kv_map, g, layer, q, q_row_stride, n_q, pt,
+                    pt_stride, tiles, blocks_per_tile, out, out_row_stride, scale_log2);
+}
+
+}  // namespace
+
+// tcgen05 K6 (GQA groups of <= 128 / 16 query heads share a CTA's KV pages)
+int prefill_attention_tc(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                         int q_row_stride, int n_q, const int* page_table, int pt_stride,
+                         const PrefillTile* tiles, int n_tiles, bf16* out, int out_row_stride,
+                         cudaStream_t st) {
+  if (n_tiles <= 0) return HS_OK;
+  if (n_q % g.n_kv || n_q / g.n_kv > kRows / 16) return HS_E_CONFIG;
+  if (g.head_dim == 128)
+    return launch_tc<128>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride, tiles,
+                          n_tiles, out, out_row_stride, st);
+  if (g.head_dim == 64)
+    return launch_tc<64>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride, tiles,
+                         n_tiles, out, out_row_stride, st);
+  return HS_E_CONFIG;
+}
+
+}  // namespace hs

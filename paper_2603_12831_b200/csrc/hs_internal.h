@@ -205,6 +205,11 @@ int prefill_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, con
                       int q_row_stride, int n_q, const int* page_table, int pt_stride,
                       const PrefillTile* tiles, int n_tiles, bf16* out, int out_row_stride,
                       cudaStream_t st);
+// tcgen05 / TMEM version (attn_prefill_tc.cu): GQA groups share KV pages
+int prefill_attention_tc(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                         int q_row_stride, int n_q, const int* page_table, int pt_stride,
+                         const PrefillTile* tiles, int n_tiles, bf16* out, int out_row_stride,
+                         cudaStream_t st);
 
 // ---- elementwise (elementwise.cu) ----
 int embed_gather(const int* tokens, int rows, const bf16* emb, int d, float* h, cudaStream_t st);

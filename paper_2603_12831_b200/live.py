@@ -386,7 +386,7 @@ class LiveEngine(Engine):
             return
         self.now = t
         L = self.layers
-        merges = chain_tokens = 0
+        merges = chain_tokens = merge_ctx = 0
         self._pg_bucket = []
         for layer, recs in enumerate(log, 1):
             self._pg_ship(self._pg_bucket)  # this layer's carries (merged at layer-1)
@@ -412,6 +412,7 @@ class LiveEngine(Engine):
                     self.queues.output_deq += 1
                     req.chain_state = "output"
                     item = ResultItem(rid, layer, t, w.enq_seq)
+                    merge_ctx += req.ctx
                     if layer < L:
                         out = self._process_merge(item, layer, t, t)
                     else:
@@ -429,6 +430,7 @@ class LiveEngine(Engine):
                 trace["layers"].append((layer, outcomes, self._snap([r for r, _ in recs])))
         rec["merges"] = merges
         rec["chain_tokens"] = chain_tokens
+        rec["merge_ctx"] = merge_ctx
         self._dirty = True
 
     # -- main loop ------------------------------------------------------------------------

@@ -804,6 +804,15 @@ class LiveCudaStep(CudaStep):
                 toks = toks[:len(reqs)]
                 if payload is not None:
                     payload["pg_log"] = log
+                # piggyback traffic the device moved: every merged result row
+                # (H2D), every shipped q|k|v row (D2H): chains carried into the
+                # next layer, injections, restarts
+                m = self.model
+                n_res = sum(1 for recs in log for _, f in recs if not f & 1)
+                n_ship = (sum(1 for recs in log[:-1] for _, f in recs if not f & 1)
+                          + sum(1 for recs in log for _, f in recs if f & 3))
+                self.h2d_bytes += n_res * m.result_bytes
+                self.d2h_bytes += n_ship * m.ship_bytes
             elif len(toks) != len(reqs):
                 raise RuntimeError(f"libhs returned {len(toks)} tokens for {len(reqs)} rows")
             if self.trace_tokens:
