@@ -12,19 +12,23 @@
 // 128 MMA rows pack every query head of the KV head's GQA group: row =
 // token * G + g (G = n_q / n_kv; 128/G tokens per block, at most the tile's
 // 64), so each KV page is read once per group instead of once per query
-// head.  Per 64-key page:
+// head.  Per 64-key page i:
 //
-//   S    = Q K^T     tcgen05.mma M=128 N=64  K=hd   (A = Q, K-major, smem;
-//                                                   B = K page, K-major, TMA)
-//   P    = exp2(S*scale - m), online max / sum in registers (one TMEM lane =
-//          one row per thread of warps 0-3), P written to smem (SW128)
-//   Otmp = P V       tcgen05.mma M=128 N=hd K=64    (A = P, K-major;
-//                                                   B = V page, MN-major)
-//   O    = O * alpha + Otmp  in registers
+//   S_i = Q K_i^T      tcgen05.mma M=128 N=64 K=hd into TMEM (double-buffered,
+//                      issued two pages ahead; A = Q K-major smem, B = the K
+//                      page K-major as TMA staged it)
+//   P_i = exp2(S_i*scale - m), one TMEM lane (row) per thread of warps 0-3;
+//         bf16 P to smem (SWIZZLE_128B, K-major)
+//   O  += P_i V_i      tcgen05.mma M=128 N=hd K=64, accumulated in TMEM
+//                      (B = the V page, MN-major)
 //
-// Warp 4 issues the TMA page loads (2-stage ring) and, from one thread, the
-// MMAs; S of the next page is issued as soon as the softmax threads have
-// read the current one, so it overlaps the O update.
+// The running max m only moves when a row's max grows by more than 2^8
+// (lazy rescaling): P <= 256 stays exact enough in bf16 and O in TMEM is
+// rescaled (tcgen05.ld / st) only on those rare pages, so the per-page work
+// on the CUDA cores is the S read-out, 64 exp2 and the P store.  Warp 4
+// issues the TMA page loads (2-stage ring) and, from one thread, every MMA.
+// ~112 KB of shared memory and 256 TMEM columns: two CTAs per SM, so one
+// CTA's softmax overlaps the other's MMAs.
 #include <math_constants.h>
 
 #include <algorithm>
@@ -36,13 +40,14 @@ namespace hs {
 
 namespace {
 
-constexpr int kTcStages = 2;
+constexpr int kTcStages = 4;
 constexpr int kTcSoftmaxThreads = 128;  // warps 0-3: one TMEM lane (row) each
 constexpr int kTcThreads = kTcSoftmaxThreads + 32;
 constexpr int kRows = 128;              // MMA M
-constexpr int kSCol = 0;                // TMEM columns of S (64)
-constexpr int kOCol = 128;              // TMEM columns of the P.V product (hd)
+constexpr int kSCol = 0;                // TMEM columns of S (2 x 64)
+constexpr int kOCol = 128;              // TMEM columns of O (hd)
 constexpr int kTmemCols = 256;
+constexpr float kRescaleLog2 = 8.0f;    // lazy-rescale threshold (P <= 2^8)
 
 // MN-major SWIZZLE_128B operand (the V page as staged by TMA: keys are
 // rows of 128 B holding 64 hd elements): LBO = byte distance between
@@ -60,6 +65,32 @@ __device__ __forceinline__ uint64_t umma_desc_mn128(uint32_t smem_addr, uint32_t
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// 32 lanes x 16 columns, no wait (batch several, then tmem_wait_ld)
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
 template <int HD>
@@ -83,7 +114,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint8_t* sP = sQ + kQBytes;
   uint8_t* sKV = sP + kPBytes;
   __shared__ uint64_t kv_full[kTcStages], kv_empty[kTcStages];
-  __shared__ uint64_t s_full, p_full, o_full;
+  __shared__ uint64_t s_full[2], p_full, o_full;
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -104,7 +135,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(&s_full, 1);
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
     mbar_init(&p_full, kTcSoftmaxThreads);
     mbar_init(&o_full, 1);
     fence_mbar_init();
@@ -153,7 +185,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t id_s = umma_idesc_bf16(kRows, kPageTokens);
       const uint32_t id_o = umma_idesc_bf16(kRows, HD) | (1u << 16);  // B (V) MN-major
       const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
-      auto mma_s = [&](int i) {  // S = Q K_i^T
+      auto mma_s = [&](int i) {  // S_i = Q K_i^T into S buffer i & 1
         const int s = i % kTcStages;
         mbar_wait(&kv_full[s], (i / kTcStages) & 1);
         tc_fence_after();
@@ -162,47 +194,49 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int j = 0; j < kKSteps; ++j) {
           const uint32_t off_a = (j >> 2) * (kRows * 128) + (j & 3) * 32;
           const uint32_t off_b = (j >> 2) * kBox + (j & 3) * 32;
-          umma_bf16(tmem + kSCol, umma_desc_k128(q_base + off_a), umma_desc_k128(k_base + off_b),
-                    id_s, j > 0);
+          umma_bf16(tmem + kSCol + (i & 1) * kPageTokens, umma_desc_k128(q_base + off_a),
+                    umma_desc_k128(k_base + off_b), id_s, j > 0);
         }
-        umma_commit(&s_full);
+        umma_commit(&s_full[i & 1]);
       };
       mma_s(0);
+      if (npages > 1) mma_s(1);
       for (int i = 0; i < npages; ++i) {
         const int s = i % kTcStages;
-        mbar_wait(&p_full, i & 1);  // P_i in smem, S_i and O_{i-1} read out of TMEM
+        mbar_wait(&p_full, i & 1);  // P_i in smem, S_i read out, O rescaled if needed
         tc_fence_after();
         const uint32_t v_base = smem_u32(sKV + s * kStageBytes + kKvBytes);
 #pragma unroll
-        for (int j = 0; j < kPageTokens / 16; ++j)  // Otmp = P_i V_i (16 keys per step)
+        for (int j = 0; j < kPageTokens / 16; ++j)  // O += P_i V_i (16 keys per step)
           umma_bf16(tmem + kOCol, umma_desc_k128(p_base + j * 32),
-                    umma_desc_mn128(v_base + j * 2048, kBox), id_o, j > 0);
+                    umma_desc_mn128(v_base + j * 2048, kBox), id_o, (i | j) != 0);
         umma_commit(&o_full);
         umma_commit(&kv_empty[s]);
-        if (i + 1 < npages) mma_s(i + 1);
         if (i + kTcStages < npages) {
-          mbar_wait(&kv_empty[s], (i / kTcStages) & 1);
+          mbar_wait(&kv_empty[s], (i / kTcStages) & 1);  // K_i, V_i consumed
           issue(i + kTcStages);
         }
+        if (i + 2 < npages) mma_s(i + 2);  // S buffer i & 1 was read out (p_full_i)
       }
     }
   } else {
-    // softmax / accumulation: thread = TMEM lane = MMA row
+    // softmax: thread = TMEM lane = MMA row
     const uint32_t t_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    float o[HD];
-#pragma unroll
-    for (int d = 0; d < HD; ++d) o[d] = 0.f;
     float m = -CUDART_INF_F, l = 0.f;
     for (int i = 0; i < npages; ++i) {
-      mbar_wait(&s_full, i & 1);
+      mbar_wait(&s_full[i & 1], (i >> 1) & 1);
       tc_fence_after();
       float sv[kPageTokens];
+      {
+        uint32_t r[4][16];
 #pragma unroll
-      for (int c = 0; c < kPageTokens / 16; ++c) {
-        float v[16];
-        tmem_ld16(t_row + kSCol + c * 16, v);
+        for (int c = 0; c < 4; ++c)
+          tmem_ld16_nw(t_row + kSCol + (i & 1) * kPageTokens + c * 16, r[c]);
+        tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 16; ++e) sv[c * 16 + e] = v[e];
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) sv[c * 16 + e] = __uint_as_float(r[c][e]);
       }
       const int kbase = i * kPageTokens;
       float mx = -CUDART_INF_F;
@@ -211,10 +245,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         sv[j] = (valid && kbase + j <= pos) ? sv[j] * scale_log2 : -CUDART_INF_F;
         mx = fmaxf(mx, sv[j]);
       }
-      const float mn = fmaxf(m, mx);
-      const float mu = mn == -CUDART_INF_F ? 0.f : mn;
-      const float alpha = exp2f(m - mu);
-      m = mn;
+      // lazy rescale: move m only when the row max outgrows it by 2^8
+      const bool grow = mx > m + kRescaleLog2;
+      const float m_new = grow ? mx : m;
+      const float alpha = grow ? exp2f(m - m_new) : 1.f;  // 0 on the first page
+      m = m_new;
+      const float mu = m == -CUDART_INF_F ? 0.f : m;
+      // the previous page's P.V must be done before P is rewritten and
+      // before O is rescaled
+      if (i > 0) {
+        mbar_wait(&o_full, (i - 1) & 1);
+        tc_fence_after();
+      }
+      if (i > 0 && __any_sync(0xffffffffu, grow)) {  // O *= alpha (warp-collective)
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c) {
+          uint32_t r[16];
+          tmem_ld16_nw(t_row + kOCol + c * 16, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+          tmem_st16(t_row + kOCol + c * 16, r);
+        }
+        tmem_wait_st();
+      }
       float rs = 0.f;
 #pragma unroll
       for (int c = 0; c < kPageTokens / 8; ++c) {  // P row -> smem (K-major SW128)
@@ -235,29 +289,29 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&p_full);
-      mbar_wait(&o_full, i & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < HD / 16; ++c) {
-        float v[16];
-        tmem_ld16(t_row + kOCol + c * 16, v);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) o[c * 16 + e] = o[c * 16 + e] * alpha + v[e];
-      }
-      tc_fence_before();
     }
-    if (valid) {
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      bf16* dst = out + static_cast<size_t>(tile.q_row + t0 + tok) * out_row_stride +
-                  static_cast<size_t>(kvh * G + gh) * HD;
+    mbar_wait(&o_full, (npages - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    bf16* dst = out + static_cast<size_t>(tile.q_row + t0 + tok) * out_row_stride +
+                static_cast<size_t>(kvh * G + gh) * HD;
 #pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
-        uint4 w;
-        w.x = pack_bf16x2(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
-        w.y = pack_bf16x2(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
-        w.z = pack_bf16x2(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
-        w.w = pack_bf16x2(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
-        reinterpret_cast<uint4*>(dst)[c] = w;
+    for (int c = 0; c < HD / 16; ++c) {
+      uint32_t r[16];
+      tmem_ld16_nw(t_row + kOCol + c * 16, r);
+      tmem_wait_ld();
+      if (valid) {
+        uint4 w0, w1;
+        w0.x = pack_bf16x2(__uint_as_float(r[0]) * inv, __uint_as_float(r[1]) * inv);
+        w0.y = pack_bf16x2(__uint_as_float(r[2]) * inv, __uint_as_float(r[3]) * inv);
+        w0.z = pack_bf16x2(__uint_as_float(r[4]) * inv, __uint_as_float(r[5]) * inv);
+        w0.w = pack_bf16x2(__uint_as_float(r[6]) * inv, __uint_as_float(r[7]) * inv);
+        w1.x = pack_bf16x2(__uint_as_float(r[8]) * inv, __uint_as_float(r[9]) * inv);
+        w1.y = pack_bf16x2(__uint_as_float(r[10]) * inv, __uint_as_float(r[11]) * inv);
+        w1.z = pack_bf16x2(__uint_as_float(r[12]) * inv, __uint_as_float(r[13]) * inv);
+        w1.w = pack_bf16x2(__uint_as_float(r[14]) * inv, __uint_as_float(r[15]) * inv);
+        reinterpret_cast<uint4*>(dst)[2 * c] = w0;
+        reinterpret_cast<uint4*>(dst)[2 * c + 1] = w1;
       }
     }
   }

@@ -44,7 +44,7 @@ class FakeHsContext:
         self.pages: dict[int, int] = {}
         self._rows_logit = 0
         self._merge_last = 0
-        self.calls = {"iter_begin": 0, "layer": 0, "cpu_submit": 0, "swap": 0}
+        self.calls = {"iter_begin": 0, "layer": 0, "cpu_submit": 0, "swap": 0, "merged": 0}
         self.max_rows_seen = 0
 
     # device queue model: work is serial on one stream
@@ -98,6 +98,7 @@ class FakeHsContext:
         if layer == self.model.n_layers:
             self._merge_last = len(merge_slot)
         self.calls["layer"] += 1
+        self.calls["merged"] += len(merge_slot) + len(carry_slot)
         self.lib.launches += 9
         self._enqueue(self.iter_s / self.model.n_layers)
 
@@ -121,6 +122,28 @@ class FakeHsContext:
         self.iters.append((self.busy_until, self._rows_logit + self._merge_last))
         self._merge_last = 0
         return len(self.iters) - 1
+
+    # synchronous (replay) entry points
+    def iter_end(self):
+        n = self._rows_logit + self._merge_last
+        self._merge_last = 0
+        self.calls["iter_end"] = self.calls.get("iter_end", 0) + 1
+        return np.arange(n, dtype=np.int32) % max(self.model.vocab, 1)
+
+    def cpu_attend(self, slots, layers, ctxs):
+        for s, l, c in zip(slots, layers, ctxs):
+            assert s in self.host_kv and 1 <= l <= self.model.n_layers
+            assert 0 < c + 1 <= self.host_kv[s], ("ctx beyond the host reservation", s, c)
+        self.calls["cpu_attend"] = self.calls.get("cpu_attend", 0) + len(slots)
+
+    def swap_out(self, slot, tokens):
+        assert slot in self.host_kv and 0 < tokens <= self.host_kv[slot]
+        self.calls["swap"] += 1
+
+    def swap_in(self, slot, tokens):
+        assert slot in self.host_kv and tokens > 0
+        assert tokens <= 64 * self.pages.get(slot, 0), ("swap-in beyond the slot's pages", slot)
+        self.calls["swap"] += 1
 
     def iter_poll(self, ticket):
         done, n = self.iters[ticket]
