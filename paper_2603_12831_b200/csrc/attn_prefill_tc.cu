@@ -9,26 +9,27 @@
 // flops per pair, the step's only tensor-bound attention.
 //
 // One CTA per (block of query tokens of one prefill tile, KV head).  The
-// 128 MMA rows pack every query head of the KV head's GQA group: row =
-// token * G + g (G = n_q / n_kv; 128/G tokens per block, at most the tile's
-// 64), so each KV page is read once per group instead of once per query
-// head.  Per 64-key page i:
+// MMA rows pack every query head of the KV head's GQA group: row = token * G
+// + g (G = n_q / n_kv), so each KV page is read once per group instead of
+// once per query head; a CTA holds NT = 1 or 2 Q tiles of 128 rows (2 when
+// the launch still fills every SM: two tiles share each staged page, half
+// the KV traffic per flop).  Per 64-key page i and Q tile t:
 //
-//   S_i = Q K_i^T      tcgen05.mma M=128 N=64 K=hd into TMEM (double-buffered,
+//   S_i = Q_t K_i^T    tcgen05.mma M=128 N=64 K=hd into TMEM (double-buffered,
 //                      issued two pages ahead; A = Q K-major smem, B = the K
 //                      page K-major as TMA staged it)
-//   P_i = exp2(S_i*scale - m), one TMEM lane (row) per thread of warps 0-3;
-//         bf16 P to smem (SWIZZLE_128B, K-major)
-//   O  += P_i V_i      tcgen05.mma M=128 N=hd K=64, accumulated in TMEM
+//   P_i = exp2(S_i*scale - m), one TMEM lane (row) per thread of the tile's
+//         four warps; bf16 P to smem (SWIZZLE_128B, K-major)
+//   O_t += P_i V_i     tcgen05.mma M=128 N=hd K=64, accumulated in TMEM
 //                      (B = the V page, MN-major)
 //
 // The running max m only moves when a row's max grows by more than 2^8
 // (lazy rescaling): P <= 256 stays exact enough in bf16 and O in TMEM is
 // rescaled (tcgen05.ld / st) only on those rare pages, so the per-page work
-// on the CUDA cores is the S read-out, 64 exp2 and the P store.  Warp 4
-// issues the TMA page loads (2-stage ring) and, from one thread, every MMA.
-// ~112 KB of shared memory and 256 TMEM columns: two CTAs per SM, so one
-// CTA's softmax overlaps the other's MMAs.
+// on the CUDA cores is the S read-out, 64 exp2 and the P store.  The last
+// warp issues the TMA page loads (4-stage ring: the KV stream is latency-
+// bound with fewer bytes in flight) and, from one thread, every MMA.  One
+// CTA per SM (up to 225 KB of shared memory, 512 TMEM columns).
 #include <math_constants.h>
 
 #include <algorithm>
@@ -41,13 +42,18 @@ namespace hs {
 namespace {
 
 constexpr int kTcStages = 4;
-constexpr int kTcSoftmaxThreads = 128;  // warps 0-3: one TMEM lane (row) each
-constexpr int kTcThreads = kTcSoftmaxThreads + 32;
+constexpr int kMaxTiles = 2;            // Q tiles of 128 rows sharing each KV page
+constexpr int kTcSoftmaxThreads = 128;  // per tile: warps 4t..4t+3, one TMEM lane (row) each
 constexpr int kRows = 128;              // MMA M
-constexpr int kSCol = 0;                // TMEM columns of S (2 x 64)
-constexpr int kOCol = 128;              // TMEM columns of O (hd)
-constexpr int kTmemCols = 256;
 constexpr float kRescaleLog2 = 8.0f;    // lazy-rescale threshold (P <= 2^8)
+
+// TMEM columns with NT tiles: S (2 buffers x NT x 64), then O (NT x 128)
+template <int NT>
+__host__ __device__ constexpr int s_col(int buf, int t) { return (buf * NT + t) * 64; }
+template <int NT>
+__host__ __device__ constexpr int o_col(int t) { return NT * 128 + t * 128; }
+template <int NT>
+constexpr int kTmemCols = NT * 256;
 
 // MN-major SWIZZLE_128B operand (the V page as staged by TMA: keys are
 // rows of 128 B holding 64 hd elements): LBO = byte distance between
@@ -93,8 +99,8 @@ __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-template <int HD>
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int HD, int NT>
+__global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
     prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, KvGeom geom, int layer,
                            const bf16* __restrict__ q, int q_row_stride, int n_q,
                            const int* __restrict__ page_table, int pt_stride,
@@ -103,31 +109,33 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   constexpr int kBox = kPageTokens * 128;       // one [64 keys][64 el] SW128 box
   constexpr int kKvBytes = (HD / 64) * kBox;    // K or V of one page
   constexpr int kStageBytes = 2 * kKvBytes;
-  constexpr int kQBytes = (HD / 64) * kRows * 128;
-  constexpr int kPBytes = kRows * 128;          // P: 128 rows x 64 keys bf16
+  constexpr int kQBytes = (HD / 64) * kRows * 128;  // one Q tile
+  constexpr int kPBytes = kRows * 128;          // one P tile: 128 rows x 64 keys bf16
   constexpr int kKSteps = HD / 16;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sP = sQ + kQBytes;
-  uint8_t* sKV = sP + kPBytes;
+  uint8_t* sQ = smem;                       // [tile][kQBytes]
+  uint8_t* sP = sQ + NT * kQBytes;      // [tile][kPBytes]
+  uint8_t* sKV = sP + NT * kPBytes;
   __shared__ uint64_t kv_full[kTcStages], kv_empty[kTcStages];
-  __shared__ uint64_t s_full[2], p_full, o_full;
+  __shared__ uint64_t s_full[NT][2], p_full[NT], o_full[NT];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const PrefillTile tile = tiles[blockIdx.x / blocks_per_tile];
   const int kvh = blockIdx.y;
   const int G = n_q / geom.n_kv;
-  const int T = min(kPageTokens, kRows / G);              // tokens per block
+  const int T = min(kPageTokens, NT * kRows / G);     // tokens per block
   const int t0 = (blockIdx.x % blocks_per_tile) * T;      // first token of the block
   const int nt = min(T, tile.nq - t0);                    // tokens of this block
   if (nt <= 0) return;                                    // (uniform per CTA)
+  const int n_tiles = (nt * G + kRows - 1) / kRows;       // Q tiles with rows (1 or 2)
   const int last_pos = tile.pos0 + t0 + nt - 1;
   const int npages = last_pos / kPageTokens + 1;
   const int* pt = page_table + static_cast<size_t>(tile.slot) * pt_stride;
+  const int mma_warp = NT * 4;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&kv_map);
@@ -135,29 +143,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(&s_full[0], 1);
-    mbar_init(&s_full[1], 1);
-    mbar_init(&p_full, kTcSoftmaxThreads);
-    mbar_init(&o_full, 1);
+    for (int t = 0; t < NT; ++t) {
+      mbar_init(&s_full[t][0], 1);
+      mbar_init(&s_full[t][1], 1);
+      mbar_init(&p_full[t], kTcSoftmaxThreads);
+      mbar_init(&o_full[t], 1);
+    }
     fence_mbar_init();
   }
-  if (warp == 4) tmem_alloc<kTmemCols>(&tmem_base_sh);
+  if (warp == mma_warp) tmem_alloc<kTmemCols<NT>>(&tmem_base_sh);
   pdl_wait();  // q (QKV epilogue) and this layer's K/V pages are written
   pdl_trigger();
 
-  // this thread's MMA row (softmax warps): token t0 + row/G, head kvh*G + row%G
-  const int row = threadIdx.x;
-  const int tok = row / G, gh = row % G;
-  const bool valid = warp < 4 && tok < nt;
+  // softmax threads: tile qt, row (TMEM lane) r; block row = qt*128 + r is
+  // token t0 + row/G of head kvh*G + row%G
+  const int qt = warp >> 2, r = threadIdx.x & (kRows - 1);
+  const int brow = threadIdx.x;
+  const int tok = brow / G, gh = brow % G;
+  const bool valid = warp < mma_warp && tok < nt;
   const int pos = tile.pos0 + t0 + tok;
-  if (warp < 4) {  // Q row -> smem, K-major SWIZZLE_128B
+  if (warp < mma_warp && qt < n_tiles) {  // Q row -> smem, K-major SWIZZLE_128B
     const bf16* src = q + static_cast<size_t>(tile.q_row + t0 + tok) * q_row_stride +
                       static_cast<size_t>(kvh * G + gh) * HD;
+    uint8_t* dq = sQ + qt * kQBytes;
 #pragma unroll
     for (int c = 0; c < HD / 8; ++c) {
       uint4 v = valid ? reinterpret_cast<const uint4*>(src)[c] : make_uint4(0, 0, 0, 0);
       const int kb = c >> 3, cc = c & 7;
-      *reinterpret_cast<uint4*>(sQ + kb * (kRows * 128) + row * 128 + ((cc ^ (row & 7)) << 4)) = v;
+      *reinterpret_cast<uint4*>(dq + kb * (kRows * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
     }
     fence_proxy_async_smem();
   }
@@ -166,7 +179,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
-  if (warp == 4) {
+  if (warp == mma_warp) {
     if (lane == 0) {
       auto issue = [&](int i) {
         const int s = i % kTcStages;
@@ -184,33 +197,38 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int i = 0; i < min(kTcStages, npages); ++i) issue(i);
       const uint32_t id_s = umma_idesc_bf16(kRows, kPageTokens);
       const uint32_t id_o = umma_idesc_bf16(kRows, HD) | (1u << 16);  // B (V) MN-major
-      const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
-      auto mma_s = [&](int i) {  // S_i = Q K_i^T into S buffer i & 1
+      auto mma_s = [&](int i) {  // S_i = Q K_i^T of every tile into S buffer i & 1
         const int s = i % kTcStages;
         mbar_wait(&kv_full[s], (i / kTcStages) & 1);
         tc_fence_after();
         const uint32_t k_base = smem_u32(sKV + s * kStageBytes);
+        for (int t = 0; t < n_tiles; ++t) {
+          const uint32_t q_base = smem_u32(sQ + t * kQBytes);
 #pragma unroll
-        for (int j = 0; j < kKSteps; ++j) {
-          const uint32_t off_a = (j >> 2) * (kRows * 128) + (j & 3) * 32;
-          const uint32_t off_b = (j >> 2) * kBox + (j & 3) * 32;
-          umma_bf16(tmem + kSCol + (i & 1) * kPageTokens, umma_desc_k128(q_base + off_a),
-                    umma_desc_k128(k_base + off_b), id_s, j > 0);
+          for (int j = 0; j < kKSteps; ++j) {
+            const uint32_t off_a = (j >> 2) * (kRows * 128) + (j & 3) * 32;
+            const uint32_t off_b = (j >> 2) * kBox + (j & 3) * 32;
+            umma_bf16(tmem + s_col<NT>(i & 1, t), umma_desc_k128(q_base + off_a),
+                      umma_desc_k128(k_base + off_b), id_s, j > 0);
+          }
+          umma_commit(&s_full[t][i & 1]);
         }
-        umma_commit(&s_full[i & 1]);
       };
       mma_s(0);
       if (npages > 1) mma_s(1);
       for (int i = 0; i < npages; ++i) {
         const int s = i % kTcStages;
-        mbar_wait(&p_full, i & 1);  // P_i in smem, S_i read out, O rescaled if needed
-        tc_fence_after();
         const uint32_t v_base = smem_u32(sKV + s * kStageBytes + kKvBytes);
+        for (int t = 0; t < n_tiles; ++t) {
+          mbar_wait(&p_full[t], i & 1);  // P_i in smem, S_i read out, O rescaled if needed
+          tc_fence_after();
+          const uint32_t p_base = smem_u32(sP + t * kPBytes);
 #pragma unroll
-        for (int j = 0; j < kPageTokens / 16; ++j)  // O += P_i V_i (16 keys per step)
-          umma_bf16(tmem + kOCol, umma_desc_k128(p_base + j * 32),
-                    umma_desc_mn128(v_base + j * 2048, kBox), id_o, (i | j) != 0);
-        umma_commit(&o_full);
+          for (int j = 0; j < kPageTokens / 16; ++j)  // O += P_i V_i (16 keys per step)
+            umma_bf16(tmem + o_col<NT>(t), umma_desc_k128(p_base + j * 32),
+                      umma_desc_mn128(v_base + j * 2048, kBox), id_o, (i | j) != 0);
+          umma_commit(&o_full[t]);
+        }
         umma_commit(&kv_empty[s]);
         if (i + kTcStages < npages) {
           mbar_wait(&kv_empty[s], (i / kTcStages) & 1);  // K_i, V_i consumed
@@ -219,24 +237,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (i + 2 < npages) mma_s(i + 2);  // S buffer i & 1 was read out (p_full_i)
       }
     }
-  } else {
-    // softmax: thread = TMEM lane = MMA row
-    const uint32_t t_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  } else if (qt < n_tiles) {
+    // softmax: thread = TMEM lane = MMA row of tile qt
+    const uint32_t t_row = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    uint8_t* sPt = sP + qt * kPBytes;
     float m = -CUDART_INF_F, l = 0.f;
     for (int i = 0; i < npages; ++i) {
-      mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+      mbar_wait(&s_full[qt][i & 1], (i >> 1) & 1);
       tc_fence_after();
       float sv[kPageTokens];
       {
-        uint32_t r[4][16];
+        uint32_t rr[4][16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          tmem_ld16_nw(t_row + kSCol + (i & 1) * kPageTokens + c * 16, r[c]);
+        for (int c = 0; c < 4; ++c) tmem_ld16_nw(t_row + s_col<NT>(i & 1, qt) + c * 16, rr[c]);
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int e = 0; e < 16; ++e) sv[c * 16 + e] = __uint_as_float(r[c][e]);
+          for (int e = 0; e < 16; ++e) sv[c * 16 + e] = __uint_as_float(rr[c][e]);
       }
       const int kbase = i * kPageTokens;
       float mx = -CUDART_INF_F;
@@ -254,18 +272,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // the previous page's P.V must be done before P is rewritten and
       // before O is rescaled
       if (i > 0) {
-        mbar_wait(&o_full, (i - 1) & 1);
+        mbar_wait(&o_full[qt], (i - 1) & 1);
         tc_fence_after();
       }
       if (i > 0 && __any_sync(0xffffffffu, grow)) {  // O *= alpha (warp-collective)
 #pragma unroll
         for (int c = 0; c < HD / 16; ++c) {
-          uint32_t r[16];
-          tmem_ld16_nw(t_row + kOCol + c * 16, r);
+          uint32_t rr[16];
+          tmem_ld16_nw(t_row + o_col<NT>(qt) + c * 16, rr);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          tmem_st16(t_row + kOCol + c * 16, r);
+          for (int e = 0; e < 16; ++e) rr[e] = __float_as_uint(__uint_as_float(rr[e]) * alpha);
+          tmem_st16(t_row + o_col<NT>(qt) + c * 16, rr);
         }
         tmem_wait_st();
       }
@@ -282,34 +300,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           rs += __bfloat162float(r2.x) + __bfloat162float(r2.y);
           w[e] = pk;
         }
-        *reinterpret_cast<uint4*>(sP + row * 128 + ((c ^ (row & 7)) << 4)) =
+        *reinterpret_cast<uint4*>(sPt + r * 128 + ((c ^ (r & 7)) << 4)) =
             make_uint4(w[0], w[1], w[2], w[3]);
       }
       l = l * alpha + rs;
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(&p_full);
+      mbar_arrive(&p_full[qt]);
     }
-    mbar_wait(&o_full, (npages - 1) & 1);
+    mbar_wait(&o_full[qt], (npages - 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     bf16* dst = out + static_cast<size_t>(tile.q_row + t0 + tok) * out_row_stride +
                 static_cast<size_t>(kvh * G + gh) * HD;
 #pragma unroll
     for (int c = 0; c < HD / 16; ++c) {
-      uint32_t r[16];
-      tmem_ld16_nw(t_row + kOCol + c * 16, r);
+      uint32_t rr[16];
+      tmem_ld16_nw(t_row + o_col<NT>(qt) + c * 16, rr);
       tmem_wait_ld();
       if (valid) {
         uint4 w0, w1;
-        w0.x = pack_bf16x2(__uint_as_float(r[0]) * inv, __uint_as_float(r[1]) * inv);
-        w0.y = pack_bf16x2(__uint_as_float(r[2]) * inv, __uint_as_float(r[3]) * inv);
-        w0.z = pack_bf16x2(__uint_as_float(r[4]) * inv, __uint_as_float(r[5]) * inv);
-        w0.w = pack_bf16x2(__uint_as_float(r[6]) * inv, __uint_as_float(r[7]) * inv);
-        w1.x = pack_bf16x2(__uint_as_float(r[8]) * inv, __uint_as_float(r[9]) * inv);
-        w1.y = pack_bf16x2(__uint_as_float(r[10]) * inv, __uint_as_float(r[11]) * inv);
-        w1.z = pack_bf16x2(__uint_as_float(r[12]) * inv, __uint_as_float(r[13]) * inv);
-        w1.w = pack_bf16x2(__uint_as_float(r[14]) * inv, __uint_as_float(r[15]) * inv);
+        w0.x = pack_bf16x2(__uint_as_float(rr[0]) * inv, __uint_as_float(rr[1]) * inv);
+        w0.y = pack_bf16x2(__uint_as_float(rr[2]) * inv, __uint_as_float(rr[3]) * inv);
+        w0.z = pack_bf16x2(__uint_as_float(rr[4]) * inv, __uint_as_float(rr[5]) * inv);
+        w0.w = pack_bf16x2(__uint_as_float(rr[6]) * inv, __uint_as_float(rr[7]) * inv);
+        w1.x = pack_bf16x2(__uint_as_float(rr[8]) * inv, __uint_as_float(rr[9]) * inv);
+        w1.y = pack_bf16x2(__uint_as_float(rr[10]) * inv, __uint_as_float(rr[11]) * inv);
+        w1.z = pack_bf16x2(__uint_as_float(rr[12]) * inv, __uint_as_float(rr[13]) * inv);
+        w1.w = pack_bf16x2(__uint_as_float(rr[14]) * inv, __uint_as_float(rr[15]) * inv);
         reinterpret_cast<uint4*>(dst)[2 * c] = w0;
         reinterpret_cast<uint4*>(dst)[2 * c + 1] = w1;
       }
@@ -317,31 +335,52 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == mma_warp) {
     tc_fence_after();
-    tmem_free<kTmemCols>(tmem);
+    tmem_free<kTmemCols<NT>>(tmem);
   }
 }
 
+template <int HD, int NT>
+int launch_tc_nt(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
+                 int q_row_stride, int n_q, const int* pt, int pt_stride,
+                 const PrefillTile* tiles, int n_tiles, bf16* out, int out_row_stride,
+                 cudaStream_t st) {
+  constexpr int kSmem = NT * ((HD / 64) * kRows * 128 + kRows * 128) +
+                        kTcStages * 2 * (HD / 64) * kPageTokens * 128 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(prefill_attn_tc_kernel<HD, NT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  const int G = n_q / g.n_kv;
+  const int T = std::min(kPageTokens, NT * kRows / G);
+  const int blocks_per_tile = (kPageTokens + T - 1) / T;
+  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
+  return launch_pdl(prefill_attn_tc_kernel<HD, NT>, dim3(n_tiles * blocks_per_tile, g.n_kv),
+                    dim3(NT * kTcSoftmaxThreads + 32), kSmem, st, kv_map, g, layer, q,
+                    q_row_stride, n_q, pt, pt_stride, tiles, blocks_per_tile, out,
+                    out_row_stride, scale_log2);
+}
+
+// Two Q tiles per CTA halve the KV traffic per flop, but only pay while the
+// launch still covers most SMs (one CTA per SM: 225 KB smem, 512 TMEM cols;
+// measured at 32k context: 128 two-tile CTAs 1088 us vs 256 one-tile 1146)
 template <int HD>
 int launch_tc(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
               int q_row_stride, int n_q, const int* pt, int pt_stride, const PrefillTile* tiles,
               int n_tiles, bf16* out, int out_row_stride, cudaStream_t st) {
-  constexpr int kSmem = (HD / 64) * kRows * 128 + kRows * 128 +
-                        kTcStages * 2 * (HD / 64) * kPageTokens * 128 + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(prefill_attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmem);
-    attr = true;
-  }
   const int G = n_q / g.n_kv;
-  const int T = std::min(kPageTokens, kRows / G);
-  const int blocks_per_tile = (kPageTokens + T - 1) / T;
-  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
-  return launch_pdl(prefill_attn_tc_kernel<HD>, dim3(n_tiles * blocks_per_tile, g.n_kv),
-                    dim3(kTcThreads), kSmem, st, kv_map, g, layer, q, q_row_stride, n_q, pt,
-                    pt_stride, tiles, blocks_per_tile, out, out_row_stride, scale_log2);
+  const int bpt2 = (kPageTokens + std::min(kPageTokens, 2 * kRows / G) - 1) /
+                   std::min(kPageTokens, 2 * kRows / G);
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (3 * n_tiles * bpt2 * g.n_kv >= 2 * sms)
+    return launch_tc_nt<HD, 2>(kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, tiles,
+                               n_tiles, out, out_row_stride, st);
+  return launch_tc_nt<HD, 1>(kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, tiles,
+                             n_tiles, out, out_row_stride, st);
 }
 
 }  // namespace

@@ -138,15 +138,30 @@ def test_decode_attention_split_k(cuda, n_q, n_kv, hd, chunk_pages):
 @pytest.mark.parametrize("n_q,n_kv,hd", [(4, 2, 64), (32, 8, 128)])
 @pytest.mark.parametrize("done,q_len", [(0, 1), (0, 64), (0, 100), (130, 37), (64, 200)])
 def test_prefill_attention_causal(cuda, n_q, n_kv, hd, done, q_len):
+    _prefill_case(cuda, n_q, n_kv, hd, done, q_len)
+
+
+# the tcgen05 kernel's GQA packings (G = 1, 4, 8 query heads per KV head:
+# 13B, 8B, 70B-TP8), the two-Q-tile CTAs of large chunks (>= 2/3 of the SMs
+# busy) and a longer context
+@pytest.mark.parametrize("n_q,n_kv,hd,done,q_len", [
+    (40, 40, 128, 70, 130), (8, 1, 128, 100, 300), (16, 2, 128, 0, 129),
+    (32, 8, 128, 0, 832), (32, 8, 128, 64, 900), (32, 8, 128, 3000, 200)])
+def test_prefill_attention_gqa_and_two_tile(cuda, n_q, n_kv, hd, done, q_len):
+    _prefill_case(cuda, n_q, n_kv, hd, done, q_len)
+
+
+def _prefill_case(cuda, n_q, n_kv, hd, done, q_len):
     import torch
     from paper_2603_12831_b200 import _lib
 
     rng = np.random.default_rng(done * 13 + q_len + hd)
-    layers, pages = 1, 16
-    pool = _make_pool(rng, layers, pages, n_kv, hd)
+    layers = 1
     total = done + q_len
     npg = (total + 63) // 64
-    max_pages = 8
+    pages = max(16, npg + 2)
+    pool = _make_pool(rng, layers, pages, n_kv, hd)
+    max_pages = max(8, npg)
     pt = np.zeros((2, max_pages), np.int32)
     pt[1, :npg] = rng.permutation(pages)[:npg]
     slot = 1
