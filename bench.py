@@ -132,8 +132,18 @@ def scenario_doc(args, cores: int, ls_rate: float = None) -> dict:
         "slo": {"ttft_s": TTFT_SLO_S, "tpot_s": TPOT_SLO_S,
                 "piggyback_reserve_us": args.piggyback_reserve_us},
         "engine": {"events": False},
-        "workload": {"seed": args.seed, "ls": ls_stream(args, ls_rate)},
+        "workload": {"seed": args.seed, "ls": ls_stream(args, ls_rate),
+                     **({"be": {"rate": args.be_rate, "lengths": be_lengths(args)}}
+                        if args.be_rate > 0 else {})},
     }
+
+
+def be_lengths(args) -> dict:
+    """Arriving BE requests: longbench-like, or (config 5) 32768-token prompts
+    with 136 outputs, prefilled on the GPU (K6) and offloaded by the policy."""
+    if args.workload == "longctx":
+        return {"kind": "fixed", "prompt": 32768, "output": 136}
+    return {"source": "longbench"}
 
 
 def ls_stream(args, ls_rate: float) -> dict:
@@ -334,7 +344,7 @@ def bench_config(args, model, cpu_threads: int, world: int) -> dict:
             "model": args.config, "ls_rate_per_s": args.ls_rate, "ls_trace": args.ls_trace,
             "iterations_per_step": model.n_layers,
             "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
-            "merge_decision": args.merges,
+            "merge_decision": args.merges, "be_arrivals_per_s": args.be_rate,
             "cpu_threads_per_replica": cpu_threads, "parallelism": f"replicas x{world}",
             "l2": "working set (16 GB weights/iteration) > 126 MB L2"}
 
@@ -430,7 +440,8 @@ class Replica:
         fit_be_chains(args, model, local_world, verbose=rank == 0)
         rt = self.rt = RuntimeConfig(
             max_rows=args.max_rows, max_slots=512,
-            kv_pages=args.gpu_kv_tokens // 64 + 512 + 64, max_pages_per_req=256,
+            kv_pages=args.gpu_kv_tokens // 64 + 512 + 64,
+            max_pages_per_req=max(256, (be_cap_tokens + 127) // 64),
             max_pos=max(16384, be_cap_tokens + 64), max_chunks=8192, cpu_threads=len(workers),
             host_kv_bytes=(args.be_chains + 4) * be_cap_tokens
             * model.kv_bytes_per_token_layer * model.n_layers, device=local,
@@ -628,6 +639,8 @@ def run_ours(args) -> None:
         "config": bench_config(args, model, rep.rt.cpu_threads, world),
         "iterations_timed": len(iters), "warmup_iterations": warm_iters,
         "gpus_active": int(tot[6]),
+        "be_prefill_tok_s": (sum(i.get("be_chunk_tokens", 0) for i in iters) * world
+                             / device_max) if device_max > 0 else 0.0,
         "ls_tpot_attainment": attain, "ls_tpot_p99_ms": float(mx[2]),
         "ls_tokens": int(tot[1]), "be_tokens": int(tot[0]), "ls_gaps": int(tot[3]),
         "slo_met": bool(attain >= 0.99),
@@ -786,6 +799,10 @@ def main() -> None:
     ap.add_argument("--be-chains", type=int, default=None,
                     help="host-resident BE requests kept live (default 32; 8 for --workload longctx)")
     ap.add_argument("--ls-decodes", type=int, default=0)
+    ap.add_argument("--be-rate", type=float, default=None,
+                    help="BE arrivals per second, prefilled on the GPU and offloaded by the "
+                         "policy, on top of the host-resident decode backlog (default 0; "
+                         "0.25 with --workload longctx: 32k-token prompts)")
     ap.add_argument("--gpu-kv-tokens", type=int, default=24576)
     ap.add_argument("--max-piggyback", type=int, default=64)
     ap.add_argument("--piggyback-reserve-us", type=float, default=100.0)
@@ -809,6 +826,12 @@ def main() -> None:
     args = ap.parse_args()
     if args.be_chains is None:
         args.be_chains = 8 if args.workload == "longctx" else 32
+    if args.be_rate is None:
+        args.be_rate = 0.25 if args.workload == "longctx" else 0.0
+    if args.workload == "longctx" and args.gpu_kv_tokens == 24576:
+        # a 32k-token prompt is prefilled on the GPU: room for one next to
+        # the LS envelope (the policy offloads it after prefill)
+        args.gpu_kv_tokens = 45056
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_replicas(args.gpus))
     if args.impl == "reference":

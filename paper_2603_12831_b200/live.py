@@ -245,6 +245,7 @@ class LiveEngine(Engine):
         rec = {"start": it.start, "decodes": len(plan.ls_decode) + len(plan.be_decode_gpu),
                "ls_decodes": len(plan.ls_decode), "be_gpu_decodes": len(plan.be_decode_gpu),
                "chunk_tokens": sum(q for _, q in plan.ls_prefill_chunks + plan.be_prefill_chunks),
+               "be_chunk_tokens": sum(q for _, q in plan.be_prefill_chunks),
                "merges": it.merges_total, "batch_tokens": plan.loads.batch_tokens,
                "marks": self._collect, **ctx_sum}
         if self.device_merges:
