@@ -133,7 +133,7 @@ def scenario_doc(args, cores: int, ls_rate: float = None) -> dict:
                 "piggyback_reserve_us": args.piggyback_reserve_us},
         "engine": {"events": False},
         "workload": {"seed": args.seed, "ls": ls_stream(args, ls_rate),
-                     **({"be": {"rate": args.be_rate, "lengths": be_lengths(args)}}
+                     **({"be": {"trace": {"rate": args.be_rate}, "lengths": be_lengths(args)}}
                         if args.be_rate > 0 else {})},
     }
 
@@ -170,7 +170,7 @@ def prepopulate_be(engine, step, n: int, seed: int, start: int = 0, fixed=None) 
     out = []
     for i in range(start, start + n):
         p, o = pairs[(seed * 7919 + i) % len(pairs)]
-        spec = RequestSpec(f"BE-{i:05d}", ServiceClass.BE, p, max(o, 8), engine.now)
+        spec = RequestSpec(f"BEH-{i:05d}", ServiceClass.BE, p, max(o, 8), engine.now)
         r = SimRequest(spec)
         engine.requests[r.id] = r
         r.admitted = True
@@ -318,7 +318,7 @@ def simulator_cost(args, model) -> dict:
 
     doc = scenario_doc(args, 16)
     doc["horizon_s"] = 2.0
-    doc["workload"]["be"] = {"rate": 4.0, "lengths": {"source": "longbench"}}
+    doc["workload"]["be"] = {"trace": {"rate": 4.0}, "lengths": {"source": "longbench"}}
     path = ROOT / "profiles" / f"b200_{args.config}_models.json"
     models = profiler.load(path) if path.exists() else None
     t = time.perf_counter()
@@ -807,9 +807,12 @@ def main() -> None:
     ap.add_argument("--max-piggyback", type=int, default=64)
     ap.add_argument("--piggyback-reserve-us", type=float, default=100.0)
     ap.add_argument("--max-rows", type=int, default=4096)
-    ap.add_argument("--pace", type=int, default=2, help="layers the host may run ahead")
-    ap.add_argument("--pace-tail", type=int, default=12,
-                    help="final layers of an iteration launched unpaced (covers host planning)")
+    ap.add_argument("--pace", type=int, default=None,
+                    help="layers the host may run ahead of the GPU (default: 2 with host-decided "
+                         "merges, whose freshness it bounds; unpaced with device-decided ones)")
+    ap.add_argument("--pace-tail", type=int, default=None,
+                    help="final layers of an iteration launched unpaced (covers host planning; "
+                         "default 12 with host-decided merges)")
     ap.add_argument("--merges", default="device", choices=["device", "host"],
                     help="piggyback merge decision: GPU controller polling the completion "
                          "tags (csrc/piggyback.cu), or the host at each layer launch")
@@ -826,6 +829,10 @@ def main() -> None:
     args = ap.parse_args()
     if args.be_chains is None:
         args.be_chains = 8 if args.workload == "longctx" else 32
+    if args.pace is None:
+        args.pace = 2 if args.merges == "host" else 64
+    if args.pace_tail is None:
+        args.pace_tail = 12 if args.merges == "host" else 0
     if args.be_rate is None:
         args.be_rate = 0.25 if args.workload == "longctx" else 0.0
     if args.workload == "longctx" and args.gpu_kv_tokens == 24576:

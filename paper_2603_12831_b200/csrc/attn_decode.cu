@@ -72,6 +72,12 @@ __global__ void __launch_bounds__(kDecThreads * WG, WG == 1 ? 2 : 1)
   const int npages = ch.page_end - ch.page_begin;
   const int* pt = page_table + static_cast<size_t>(ch.slot) * pt_stride + ch.page_begin;
 
+  // the chunk's page ids, read once: the refill of a stage then issues its
+  // TMA at once instead of waiting on a dependent global load per page (the
+  // page table was uploaded ahead of the iteration: safe before the PDL wait)
+  constexpr int kPtCache = 64;
+  __shared__ int pt_s[kPtCache];
+  for (int i = threadIdx.x; i < min(npages, kPtCache); i += kThreads) pt_s[i] = pt[i];
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&kv_map);
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
@@ -81,7 +87,7 @@ __global__ void __launch_bounds__(kDecThreads * WG, WG == 1 ? 2 : 1)
 
   auto issue = [&](int i) {
     const int s = i % kStages;
-    const int phys = pt[i];
+    const int phys = i < kPtCache ? pt_s[i] : pt[i];
     uint8_t* dst = smem + s * kStageBytes;
     mbar_expect_tx(&full[s], kStageBytes);
     const int rk = static_cast<int>(kv_row(geom, layer, phys, 0, kvh));

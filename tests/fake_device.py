@@ -69,6 +69,7 @@ class FakeHsContext:
 
     def host_kv_reserve(self, slot, cap):
         assert 0 <= slot < self.rt.max_slots and cap > 0
+        assert slot not in self.host_kv, ("slot already holds a host KV region", slot)
         self.host_kv[slot] = cap
 
     def host_kv_release(self, slot):
