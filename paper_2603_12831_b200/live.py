@@ -322,15 +322,16 @@ class LiveEngine(Engine):
         merged at layer x ships at x+1 and needs another iteration), so one
         whose item the host mirror shows at layer m can be merged this
         iteration only at m .. m+lag, lag = iterations launched but not yet
-        replayed; chains injected in those iterations at 2 .. 1+lag."""
+        replayed; a chain injected in one of those (its first item is layer 1)
+        at 1 .. lag."""
         L = self.layers
         lag = self.step.iterations_in_flight()
         cnt = [0] * (L + 1)
         for w in self._order:
             for k in range(min(lag, L - 1) + 1):
                 cnt[(w.layer - 1 + k) % L + 1] += 1
-        for _ in range(injected_before):
-            for k in range(1, min(lag, L - 1) + 1):
+        for _ in range(injected_before):  # taken at layer 1 of an earlier iteration at best
+            for k in range(min(lag, L)):
                 cnt[k % L + 1] += 1
         return [min(cap, c) for c in cnt[1:]]
 
