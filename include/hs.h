@@ -330,6 +330,13 @@ int hs_pg_inject(hs_ctx* ctx, const int* slots, const int* ctx_tokens, const int
 int hs_pg_stop(hs_ctx* ctx, const int* slots, const int* stop, int n);
 int hs_pg_iter(hs_ctx* ctx, int cap, const int* merge_bound, int inject_bound);
 int hs_pg_log(hs_ctx* ctx, int ticket, int* out, int n);
+/* Tensor-parallel groups: the ranks agree on every merge.  Phase 0 moves this
+ * rank's completion tags into the POSIX shared-memory segment
+ * "<prefix>.<rank>"; after a barrier across the group, phase 1 maps the
+ * peers' segments.  Each rank's controller then merges an item only once
+ * every rank's CPU pool has finished its heads of it, so all ranks take the
+ * same decisions on the same FIFO (the ranks must issue identical calls). */
+int hs_pg_share_tags(hs_ctx* ctx, const char* prefix, int rank, int world, int phase);
 /* stream marks for launch pacing, and timing events (CUDA events on the
  * compute stream; elapsed in ms between two timer ids) */
 int hs_mark(hs_ctx* ctx);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <map>
+#include <string>
 #include <vector>
 
 #include "hs_internal.h"
@@ -49,6 +50,10 @@ struct PgDev {
   int* work_tail_d = nullptr; // published entries (mapped host)
   int* log_d = nullptr;       // per-iteration decision log (mapped host)
   const unsigned* tags = nullptr;  // completion tags (mapped host)
+  // tensor-parallel group: every rank's completion tags (shared host
+  // segments); an item is ready once all ranks' CPU pools finished it
+  const unsigned* peer_tags[8] = {};
+  int n_peer = 0;
   int list_cap = 0;           // entries per list in `lists`
   int log_stride = 0;         // ints per iteration in the log
 };
@@ -186,6 +191,11 @@ struct hs_ctx {
   int pg_inj_bound = 0;       // host bound on the layer-1 injections taken
   std::vector<int> pg_bound;  // host bound on the merges of each layer
   int pg_iter_slot = 0;       // ring slot of the iteration being issued
+  // TP groups: this rank's tags moved into a POSIX shm segment (shared with
+  // the peers) and the peers' segments mapped here
+  std::vector<std::pair<void*, size_t>> pg_shm;  // mapped segments (own first)
+  std::string pg_shm_own;                        // name to unlink on destroy
+  unsigned* pg_tag_alloc = nullptr;              // the original cudaHostAlloc tags
 };
 
 // the fp32 validation datapath of hs_layer (step_f32.cu); called after the

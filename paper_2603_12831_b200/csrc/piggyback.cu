@@ -29,8 +29,13 @@
 //
 // The host never sits between a completion and its merge: no host poll, no
 // host decision, no per-layer host<->device round trip.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "hs_common.cuh"
@@ -158,9 +163,13 @@ __global__ void pg_control_kernel(PgDev p, int layer, int n_layers, int cap, int
     bool ok = false;
     if (i < avail) {
       const int* e = p.q + static_cast<size_t>((head + i) % p.Q) * 3;
-      if (e[1] == layer)
-        ok = ld_acquire_sys(p.tags + e[0]) ==
-             static_cast<unsigned>(HS_RESULT_TAG(e[2], layer));
+      if (e[1] == layer) {
+        const unsigned want = static_cast<unsigned>(HS_RESULT_TAG(e[2], layer));
+        ok = ld_acquire_sys(p.tags + e[0]) == want;
+        // a TP group merges an item only once every rank's pool finished
+        // its heads: all ranks read the same tags, take the same decision
+        for (int r = 0; r < p.n_peer; ++r) ok = ok && ld_acquire_sys(p.peer_tags[r] + e[0]) == want;
+      }
     }
     const unsigned m = __ballot_sync(0xffffffffu, ok);
     const int run = m == 0xffffffffu ? 32 : __ffs(~m) - 1;
@@ -310,6 +319,17 @@ int pg_alloc(hs_ctx* c) {
 }
 
 void pg_free(hs_ctx* c) {
+  for (auto& seg : c->pg_shm) {
+    cudaHostUnregister(seg.first);
+    munmap(seg.first, seg.second);
+  }
+  c->pg_shm.clear();
+  if (!c->pg_shm_own.empty()) shm_unlink(c->pg_shm_own.c_str());
+  c->pg_shm_own.clear();
+  if (c->pg_tag_alloc) {  // the context frees its own allocation
+    c->tag_h = c->pg_tag_alloc;
+    c->pg_tag_alloc = nullptr;
+  }
   if (c->pg.q) cudaFree(c->pg.q);
   if (c->pg_work_h) cudaFreeHost(c->pg_work_h);
   c->pg = PgDev{};
@@ -387,8 +407,7 @@ int hs_pg_enable(hs_ctx* c, int on) {
     c->pg_on = false;
     return HS_OK;
   }
-  if (c->fp32 || c->tp_world > 1)
-    return set_error(HS_E_CONFIG, "device-polled merges: bf16 single-rank datapath only");
+  if (c->fp32) return set_error(HS_E_CONFIG, "device-polled merges: bf16 datapath only");
   if (c->pg_on) return stage_ops(c, {2, 0, 0, 0});  // re-enable: drop the queued items
   if (int rc = pg_alloc(c)) return rc;
   if (int rc = ctx_cpu_service(c)) return rc;
@@ -460,4 +479,58 @@ int hs_pg_log(hs_ctx* c, int ticket, int* out, int n) {
     for (int i = 0; i < 2 * cnt; ++i) out[k++] = e[1 + i];
   }
   return k;
+}
+
+// Tensor-parallel agreement on the merge decision: phase 0 moves this rank's
+// completion tags into the shared segment "<prefix>.<rank>"; after a barrier
+// across the group, phase 1 maps every peer's segment, so each rank's
+// controller reads all ranks' tags and they take identical decisions.
+int hs_pg_share_tags(hs_ctx* c, const char* prefix, int rank, int world, int phase) {
+  if (!c->pg_on) return set_error(HS_E_CONFIG, "device-polled merges are off");
+  if (world < 1 || world > 8 || rank < 0 || rank >= world)
+    return set_error(HS_E_CONFIG, "rank %d of %d out of range", rank, world);
+  const size_t bytes = static_cast<size_t>(c->r.max_slots) * sizeof(unsigned);
+  auto map_seg = [&](const std::string& name, bool create, void** out) -> int {
+    const int fd = shm_open(name.c_str(), create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
+    if (fd < 0) return set_error(HS_E_CONFIG, "shm_open %s failed", name.c_str());
+    if (create && ftruncate(fd, static_cast<off_t>(bytes)) != 0) {
+      close(fd);
+      return set_error(HS_E_CONFIG, "ftruncate %s failed", name.c_str());
+    }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) return set_error(HS_E_CONFIG, "mmap %s failed", name.c_str());
+    if (cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) !=
+        cudaSuccess) {
+      munmap(p, bytes);
+      return set_error(HS_E_CUDA, "cudaHostRegister %s failed", name.c_str());
+    }
+    c->pg_shm.emplace_back(p, bytes);
+    *out = p;
+    return HS_OK;
+  };
+  const std::string base = std::string(prefix) + ".";
+  if (phase == 0) {
+    PG_CK(cudaDeviceSynchronize());
+    void* p = nullptr;
+    c->pg_shm_own = base + std::to_string(rank);
+    if (int rc = map_seg(c->pg_shm_own, true, &p)) return rc;
+    std::memcpy(p, c->tag_h, bytes);  // the current tags (all retracted at start)
+    c->pg_tag_alloc = c->tag_h;
+    c->tag_h = static_cast<unsigned*>(p);
+    PG_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->tag_d), p, 0));
+    c->pg.tags = c->tag_d;
+    return HS_OK;
+  }
+  int n = 0;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) continue;
+    void* p = nullptr;
+    if (int rc = map_seg(base + std::to_string(r), false, &p)) return rc;
+    unsigned* d = nullptr;
+    PG_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), p, 0));
+    c->pg.peer_tags[n++] = d;
+  }
+  c->pg.n_peer = n;
+  return HS_OK;
 }

@@ -1094,8 +1094,8 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   const bool tp = c->tp_world > 1;  // row-parallel O / down: fused all-reduce
   if (l < 0 || l >= m.layers) return set_error(HS_E_CONFIG, "layer %d out of range", d->layer);
   const bool dev_merges = c->pg_on;  // merge decision taken on the device (piggyback.cu)
-  if (dev_merges && (c->fp32 || tp))
-    return set_error(HS_E_CONFIG, "device-polled merges: bf16 single-rank datapath only");
+  if (dev_merges && c->fp32)
+    return set_error(HS_E_CONFIG, "device-polled merges: bf16 datapath only");
   int C = d->n_carry, M = d->n_merge, R = d->n_restart;
   if (!dev_merges) {
     if (B + C > r.max_rows || B + M > r.max_rows || d->n_restart > M)

@@ -121,6 +121,7 @@ _CTX_SIGS = {
     "hs_pg_stop": [C.c_void_p, _IP, _IP, C.c_int],
     "hs_pg_iter": [C.c_void_p, C.c_int, _IP, C.c_int],
     "hs_pg_log": [C.c_void_p, C.c_int, _IP, C.c_int],
+    "hs_pg_share_tags": [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int],
 }
 _NONNEG_RETURNS = {"hs_iter_end", "hs_cpu_poll", "hs_cpu_in_flight", "hs_swap_done", "hs_mark",
                    "hs_timer", "hs_iter_poll", "hs_iter_ntokens", "hs_pg_log"}
@@ -358,6 +359,9 @@ class HsContext:
         b = _i32(bounds)
         self._call("hs_pg_iter", cap, _ip(b), inject_bound)
 
+    def pg_share_tags(self, prefix: str, rank: int, world: int, phase: int) -> None:
+        self._call("hs_pg_share_tags", prefix.encode(), rank, world, phase)
+
     def pg_log(self, ticket: int) -> list[list[tuple[int, int]]]:
         """Per layer (1..L): [(slot, flags)] decided by the device."""
         if not hasattr(self, "_pg_buf"):
@@ -462,7 +466,7 @@ class CudaStep(LayerStep):
         self.ctx = ctx if ctx is not None else HsContext(model, self.rt)
         if weights is not None:
             self.ctx.load_weights(weights)
-        else:
+        elif ctx is None:  # a caller-built context already holds its weights
             self.ctx.init_weights(weight_seed)
         self.keep = keep_logits
         if keep_logits:
@@ -733,6 +737,9 @@ class LiveCudaStep(CudaStep):
     def end_iteration(self, plan, payload=None) -> None:
         """Queue the token readback; the iteration completes asynchronously."""
         ticket = self.ctx.iter_end_async()
+        flush = getattr(self.ctx, "flush", None)
+        if flush is not None:  # TP group leader: ship this iteration's calls to the followers
+            flush()
         reqs = list(self._logit_reqs) if self.device_merges else self._logit_reqs + self._merge_L
         self._inflight.append((ticket, reqs, payload))
         self.iterations += 1

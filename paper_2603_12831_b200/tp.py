@@ -94,3 +94,97 @@ def open_group(ctx, rank: int, world: int, group=None) -> None:
     dist.all_gather_object(gathered, mine.raw, group=group)
     blob = b"".join(gathered)
     _lib.check(lib.hs_tp_open(ctx.h, rank, world, C.c_char_p(blob)), "hs_tp_open")
+
+
+# ---------------------------------------------------------------- live mode
+#
+# A live TP group has one planner: rank 0 runs the LiveEngine and its
+# context is wrapped in a MirrorContext that forwards every state-changing
+# libhs call to the followers (one message per iteration over
+# torch.distributed); the followers replay the calls on their own shard
+# contexts.  The merge decisions need no message at all: with device-polled
+# merges every rank's controller reads all ranks' completion tags (shared
+# host segments, hs_pg_share_tags) and merges an item only once every rank's
+# CPU pool has finished its heads, so the ranks take identical decisions on
+# identical FIFOs -- the per-layer agreement a live group needs.  The
+# fused all-reduce keeps the residual streams (and the tokens) bit-identical.
+
+# calls that change device or replica state, in the order rank 0 issued them
+# (cpu_submit only occurs with host-decided merges, which a live group cannot
+# use on GPUs: rank 0 alone would see its own pool's completions)
+_MIRRORED = ("set_page_table", "host_kv_reserve", "host_kv_release", "iter_begin", "layer",
+             "pg_inject", "pg_stop", "pg_iter", "pg_enable", "iter_end_async", "swap_async",
+             "cpu_submit", "sync")
+
+
+def share_tags(ctx, rank: int, world: int, prefix: str, group=None) -> None:
+    """Merge agreement across a TP group (hs_pg_share_tags, two phases
+    around a barrier).  The context must have device-polled merges on."""
+    import torch.distributed as dist
+
+    ctx.pg_share_tags(prefix, rank, world, 0)
+    dist.barrier(group=group)
+    ctx.pg_share_tags(prefix, rank, world, 1)
+    dist.barrier(group=group)
+
+
+class MirrorContext:
+    """Rank 0's HsContext, recording the state-changing calls for the
+    followers (`flush` ships them; `swap_done` turning true is recorded as a
+    wait, so a follower never uses pages its own copy has not landed)."""
+
+    def __init__(self, ctx, group=None):
+        self._ctx, self._group = ctx, group
+        self._cmds: list = []
+
+    def __getattr__(self, name):
+        attr = getattr(self._ctx, name)
+        if name not in _MIRRORED:
+            return attr
+
+        def call(*a, **kw):
+            self._cmds.append((name, a, kw))
+            return attr(*a, **kw)
+
+        return call
+
+    def swap_done(self, ticket: int) -> bool:
+        done = self._ctx.swap_done(ticket)
+        if done:
+            self._cmds.append(("swap_wait", (ticket,), {}))
+        return done
+
+    def flush(self, stop: bool = False) -> None:
+        import torch.distributed as dist
+
+        msg = [(self._cmds, stop)]
+        self._cmds = []
+        dist.broadcast_object_list(msg, src=0, group=self._group)
+
+
+def follow(ctx, group=None, on_iteration=None) -> int:
+    """A follower rank: replay rank 0's calls on this rank's shard context
+    until rank 0 stops; `on_iteration(ticket)` after each replayed
+    iteration end.  Returns the number of iterations replayed."""
+    import time
+
+    import torch.distributed as dist
+
+    n = 0
+    ctx.anchor()  # iteration completion times are reported relative to it
+    while True:
+        msg = [None]
+        dist.broadcast_object_list(msg, src=0, group=group)
+        cmds, stop = msg[0]
+        for name, a, kw in cmds:
+            if name == "swap_wait":
+                while not ctx.swap_done(a[0]):
+                    time.sleep(5e-5)
+                continue
+            out = getattr(ctx, name)(*a, **kw)
+            if name == "iter_end_async":
+                n += 1
+                if on_iteration:
+                    on_iteration(out)
+        if stop:
+            return n

@@ -133,3 +133,187 @@ def test_tp2_two_processes_match_full_oracle(cuda):
     assert not bad, bad
     assert max_rel < 2e-2, max_rel
     print(f"tp2: compared={compared} max_rel={max_rel:.2e} ties={ties}")
+
+
+def _live_rank(rank, world, port, q):
+    """One rank of a live TP group: rank 0 plans (LiveEngine, device-polled
+    merges, its context mirrored to the follower), rank 1 replays rank 0's
+    calls; both ranks' controllers read both ranks' completion tags."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2603_12831_b200.live import LiveEngine
+    from paper_2603_12831_b200.runtime import HsContext, LiveCudaStep, RuntimeConfig
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = TRANSFORMERS["tiny"]
+        w = make_weights(cfg, 0)
+        sc = tp.shard_config(cfg, world)
+        rt = RuntimeConfig(max_rows=1024, max_slots=64, kv_pages=256, max_pages_per_req=16,
+                           max_pos=2048, max_chunks=1024, cpu_threads=2,
+                           host_kv_bytes=128 << 20)
+        ctx = HsContext(sc, rt)
+        ctx.load_weights(tp.shard_weights(device_weights(w), cfg, rank, world))
+        tp.open_group(ctx, rank, world)
+        ctx.pg_enable(True)
+        tp.share_tags(ctx, rank, world, f"/hs_tp_test_{port}")
+        if rank == 0:
+            mirror = tp.MirrorContext(ctx)
+            step = LiveCudaStep(sc, rt, ctx=mirror, device_merges=True)
+            step.ctx.keep_logits(True)
+            step.keep = True
+            step.trace_tokens = True
+            doc = copy.deepcopy(APPENDIX_B)
+            doc["profiles"]["cluster"]["gpu_kv_capacity"] = 1600
+            eng = LiveEngine(scenario_from_dict(doc, "tp_live"), step=step, pace_layers=64,
+                             pace_tail=0, batch_trace=True)
+            # two processes time-share the test box's one GPU (every fused
+            # all-reduce waits for a context switch): a bounded run
+            n = eng.run_live(horizon_s=40.0, max_iterations=500)
+            step.finish()
+            mirror.flush(stop=True)
+            q.put((0, dict(eng.counters), eng.batch_trace,
+                   [(r, t.tolist(), lg) for r, t, lg in step.token_log], n, eng.stalled))
+        else:
+            toks = []
+
+            def grab(ticket):
+                import time
+
+                while True:
+                    res = ctx.iter_poll(ticket)
+                    if res is not None:
+                        toks.append(res[0].tolist())
+                        return
+                    time.sleep(5e-5)
+
+            n = tp.follow(ctx, on_iteration=grab)
+            q.put((1, n, toks))
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_live_tp2_device_merges_agree_and_match_oracle(cuda):
+    """Live TP=2 (config 4's path): one planner, merges decided on both
+    ranks' devices from both ranks' completion tags.  Both ranks emit
+    identical tokens, and rank 0's realised schedule replayed through the
+    full-model oracle matches (logits within 2e-2)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from oracle.replay import replay
+    from paper_2603_12831_b200.runtime import prompt_tokens
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_live_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in procs:
+        msg = q.get(timeout=1500)
+        out[msg[0]] = msg[1:]
+    for p in procs:
+        p.join(timeout=60)
+    assert [p.exitcode for p in procs] == [0, 0], [p.exitcode for p in procs]
+    counters, trace, token_log, n0, stalled = out[0]
+    n1, toks1 = out[1]
+    assert not stalled and counters["tokens_total"] > 500, counters
+    assert counters["merges"] > 0 and counters["be_tokens_cpu"] > 0
+    assert n1 == n0 == len(token_log)
+    for (reqs, t0, _), t1 in zip(token_log, toks1):  # rank 1's rows: same, plus padding
+        assert t1[:len(t0)] == t0
+    cfg = TRANSFORMERS["tiny"]
+    w = make_weights(cfg, 0)
+    tl = [(r, np.asarray(t, np.int32), lg) for r, t, lg in token_log]
+    st = replay(trace, tl, cfg, w, lambda rid, k: prompt_tokens(rid, k, cfg.vocab, 0))
+    assert st.compared == counters["tokens_total"]
+    assert not st.bad, st.bad[:5]
+    assert st.max_rel < 2e-2, st.max_rel
+    print(f"live tp2: iterations={n0} tokens={st.compared} merges={counters['merges']} "
+          f"max_rel={st.max_rel:.2e} ties={st.ties}")
+
+
+def _mirror_rank(rank, world, port, q):
+    """CPU: the live-TP call mirroring over gloo against recording libhs
+    stand-ins (tests/fake_device.py)."""
+    import os
+    import sys
+    from pathlib import Path
+
+    import torch.distributed as dist
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from fake_device import FakePgContext
+
+    from paper_2603_12831_b200.live import LiveEngine
+    from paper_2603_12831_b200.runtime import LiveCudaStep, RuntimeConfig
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc = tp.shard_config(TRANSFORMERS["tiny"], world)
+        rt = RuntimeConfig(max_rows=1024, max_slots=64, kv_pages=256, max_pages_per_req=16,
+                           max_pos=2048, max_chunks=1024, cpu_threads=2, host_kv_bytes=1 << 20)
+        # host-decided merges: the stand-ins cannot share completion tags across
+        # processes, so the follower's fake replays rank 0's merge lists (the
+        # device-decided agreement itself is the GPU test above)
+        fake = FakePgContext(sc, rt, iter_ms=0.25, cpu_ms=0.5, rng_seed=rank)
+        if rank == 0:
+            mirror = tp.MirrorContext(fake)
+            step = LiveCudaStep(sc, rt, ctx=mirror)
+            doc = copy.deepcopy(APPENDIX_B)
+            doc["profiles"]["cluster"]["gpu_kv_capacity"] = 1600
+            eng = LiveEngine(scenario_from_dict(doc, "mirror"), step=step, pace_layers=1)
+            eng.run_live(horizon_s=30.0)
+            step.finish()
+            mirror.flush(stop=True)
+            q.put((0, dict(fake.calls), sorted(fake.pages.items()), len(fake.iters),
+                   eng.counters["tokens_total"]))
+        else:
+            n = tp.follow(fake)
+            q.put((1, dict(fake.calls), sorted(fake.pages.items()), n, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_live_tp_mirror_replays_every_call():
+    """The follower of a live TP group replays exactly the state-changing
+    calls of the planning rank: the same iterations, layers, page tables,
+    swaps and host-KV reservations (two gloo ranks on CPU)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mirror_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in procs:
+        msg = q.get(timeout=300)
+        out[msg[0]] = msg[1:]
+    for p in procs:
+        p.join(timeout=60)
+    assert [p.exitcode for p in procs] == [0, 0]
+    calls0, pages0, iters0, tokens = out[0]
+    calls1, pages1, iters1, _ = out[1]
+    assert tokens > 1000
+    assert iters0 == iters1 > 100
+    for k in ("iter_begin", "layer", "swap", "cpu_submit", "merged"):
+        assert calls0[k] == calls1[k], (k, calls0[k], calls1[k])
+    assert calls0["swap"] > 0
+    assert pages0 == pages1
