@@ -423,34 +423,34 @@ def run_reference(args) -> None:
 class Replica:
     """One GPU replica: context, engine, BE backlog and trace."""
 
-    def __init__(self, args, world: int, rank: int, local: int, local_world: int):
+    def __init__(self, args, world: int, rank: int, local: int, local_world: int,
+                 model=None, make_ctx=None):
         from paper_2603_12831_b200 import profiler, replicas
         from paper_2603_12831_b200.models import get_transformer
-        from paper_2603_12831_b200.runtime import LiveCudaStep, RuntimeConfig
+        from paper_2603_12831_b200.runtime import LiveCudaStep
 
         self.args, self.world, self.rank = args, world, rank
-        model = self.model = get_transformer(args.config)
+        model = self.model = model or get_transformer(args.config)
         # the replica's CPU-attention cores: its GPU's NUMA node, split among the
         # GPUs on that node; two cores stay free for the engine thread
         cpus = replicas.core_set(local, local_world)
         workers = replica_workers(cpus)
         self.cores = len(cpus)
         self.be_fixed = (32768, 136) if args.workload == "longctx" else None
-        be_cap_tokens = be_cap(args)
         fit_be_chains(args, model, local_world, verbose=rank == 0)
-        rt = self.rt = RuntimeConfig(
-            max_rows=args.max_rows, max_slots=512,
-            kv_pages=args.gpu_kv_tokens // 64 + 512 + 64,
-            max_pages_per_req=max(256, (be_cap_tokens + 127) // 64),
-            max_pos=max(16384, be_cap_tokens + 64), max_chunks=8192, cpu_threads=len(workers),
-            host_kv_bytes=(args.be_chains + 4) * be_cap_tokens
-            * model.kv_bytes_per_token_layer * model.n_layers, device=local,
-            cpu_list=tuple(workers) if args.pin else ())
+        rt = self.rt = _replica_rt(args, model, local, local_world)
+        # make_ctx (a TP group's rank 0): the caller builds the context -- the
+        # shard, the group's exchange and shared tags -- and mirrors it
         self.step = LiveCudaStep(model, rt, weight_seed=args.seed,
-                                 device_merges=args.merges == "device")
+                                 device_merges=args.merges == "device",
+                                 ctx=make_ctx(rt) if make_ctx else None)
         models_path = ROOT / "profiles" / f"b200_{args.config}_models.json"
         scen = self.scenario(args.ls_rate)
-        if args.calibrate or not models_path.exists():
+        if make_ctx and not models_path.exists():
+            # a TP shard cannot run the profiler's probes alone (the fused
+            # all-reduce needs every rank); use the unsharded model's fit
+            models_path = ROOT / "profiles" / "b200_llama3-8b_models.json"
+        if not make_ctx and (args.calibrate or not models_path.exists()):
             self.models = profiler.calibrate(
                 self.step.ctx, scen.cluster, max_batch=args.max_rows,
                 log=(lambda m: print(m, file=sys.stderr)) if rank == 0 else None)
@@ -548,6 +548,100 @@ def timed_window(rep, iterations: int, dist) -> dict:
               "be_cpu": eng.counters["be_tokens_cpu"] - be_cpu0,
               "host_s": {k: eng.host_s[k] - host0[k] for k in host0}, "iters": iters})
     return m
+
+
+def run_tp(args) -> None:
+    """Config 4: one tensor-parallel group over all ranks of the job (one
+    process per GPU).  Rank 0 plans and serves through a MirrorContext; the
+    other ranks replay its calls on their shards (tp.follow); the fused
+    all-reduce runs over P2P / NVLink and the ranks agree on every merge
+    through shared completion tags (device-polled merges)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_12831_b200 import tp
+    from paper_2603_12831_b200.models import get_transformer
+    from paper_2603_12831_b200.runtime import HsContext
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.tp:
+        raise SystemExit(f"bench: --tp {args.tp} needs WORLD_SIZE {args.tp} (got {world})")
+    if args.merges != "device":
+        raise SystemExit("bench: a live TP group needs --merges device (merge agreement)")
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    shard = tp.shard_config(get_transformer(args.config), world)
+    prefix = f"/hs_bench_tp_{os.environ.get('MASTER_PORT', '0')}"
+    ctx_box = {}
+
+    def make_ctx(rt):
+        ctx = HsContext(shard, rt)
+        ctx.init_weights(args.seed * 131 + rank)  # random-init shard of each rank
+        tp.open_group(ctx, rank, world)
+        ctx.pg_enable(True)
+        tp.share_tags(ctx, rank, world, prefix)
+        ctx_box["ctx"] = ctx
+        return tp.MirrorContext(ctx) if rank == 0 else ctx
+
+    args.pace, args.pace_tail = 64, 0  # unpaced: the followers get one message per iteration
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    if rank != 0:
+        # the same runtime sizes as rank 0's replica
+        rt = _replica_rt(argparse.Namespace(**vars(args)), shard, local, local_world)
+        ctx = make_ctx(rt)
+        tp.follow(ctx)
+        dist.barrier()
+        return
+    rep = Replica(args, 1, 0, local, local_world, model=shard, make_ctx=make_ctx)
+    L = shard.n_layers
+    rep.start(args.ls_rate)
+    warm = rep.warm(args.warmup * L, args.warmup_s, max(args.warmup, 40) * L)
+    with ClockSampler(local) as clocks:
+        m = timed_window(rep, args.steps * L, None)
+    rep.step.finish()
+    rep.step.ctx.flush(stop=True)
+    dist.barrier()
+    iters = m["iters"]
+    line = {
+        "metric": METRIC, "value": m["be_tokens"] / m["device_s"] if m["device_s"] else 0.0,
+        "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": m["device_s"] * 1e3 / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weight shards, synthetic KV, Poisson LS trace)",
+        "config": dict(bench_config(args, shard, rep.rt.cpu_threads, 1),
+                       parallelism=f"tp{world} (one group, live, device-decided merges)"),
+        "iterations_timed": len(iters), "warmup_iterations": warm,
+        "ls_tpot_attainment": m["tpot_attainment"], "ls_tpot_p99_ms": m["tpot_p99_ms"],
+        "be_tokens": m["be_tokens"], "ls_gaps": m["ls_gaps"],
+        "be_tokens_via_cpu_attention": m["be_cpu"],
+        "iteration_ms_p50": statistics.median(i["device_ms"] for i in iters
+                                              if i.get("device_ms")) if iters else None,
+        "e2e": {"value": m["be_tokens"] / m["wall_s"] if m["wall_s"] else 0.0, "unit": UNIT,
+                "h2d_bytes_per_step": m["h2d"] / max(args.steps, 1),
+                "d2h_bytes_per_step": m["d2h"] / max(args.steps, 1)},
+        "gpu_launches": int(m["launches"]), "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _replica_rt(args, model, local: int, local_world: int):
+    """The RuntimeConfig Replica builds for `model` (TP followers need the
+    same sizes as rank 0 without building an engine)."""
+    from paper_2603_12831_b200 import replicas
+    from paper_2603_12831_b200.runtime import RuntimeConfig
+
+    cpus = replicas.core_set(local, local_world)
+    workers = replica_workers(cpus)
+    fit_be_chains(args, model, local_world)
+    cap = be_cap(args)
+    return RuntimeConfig(
+        max_rows=args.max_rows, max_slots=512, kv_pages=args.gpu_kv_tokens // 64 + 512 + 64,
+        max_pages_per_req=max(256, (cap + 127) // 64), max_pos=max(16384, cap + 64),
+        max_chunks=8192, cpu_threads=len(workers),
+        host_kv_bytes=(args.be_chains + 4) * cap * model.kv_bytes_per_token_layer * model.n_layers,
+        device=local, cpu_list=tuple(workers) if args.pin else ())
 
 
 def run_ours(args) -> None:
@@ -778,6 +872,8 @@ def main() -> None:
     C_void_p, C_POINTER, C_byref = ctypes.c_void_p, ctypes.POINTER, ctypes.byref
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--tp", type=int, default=1,
+                    help="config 4: all ranks form one tensor-parallel group (live, one planner)")
     ap.add_argument("--steps", type=int, default=40, help="timed steps (chain cycles)")
     ap.add_argument("--warmup", type=int, default=8, help="warm-up steps (at least)")
     ap.add_argument("--warmup-s", type=float, default=2.0,
@@ -845,6 +941,8 @@ def main() -> None:
         sys.exit(spawn_replicas(args.gpus))
     if args.impl == "reference":
         run_reference(args)
+    elif args.tp > 1:
+        run_tp(args)
     else:
         run_ours(args)
 

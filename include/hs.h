@@ -332,10 +332,12 @@ int hs_pg_iter(hs_ctx* ctx, int cap, const int* merge_bound, int inject_bound);
 int hs_pg_log(hs_ctx* ctx, int ticket, int* out, int n);
 /* Tensor-parallel groups: the ranks agree on every merge.  Phase 0 moves this
  * rank's completion tags into the POSIX shared-memory segment
- * "<prefix>.<rank>"; after a barrier across the group, phase 1 maps the
- * peers' segments.  Each rank's controller then merges an item only once
- * every rank's CPU pool has finished its heads of it, so all ranks take the
- * same decisions on the same FIFO (the ranks must issue identical calls). */
+ * "<prefix>.<rank>" (rank 0 also creates "<prefix>.dec"); after a barrier
+ * across the group, phase 1 maps the peers' segments.  Rank 0's controller
+ * then merges an item only once every rank's CPU pool has finished its heads
+ * of it and publishes each layer's decision in "<prefix>.dec"; the other
+ * ranks' controllers apply that decision (one snapshot of the tags for the
+ * whole group).  The ranks must issue identical calls. */
 int hs_pg_share_tags(hs_ctx* ctx, const char* prefix, int rank, int world, int phase);
 /* stream marks for launch pacing, and timing events (CUDA events on the
  * compute stream; elapsed in ms between two timer ids) */

@@ -54,11 +54,17 @@ struct PgDev {
   // segments); an item is ready once all ranks' CPU pools finished it
   const unsigned* peer_tags[8] = {};
   int n_peer = 0;
+  // TP group: rank 0's controller publishes each layer's decision (merged
+  // count, injections) into a shared ring; the followers' controllers take
+  // it from there, so every rank applies one snapshot of the tags
+  int* dec = nullptr;         // [kDecRing][4]: seq, k, n_inj, pad (mapped, shared)
+  int dec_role = 0;           // 0 = single rank, 1 = publishes, 2 = follows
   int list_cap = 0;           // entries per list in `lists`
   int log_stride = 0;         // ints per iteration in the log
 };
 enum { PG_HEAD = 0, PG_TAIL = 1, PG_PUB = 2, PG_INJ_HEAD = 3, PG_INJ_TAIL = 4, PG_PREV_N = 5,
-       PG_STATE_INTS = 8 };
+       PG_SEQ = 6, PG_STATE_INTS = 8 };
+constexpr int kDecRing = 64;
 
 // device pointers of one hs_layer call's row lists (packed staging run)
 struct LayerRows {
@@ -194,7 +200,8 @@ struct hs_ctx {
   // TP groups: this rank's tags moved into a POSIX shm segment (shared with
   // the peers) and the peers' segments mapped here
   std::vector<std::pair<void*, size_t>> pg_shm;  // mapped segments (own first)
-  std::string pg_shm_own;                        // name to unlink on destroy
+  std::string pg_shm_own;                        // names to unlink on destroy
+  std::string pg_shm_dec;
   unsigned* pg_tag_alloc = nullptr;              // the original cudaHostAlloc tags
 };
 

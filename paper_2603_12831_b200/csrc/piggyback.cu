@@ -179,7 +179,41 @@ __global__ void pg_control_kernel(PgDev p, int layer, int n_layers, int cap, int
   k = min(k, limit);
   // layer-1 injections fill the rest of the cap (engine.py:912-918)
   const int inj_head = p.st[PG_INJ_HEAD];
-  const int n_inj = layer == 1 ? max(0, min(min(p.st[PG_INJ_TAIL] - inj_head, cap - k), c_max)) : 0;
+  int n_inj = layer == 1 ? max(0, min(min(p.st[PG_INJ_TAIL] - inj_head, cap - k), c_max)) : 0;
+  if (p.dec_role) {
+    // TP group: one snapshot of the tags for every rank.  Rank 0 publishes
+    // its decision (taken over all ranks' tags) for this layer; the others
+    // apply it (their FIFOs are identical: same calls, same decisions)
+    const int seq = p.st[PG_SEQ] + 1;
+    int* slot = p.dec + (seq % kDecRing) * 4;
+    if (p.dec_role == 1) {
+      if (lane == 0) {
+        slot[1] = k;
+        slot[2] = n_inj;
+        __threadfence_system();
+        st_release_sys(slot, seq);
+      }
+    } else {
+      int got = 0;
+      if (lane == 0) {
+        const long long t0 = clock64();
+        for (;;) {
+          int v;
+          asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(slot) : "memory");
+          if (v == seq) break;
+          if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s: the leader is gone
+          __nanosleep(200);
+        }
+        got = 1;
+      }
+      __syncwarp();
+      (void)got;
+      k = *reinterpret_cast<volatile int*>(slot + 1);
+      n_inj = *reinterpret_cast<volatile int*>(slot + 2);
+    }
+    __syncwarp();
+    if (lane == 0) p.st[PG_SEQ] = seq;
+  }
   const int n_prev = layer == 1 ? 0 : min(p.st[PG_PREV_N], c_max);
   const int n_carry = layer == 1 ? n_inj : n_prev;
   const bool last = layer == n_layers;
@@ -326,6 +360,8 @@ void pg_free(hs_ctx* c) {
   c->pg_shm.clear();
   if (!c->pg_shm_own.empty()) shm_unlink(c->pg_shm_own.c_str());
   c->pg_shm_own.clear();
+  if (!c->pg_shm_dec.empty()) shm_unlink(c->pg_shm_dec.c_str());
+  c->pg_shm_dec.clear();
   if (c->pg_tag_alloc) {  // the context frees its own allocation
     c->tag_h = c->pg_tag_alloc;
     c->pg_tag_alloc = nullptr;
@@ -510,6 +546,34 @@ int hs_pg_share_tags(hs_ctx* c, const char* prefix, int rank, int world, int pha
     return HS_OK;
   };
   const std::string base = std::string(prefix) + ".";
+  const size_t dec_bytes = static_cast<size_t>(kDecRing) * 4 * sizeof(int);
+  auto map_dec = [&](bool create) -> int {
+    const std::string name = base + "dec";
+    const int fd = shm_open(name.c_str(), create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
+    if (fd < 0) return set_error(HS_E_CONFIG, "shm_open %s failed", name.c_str());
+    if (create && ftruncate(fd, static_cast<off_t>(dec_bytes)) != 0) {
+      close(fd);
+      return set_error(HS_E_CONFIG, "ftruncate %s failed", name.c_str());
+    }
+    void* p = mmap(nullptr, dec_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) return set_error(HS_E_CONFIG, "mmap %s failed", name.c_str());
+    if (create) std::memset(p, 0, dec_bytes);
+    if (cudaHostRegister(p, dec_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) !=
+        cudaSuccess) {
+      munmap(p, dec_bytes);
+      return set_error(HS_E_CUDA, "cudaHostRegister %s failed", name.c_str());
+    }
+    c->pg_shm.emplace_back(p, dec_bytes);
+    if (create) c->pg_shm_dec = name;
+    PG_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->pg.dec), p, 0));
+    c->pg.dec_role = create ? 1 : 2;
+    return HS_OK;
+  };
+  if (phase == 0 && world > 1 && rank == 0)
+    if (int rc = map_dec(true)) return rc;
+  if (phase == 1 && world > 1 && rank != 0)
+    if (int rc = map_dec(false)) return rc;
   if (phase == 0) {
     PG_CK(cudaDeviceSynchronize());
     void* p = nullptr;
