@@ -514,6 +514,10 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
     RC(dalloc(&c->kv_pool, pool_elems));
     if (make_kv_map(&c->m_kv, c->kv_pool, c->geom)) return set_error(HS_E_CUDA, "kv map failed");
   }
+  // zero the pool: the attention kernels multiply the masked tail of a page
+  // (P = 0) into V, and 0 x NaN is NaN -- recycled device memory can hold any
+  // bit pattern where no token has been written yet
+  CK(cudaMemset(c->kv_pool, 0, pool_elems * (c->fp32 ? sizeof(float) : sizeof(bf16))));
   RC(dalloc(&c->page_table, static_cast<size_t>(r.max_slots) * r.max_pages_per_req));
   CK(cudaMemset(c->page_table, 0, static_cast<size_t>(r.max_slots) * r.max_pages_per_req * 4));
   // activations

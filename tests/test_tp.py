@@ -135,7 +135,7 @@ def test_tp2_two_processes_match_full_oracle(cuda):
     print(f"tp2: compared={compared} max_rel={max_rel:.2e} ties={ties}")
 
 
-def _live_rank(rank, world, port, q):
+def _live_rank(rank, world, port, q, device_merges=True, max_iterations=300):
     """One rank of a live TP group: rank 0 plans (LiveEngine, device-polled
     merges, its context mirrored to the follower), rank 1 replays rank 0's
     calls; both ranks' controllers read both ranks' completion tags."""
@@ -160,11 +160,12 @@ def _live_rank(rank, world, port, q):
         ctx = HsContext(sc, rt)
         ctx.load_weights(tp.shard_weights(device_weights(w), cfg, rank, world))
         tp.open_group(ctx, rank, world)
-        ctx.pg_enable(True)
-        tp.share_tags(ctx, rank, world, f"/hs_tp_test_{port}")
+        if device_merges:
+            ctx.pg_enable(True)
+            tp.share_tags(ctx, rank, world, f"/hs_tp_test_{port}")
         if rank == 0:
             mirror = tp.MirrorContext(ctx)
-            step = LiveCudaStep(sc, rt, ctx=mirror, device_merges=True)
+            step = LiveCudaStep(sc, rt, ctx=mirror, device_merges=device_merges)
             step.ctx.keep_logits(True)
             step.keep = True
             step.trace_tokens = True
@@ -174,7 +175,7 @@ def _live_rank(rank, world, port, q):
                              pace_tail=0, batch_trace=True)
             # two processes time-share the test box's one GPU (every fused
             # all-reduce waits for a context switch): a bounded run
-            n = eng.run_live(horizon_s=40.0, max_iterations=300)
+            n = eng.run_live(horizon_s=40.0, max_iterations=max_iterations)
             step.finish()
             mirror.flush(stop=True)
             q.put((0, dict(eng.counters), eng.batch_trace,
