@@ -424,7 +424,7 @@ class Replica:
     """One GPU replica: context, engine, BE backlog and trace."""
 
     def __init__(self, args, world: int, rank: int, local: int, local_world: int,
-                 model=None, make_ctx=None):
+                 model=None, make_ctx=None, device=None):
         from paper_2603_12831_b200 import profiler, replicas
         from paper_2603_12831_b200.models import get_transformer
         from paper_2603_12831_b200.runtime import LiveCudaStep
@@ -438,7 +438,7 @@ class Replica:
         self.cores = len(cpus)
         self.be_fixed = (32768, 136) if args.workload == "longctx" else None
         fit_be_chains(args, model, local_world, verbose=rank == 0)
-        rt = self.rt = _replica_rt(args, model, local, local_world)
+        rt = self.rt = _replica_rt(args, model, local, local_world, device)
         # make_ctx (a TP group's rank 0): the caller builds the context -- the
         # shard, the group's exchange and shared tags -- and mirrors it
         self.step = LiveCudaStep(model, rt, weight_seed=args.seed,
@@ -570,7 +570,9 @@ def run_tp(args) -> None:
         raise SystemExit(f"bench: --tp {args.tp} needs WORLD_SIZE {args.tp} (got {world})")
     if args.merges != "device":
         raise SystemExit("bench: a live TP group needs --merges device (merge agreement)")
-    torch.cuda.set_device(local)
+    # a group larger than the box (a functional run) time-shares its GPUs
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo")
     shard = tp.shard_config(get_transformer(args.config), world)
     prefix = f"/hs_bench_tp_{os.environ.get('MASTER_PORT', '0')}"
@@ -589,16 +591,16 @@ def run_tp(args) -> None:
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
     if rank != 0:
         # the same runtime sizes as rank 0's replica
-        rt = _replica_rt(argparse.Namespace(**vars(args)), shard, local, local_world)
+        rt = _replica_rt(argparse.Namespace(**vars(args)), shard, local, local_world, dev)
         ctx = make_ctx(rt)
         tp.follow(ctx)
         dist.barrier()
         return
-    rep = Replica(args, 1, 0, local, local_world, model=shard, make_ctx=make_ctx)
+    rep = Replica(args, 1, 0, local, local_world, model=shard, make_ctx=make_ctx, device=dev)
     L = shard.n_layers
     rep.start(args.ls_rate)
     warm = rep.warm(args.warmup * L, args.warmup_s, max(args.warmup, 40) * L)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev) as clocks:
         m = timed_window(rep, args.steps * L, None)
     rep.step.finish()
     rep.step.ctx.flush(stop=True)
@@ -626,7 +628,7 @@ def run_tp(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def _replica_rt(args, model, local: int, local_world: int):
+def _replica_rt(args, model, local: int, local_world: int, device=None):
     """The RuntimeConfig Replica builds for `model` (TP followers need the
     same sizes as rank 0 without building an engine)."""
     from paper_2603_12831_b200 import replicas
@@ -641,7 +643,7 @@ def _replica_rt(args, model, local: int, local_world: int):
         max_pages_per_req=max(256, (cap + 127) // 64), max_pos=max(16384, cap + 64),
         max_chunks=8192, cpu_threads=len(workers),
         host_kv_bytes=(args.be_chains + 4) * cap * model.kv_bytes_per_token_layer * model.n_layers,
-        device=local, cpu_list=tuple(workers) if args.pin else ())
+        device=local if device is None else device, cpu_list=tuple(workers) if args.pin else ())
 
 
 def run_ours(args) -> None:
