@@ -72,6 +72,7 @@ class LiveEngine(Engine):
         # FIFO head-run merge rule (engine.py:902-919) relies on
         self._order: deque = deque()
         self._finished: set[str] = set()
+        self._pg_done = self._pg_merged = 0  # device mode: CPU completions polled / merged
         self._swaps: dict[int, tuple[str, str]] = {}
         self._swapin_wait: set[str] = set()
         self._collect: Optional[list] = None  # tokens emitted by the iteration being launched
@@ -132,11 +133,13 @@ class LiveEngine(Engine):
         for rid, layer in self.step.cpu_poll():
             if self.device_merges:
                 # a hint that the device has something to merge (the device
-                # decides from the completion tags themselves)
-                w = self._submitted.get(rid)
-                if w is not None and w.layer == layer:
-                    self._finished.add(rid)
-                    self._dirty = True
+                # decides from the completion tags themselves).  Counted, not
+                # matched against the host mirror: a completion can be polled
+                # before the replay of the iteration that shipped the item
+                # reaches the mirror, and a dropped hint would leave the
+                # engine idle with a merge waiting on the device.
+                self._pg_done += 1
+                self._dirty = True
                 continue
             self._finished.add(rid)
         while not self.device_merges and self._order and self._order[0].req_id in self._finished:
@@ -184,7 +187,7 @@ class LiveEngine(Engine):
     def _live_iteration(self, plan) -> bool:
         cap = self._merge_cap(plan.loads)
         pending = (self.queues.output or self.pending_injections
-                   or (self.device_merges and (self._pg_inj or self._finished)))
+                   or (self.device_merges and (self._pg_inj or self._pg_done > self._pg_merged)))
         has_work = (plan.ls_decode or plan.ls_prefill_chunks or plan.be_prefill_chunks
                     or plan.be_decode_gpu or (cap > 0 and pending))
         if not has_work:
@@ -280,7 +283,7 @@ class LiveEngine(Engine):
     # -- device-polled merges ----------------------------------------------------------
 
     def _runnable(self) -> bool:
-        if self.device_merges and (self._pg_inj or self._finished):
+        if self.device_merges and (self._pg_inj or self._pg_done > self._pg_merged):
             return True
         return super()._runnable()
 
@@ -409,7 +412,7 @@ class LiveEngine(Engine):
                         raise AssertionError(f"device merged {rid} at layer {layer}, host FIFO "
                                              f"head is {w.req_id} at layer {w.layer}")
                     self._submitted.pop(rid, None)
-                    self._finished.discard(rid)
+                    self._pg_merged += 1
                     self.queues.output_enq += 1
                     self.queues.output_deq += 1
                     req.chain_state = "output"
