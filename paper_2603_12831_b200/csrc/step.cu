@@ -85,9 +85,14 @@ MetaLayout layout_of(const hs_rt_cfg& r) {
     }                                                                                      \
   } while (0)
 
+// Every device buffer starts zeroed: memory recycled from a context freed
+// earlier in the process holds that context's bytes (NaN patterns included),
+// and masked attention tails multiply P = 0 into whatever V holds.
 template <typename T>
 int dalloc(T** p, size_t n) {
-  CK(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T)));
+  const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+  CK(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+  CK(cudaMemset(*p, 0, bytes));
   return HS_OK;
 }
 
