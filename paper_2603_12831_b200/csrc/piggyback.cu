@@ -316,7 +316,8 @@ int pg_alloc(hs_ctx* c) {
   int* base = nullptr;
   if (cudaMalloc(&base, ints * sizeof(int)) != cudaSuccess)
     return set_error(HS_E_CUDA, "device-polled merges: allocation failed");
-  cudaMemset(base, 0, ints * sizeof(int));
+  if (cudaMemsetAsync(base, 0, ints * sizeof(int), c->st) != cudaSuccess)
+    return set_error(HS_E_CUDA, "device-polled merges: clear failed");
   p.q = base;
   p.inj = p.q + static_cast<size_t>(p.Q) * 3;
   p.st = p.inj + p.Qi;

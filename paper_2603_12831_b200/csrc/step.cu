@@ -93,6 +93,18 @@ int dalloc(T** p, size_t n) {
   const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
   CK(cudaMalloc(reinterpret_cast<void**>(p), bytes));
   CK(cudaMemset(*p, 0, bytes));
+  // cudaMemset runs on the legacy stream, which does not order against the
+  // context's non-blocking streams: finish it before anything can use p
+  CK(cudaDeviceSynchronize());
+  return HS_OK;
+}
+
+// Host-to-device copy ordered on the context stream and complete on return
+// (a pageable cudaMemcpy can return before its DMA has landed, and the
+// legacy stream it uses does not order against the non-blocking streams).
+int h2d(hs_ctx* c, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));
   return HS_OK;
 }
 
@@ -341,8 +353,8 @@ int rope_init(hs_ctx* c) {
     }
   RC(dalloc(&c->rope_cos, cs.size()));
   RC(dalloc(&c->rope_sin, sn.size()));
-  CK(cudaMemcpy(c->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  RC(h2d(c, c->rope_cos, cs.data(), cs.size() * 4));
+  RC(h2d(c, c->rope_sin, sn.data(), sn.size() * 4));
   return HS_OK;
 }
 
@@ -618,7 +630,8 @@ int create(const hs_model_cfg* mc, const hs_rt_cfg* rc, hs_ctx* c) {
   c->timers.resize(8192);
   for (auto& e : c->marks) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : c->timers) CK(cudaEventCreate(&e));
-  CK(cudaStreamSynchronize(c->st));
+  // legacy-stream memsets/copies above vs the non-blocking streams
+  CK(cudaDeviceSynchronize());
   return HS_OK;
 }
 
@@ -779,8 +792,8 @@ int probe_pages(hs_ctx* c, int g, int tokens) {
   std::vector<int> pt(per);
   for (int s = 0; s < g; ++s) {
     for (int i = 0; i < per; ++i) pt[i] = (s * per + i) % c->r.kv_pages;
-    CK(cudaMemcpy(c->page_table + static_cast<size_t>(s) * c->r.max_pages_per_req, pt.data(),
-                  per * 4, cudaMemcpyHostToDevice));
+    RC(h2d(c, c->page_table + static_cast<size_t>(s) * c->r.max_pages_per_req, pt.data(),
+                  per * 4));
   }
   return HS_OK;
 }
@@ -852,7 +865,7 @@ int hs_set_weight(hs_ctx* c, int kind, int layer, const void* host, size_t bytes
     }
     if (bytes != 2 * want)
       return set_error(HS_E_CONFIG, "fp32 weight %d: %zu bytes, want %zu", kind, bytes, 2 * want);
-    CK(cudaMemcpy(fdst, host, bytes, cudaMemcpyHostToDevice));
+    RC(h2d(c, fdst, host, bytes));
     return HS_OK;
   }
   if (bytes != want) return set_error(HS_E_CONFIG, "weight %d: %zu bytes, want %zu", kind, bytes, want);
@@ -860,7 +873,7 @@ int hs_set_weight(hs_ctx* c, int kind, int layer, const void* host, size_t bytes
     // rows reordered for the fused epilogues (see permute_rows)
     bf16* tmp = nullptr;
     CK(cudaMalloc(reinterpret_cast<void**>(&tmp), bytes));
-    CK(cudaMemcpy(tmp, host, bytes, cudaMemcpyHostToDevice));
+    RC(h2d(c, tmp, host, bytes));
     const int rows = kind == HS_W_QKV ? m.qkv_n() : 2 * m.ffn;
     const int rc = permute_rows(tmp, static_cast<bf16*>(dst), rows, m.d,
                                 kind == HS_W_QKV ? 1 : 0, kind == HS_W_QKV ? m.hd : m.ffn, c->st);
@@ -869,7 +882,7 @@ int hs_set_weight(hs_ctx* c, int kind, int layer, const void* host, size_t bytes
     if (rc != HS_OK) return set_error(HS_E_CUDA, "weight permutation failed");
     return HS_OK;
   }
-  CK(cudaMemcpy(dst, host, bytes, cudaMemcpyHostToDevice));
+  RC(h2d(c, dst, host, bytes));
   return HS_OK;
 }
 
@@ -1590,7 +1603,7 @@ int hs_probe_pcie(hs_ctx* c, int dir, int rows, int reps, float* us, double* byt
   const int qkv = m.qkv_n(), nqh = m.n_q * m.hd;
   std::vector<int> ident(rows);
   for (int i = 0; i < rows; ++i) ident[i] = i;
-  CK(cudaMemcpy(c->dm_layer, ident.data(), rows * sizeof(int), cudaMemcpyHostToDevice));
+  RC(h2d(c, c->dm_layer, ident.data(), rows * sizeof(int)));
   bf16* scratch = reinterpret_cast<bf16*>(c->part);
   const int w = (dir == 0 || dir == 2) ? qkv : nqh;
   *bytes = 2.0 * rows * w;
@@ -1624,7 +1637,7 @@ int hs_probe_dense_mode(hs_ctx* c, int n, int mode, int layers, int reps, float*
   auto on = [mode](int b) { return (mode >> b) & 1; };
   // every row a carry row of slot 0 at position 0 (page-table row 0 valid)
   RC(probe_pages(c, 1, 64));
-  CK(cudaMemset(c->dm_layer, 0, 2 * static_cast<size_t>(n) * sizeof(int)));
+  CK(cudaMemsetAsync(c->dm_layer, 0, 2 * static_cast<size_t>(n) * sizeof(int), c->st));
   const int* cslot = c->dm_layer;
   const int* cpos = c->dm_layer + n;
   auto planes = [&](int n_out, int k) {
@@ -1663,7 +1676,7 @@ int hs_probe_gemm(hs_ctx* c, int which, int n, int fused, int reps, float* us) {
   const int d_ = m.d, nqh = m.n_q * m.hd;
   EpiParams ep = epi_base(c);
   // QKV epilogue as a pure ship of n carry rows (slot 0, position 0)
-  CK(cudaMemset(c->dm_layer, 0, 2 * static_cast<size_t>(n) * sizeof(int)));
+  CK(cudaMemsetAsync(c->dm_layer, 0, 2 * static_cast<size_t>(n) * sizeof(int), c->st));
   ep.n_batch = 0;
   ep.carry_slot = c->dm_layer;
   ep.carry_pos = c->dm_layer + n;
@@ -1705,8 +1718,8 @@ int hs_probe_decode(hs_ctx* c, int g, int ctx_len, int reps, float* us) {
   if (static_cast<int>(ch.size() / 5) > c->r.max_chunks)
     return set_error(HS_E_CAPACITY, "probe exceeds max_chunks");
   const MetaLayout L = layout_of(c->r);
-  CK(cudaMemcpy(c->dm + L.chunks, ch.data(), ch.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->dm + L.row_chunk_begin, beg.data(), beg.size() * 4, cudaMemcpyHostToDevice));
+  RC(h2d(c, c->dm + L.chunks, ch.data(), ch.size() * 4));
+  RC(h2d(c, c->dm + L.row_chunk_begin, beg.data(), beg.size() * 4));
   const int nch = static_cast<int>(ch.size() / 5), nqh = m.n_q * m.hd;
   return time_reps(c, reps, [&]() -> int {
     RC(decode_attention(c->m_kv, c->geom, 0, c->qbuf, nqh, m.n_q, c->page_table,
@@ -1726,7 +1739,7 @@ int hs_probe_prefill(hs_ctx* c, int q, int done, int reps, float* us) {
   std::vector<int> tiles;
   for (int j = 0; j < q; j += 64) tiles.insert(tiles.end(), {0, j, done + j, std::min(64, q - j)});
   const MetaLayout L = layout_of(c->r);
-  CK(cudaMemcpy(c->dm + L.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice));
+  RC(h2d(c, c->dm + L.tiles, tiles.data(), tiles.size() * 4));
   const int nt = static_cast<int>(tiles.size() / 4), nqh = m.n_q * m.hd;
   return time_reps(c, reps, [&]() -> int {
     return prefill_attention(c->m_kv, c->geom, 0, c->qbuf, nqh, m.n_q, c->page_table,
