@@ -34,7 +34,8 @@ def _live_run(pace_layers=1, pace_tail=0, cpu_threads=4, device_merges=False):
 
     cfg = TRANSFORMERS["tiny"]
     w = make_weights(cfg, 0)
-    rt = RuntimeConfig(max_rows=1024, max_slots=64, kv_pages=256, max_pages_per_req=16,
+    # rows: a 1024-token prefill budget plus the decode rows of the same plan
+    rt = RuntimeConfig(max_rows=2048, max_slots=64, kv_pages=256, max_pages_per_req=16,
                        max_pos=2048, max_chunks=1024, cpu_threads=cpu_threads,
                        host_kv_bytes=256 << 20)
     step = LiveCudaStep(cfg, rt, weights=device_weights(w), keep_logits=True,
