@@ -41,7 +41,7 @@ namespace hs {
 
 namespace {
 
-constexpr int kTcStages = 4;
+constexpr int kTcStages = 3;
 constexpr int kMaxTiles = 2;            // Q tiles of 128 rows sharing each KV page
 constexpr int kTcSoftmaxThreads = 128;  // per tile: warps 4t..4t+3, one TMEM lane (row) each
 constexpr int kRows = 128;              // MMA M
@@ -67,6 +67,13 @@ __device__ __forceinline__ uint64_t umma_desc_mn128(uint32_t smem_addr, uint32_t
   d |= static_cast<uint64_t>(1u) << 46;
   d |= static_cast<uint64_t>(2u) << 61;
   return d;
+}
+
+// one MUFU.EX2 (subnormal results flush to 0, far below bf16 P's resolution)
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -117,10 +124,12 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                       // [tile][kQBytes]
-  uint8_t* sP = sQ + NT * kQBytes;      // [tile][kPBytes]
-  uint8_t* sKV = sP + NT * kPBytes;
+  uint8_t* sP = sQ + NT * kQBytes;      // [tile][buffer][kPBytes]
+  uint8_t* sKV = sP + NT * 2 * kPBytes;
   __shared__ uint64_t kv_full[kTcStages], kv_empty[kTcStages];
-  __shared__ uint64_t s_full[NT][2], p_full[NT], o_full[NT];
+  // S, P and the P.V commit are double-buffered by page parity: a page's
+  // softmax writes its P while the previous page's P.V is still running
+  __shared__ uint64_t s_full[NT][2], p_full[NT][2], o_full[NT][2];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -144,10 +153,11 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
       mbar_init(&kv_empty[s], 1);
     }
     for (int t = 0; t < NT; ++t) {
-      mbar_init(&s_full[t][0], 1);
-      mbar_init(&s_full[t][1], 1);
-      mbar_init(&p_full[t], kTcSoftmaxThreads);
-      mbar_init(&o_full[t], 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&s_full[t][b], 1);
+        mbar_init(&p_full[t][b], kTcSoftmaxThreads);
+        mbar_init(&o_full[t][b], 1);
+      }
     }
     fence_mbar_init();
   }
@@ -220,14 +230,15 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
         const int s = i % kTcStages;
         const uint32_t v_base = smem_u32(sKV + s * kStageBytes + kKvBytes);
         for (int t = 0; t < n_tiles; ++t) {
-          mbar_wait(&p_full[t], i & 1);  // P_i in smem, S_i read out, O rescaled if needed
+          // P_i in smem, S_i read out, O rescaled if needed
+          mbar_wait(&p_full[t][i & 1], (i >> 1) & 1);
           tc_fence_after();
-          const uint32_t p_base = smem_u32(sP + t * kPBytes);
+          const uint32_t p_base = smem_u32(sP + (t * 2 + (i & 1)) * kPBytes);
 #pragma unroll
           for (int j = 0; j < kPageTokens / 16; ++j)  // O += P_i V_i (16 keys per step)
             umma_bf16(tmem + o_col<NT>(t), umma_desc_k128(p_base + j * 32),
                       umma_desc_mn128(v_base + j * 2048, kBox), id_o, (i | j) != 0);
-          umma_commit(&o_full[t]);
+          umma_commit(&o_full[t][i & 1]);
         }
         umma_commit(&kv_empty[s]);
         if (i + kTcStages < npages) {
@@ -240,7 +251,6 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
   } else if (qt < n_tiles) {
     // softmax: thread = TMEM lane = MMA row of tile qt
     const uint32_t t_row = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    uint8_t* sPt = sP + qt * kPBytes;
     float m = -CUDART_INF_F, l = 0.f;
     for (int i = 0; i < npages; ++i) {
       mbar_wait(&s_full[qt][i & 1], (i >> 1) & 1);
@@ -257,25 +267,29 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
           for (int e = 0; e < 16; ++e) sv[c * 16 + e] = __uint_as_float(rr[c][e]);
       }
       const int kbase = i * kPageTokens;
-      float mx = -CUDART_INF_F;
+      if (valid && kbase + kPageTokens - 1 <= pos) {  // every key of the page visible
 #pragma unroll
-      for (int j = 0; j < kPageTokens; ++j) {
-        sv[j] = (valid && kbase + j <= pos) ? sv[j] * scale_log2 : -CUDART_INF_F;
-        mx = fmaxf(mx, sv[j]);
+        for (int j = 0; j < kPageTokens; ++j) sv[j] *= scale_log2;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kPageTokens; ++j)
+          sv[j] = (valid && kbase + j <= pos) ? sv[j] * scale_log2 : -CUDART_INF_F;
       }
+      float mx4[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
+#pragma unroll
+      for (int j = 0; j < kPageTokens; ++j) mx4[j & 3] = fmaxf(mx4[j & 3], sv[j]);
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       // lazy rescale: move m only when the row max outgrows it by 2^8
       const bool grow = mx > m + kRescaleLog2;
       const float m_new = grow ? mx : m;
       const float alpha = grow ? exp2f(m - m_new) : 1.f;  // 0 on the first page
       m = m_new;
       const float mu = m == -CUDART_INF_F ? 0.f : m;
-      // the previous page's P.V must be done before P is rewritten and
-      // before O is rescaled
-      if (i > 0) {
-        mbar_wait(&o_full[qt], (i - 1) & 1);
-        tc_fence_after();
-      }
+      // O is rescaled only once the previous page's P.V is done; this
+      // page's P buffer is free once the P.V of page i - 2 is done
       if (i > 0 && __any_sync(0xffffffffu, grow)) {  // O *= alpha (warp-collective)
+        mbar_wait(&o_full[qt][(i - 1) & 1], ((i - 1) >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
         for (int c = 0; c < HD / 16; ++c) {
           uint32_t rr[16];
@@ -287,13 +301,18 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
         }
         tmem_wait_st();
       }
+      if (i >= 2) {
+        mbar_wait(&o_full[qt][i & 1], ((i - 2) >> 1) & 1);
+        tc_fence_after();
+      }
+      uint8_t* sPt = sP + (qt * 2 + (i & 1)) * kPBytes;
       float rs = 0.f;
 #pragma unroll
       for (int c = 0; c < kPageTokens / 8; ++c) {  // P row -> smem (K-major SW128)
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float a = exp2f(sv[c * 8 + 2 * e] - mu), b = exp2f(sv[c * 8 + 2 * e + 1] - mu);
+          const float a = ex2_ftz(sv[c * 8 + 2 * e] - mu), b = ex2_ftz(sv[c * 8 + 2 * e + 1] - mu);
           const uint32_t pk = pack_bf16x2(a, b);
           // the row sum is taken over the bf16-rounded P the MMA consumes
           const __nv_bfloat162 r2 = *reinterpret_cast<const __nv_bfloat162*>(&pk);
@@ -306,9 +325,10 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
       l = l * alpha + rs;
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(&p_full[qt]);
+      mbar_arrive(&p_full[qt][i & 1]);
     }
-    mbar_wait(&o_full[qt], (npages - 1) & 1);
+    // MMAs complete in issue order: the last page's commit covers them all
+    mbar_wait(&o_full[qt][(npages - 1) & 1], ((npages - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     bf16* dst = out + static_cast<size_t>(tile.q_row + t0 + tok) * out_row_stride +
@@ -346,7 +366,7 @@ int launch_tc_nt(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf
                  int q_row_stride, int n_q, const int* pt, int pt_stride,
                  const PrefillTile* tiles, int n_tiles, bf16* out, int out_row_stride,
                  cudaStream_t st) {
-  constexpr int kSmem = NT * ((HD / 64) * kRows * 128 + kRows * 128) +
+  constexpr int kSmem = NT * ((HD / 64) * kRows * 128 + 2 * kRows * 128) +
                         kTcStages * 2 * (HD / 64) * kPageTokens * 128 + 1024;
   static bool attr = false;
   if (!attr) {

@@ -497,3 +497,15 @@ class LiveEngine(Engine):
 
     def drain(self) -> None:
         self._resolve_iterations(block=True)
+
+    def stall_report(self) -> dict:
+        """Diagnostic for a stalled run: every unfinished request's state and
+        the KV accounting."""
+        reqs = {r.id: (r.phase, r.chain_state, r.swap_state, r.kv_place, r.ctx, r.kv_held,
+                       r.gpu_reserved, r.swap_reserved, r.tokens_out, r.output_len)
+                for r in self.requests.values() if r.phase not in ("done", "rejected")}
+        return {"gpu_used": self.kv.gpu_used, "gpu_capacity": self.kv.gpu_capacity,
+                "host_used": list(self.kv.host_used), "pending_injections": len(self.pending_injections),
+                "pg": (len(self._pg_inj), len(self._pg_enq), self._pg_done, self._pg_merged,
+                       len(self._order)),
+                "reqs": reqs}

@@ -65,7 +65,7 @@ def test_live_engine_matches_oracle_replay(cuda, pace_layers, pace_tail, device_
 
     cfg, w, eng, step, n = _live_run(pace_layers, pace_tail, device_merges=device_merges)
     c = eng.counters
-    assert not eng.stalled and c["tokens_total"] == 6280, (n, c)
+    assert not eng.stalled and c["tokens_total"] == 6280, (n, c, eng.stall_report())
     # the async machinery the bench relies on was exercised
     assert c["swap_out_done"] > 0 and c["injections"] > 0, c
     assert c["merges"] > 0 and c["be_tokens_cpu"] > 0, c
