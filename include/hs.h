@@ -90,11 +90,13 @@ int hs_op_decode_attention(const void* kv_pool, int layers, int pages, int n_kv,
                            float* o_part, float* lse_part, void* stream);
 /* K1+K2 fused: the last CTA of each (row, KV head) merges the row's chunks
  * and writes out[row] (bf16); counters: int32[rows * n_kv], zeroed once
- * (the kernel resets them). */
+ * (the kernel resets them).  rows: decode rows of the list; when every row
+ * is one chunk (n_chunks == rows) a small launch splits each row's pages
+ * over a thread-block cluster merged in distributed shared memory. */
 int hs_op_decode_attention_fused(const void* kv_pool, int layers, int pages, int n_kv,
                                  int head_dim, int layer, const void* q, int q_row_stride, int n_q,
                                  const int* page_table, int pt_stride, const int* chunks,
-                                 int n_chunks, const int* row_chunk_begin, float* o_part,
+                                 int n_chunks, int rows, const int* row_chunk_begin, float* o_part,
                                  float* lse_part, int* counters, void* out, int out_row_stride,
                                  void* stream);
 /* K2: LSE-merge the chunks of each row (row_chunk_begin: int32[rows+1]). */

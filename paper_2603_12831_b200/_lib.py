@@ -31,7 +31,7 @@ _SIGNATURES: dict[str, list] = {
     "hs_op_gemm_bf16_blocked": [_vp, _i, _i, _vp, _i, _i, _fp, _i, C.POINTER(C.c_int), _vp],
     "hs_op_decode_attention": [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _ip, _i, _ip, _i, _fp, _fp,
                                _vp],
-    "hs_op_decode_attention_fused": [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _ip, _i, _ip, _i,
+    "hs_op_decode_attention_fused": [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _ip, _i, _ip, _i, _i,
                                      _ip, _fp, _fp, _ip, _vp, _i, _vp],
     "hs_op_decode_combine": [_fp, _fp, _ip, _i, _i, _i, _i, _vp, _i, _fp, _vp],
     "hs_op_prefill_attention": [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _ip, _i, _ip, _i, _vp, _i,

@@ -18,10 +18,14 @@
 // instruction used for the tiny GQA tiles is irrelevant to that bound.
 #include <math_constants.h>
 
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace hs {
 
@@ -40,7 +44,10 @@ int make_kv_map(CUtensorMap* map, const bf16* pool, const KvGeom& g) {
 // WG warp groups of 4 warps: with WG = 2 the groups take alternate pages of
 // the chunk (one CTA per SM for small batches, where the page loop's
 // latency, not HBM, bounds the launch), with twice the stages in flight.
-template <int HD, int WG>
+// CL > 1 (whole rows, small launches): the CL CTAs of a cluster split the
+// chunk's pages into contiguous ranges and rank 0 LSE-merges their
+// normalised partials through distributed shared memory.
+template <int HD, int WG, int CL>
 __global__ void __launch_bounds__(kDecThreads * WG, WG == 1 ? 2 : 1)
     decode_attn_kernel(const __grid_constant__ CUtensorMap kv_map, KvGeom geom, int layer,
                        const bf16* __restrict__ q, int q_row_stride, int n_q,
@@ -66,11 +73,17 @@ __global__ void __launch_bounds__(kDecThreads * WG, WG == 1 ? 2 : 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
-  const DecodeChunk ch = chunks[blockIdx.x];
+  const int crank = CL > 1 ? static_cast<int>(blockIdx.x % CL) : 0;  // rank in the x-cluster
+  const DecodeChunk ch = chunks[CL > 1 ? blockIdx.x / CL : blockIdx.x];
   const int kvh = blockIdx.y;
   const int G = n_q / geom.n_kv;
-  const int npages = ch.page_end - ch.page_begin;
-  const int* pt = page_table + static_cast<size_t>(ch.slot) * pt_stride + ch.page_begin;
+  // this CTA's pages: the chunk, or its crank-th contiguous range
+  const int cpages = ch.page_end - ch.page_begin;
+  const int cper = (cpages + CL - 1) / CL;
+  const int p_lo = min(cpages, crank * cper);
+  const int npages = min(cpages, p_lo + cper) - p_lo;
+  const int page0 = ch.page_begin + p_lo;
+  const int* pt = page_table + static_cast<size_t>(ch.slot) * pt_stride + page0;
 
   // the chunk's page ids, read once: the refill of a stage then issues its
   // TMA at once instead of waiting on a dependent global load per page (the
@@ -102,7 +115,7 @@ __global__ void __launch_bounds__(kDecThreads * WG, WG == 1 ? 2 : 1)
   // cannot hold this layer's new token (position ctx-1, written by the QKV
   // epilogue just before) are safe to stream; the chunk list and the page
   // table were uploaded ahead of the iteration.
-  const int safe = max(0, min(npages, (ch.ctx - 1) / kPageTokens - ch.page_begin));
+  const int safe = max(0, min(npages, (ch.ctx - 1) / kPageTokens - page0));
   const int first = min(kStages, npages);
   if (threadIdx.x == 0)
     for (int i = 0; i < min(first, safe); ++i) issue(i);
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(kDecThreads * WG, WG == 1 ? 2 : 1)
    if (i < npages) {
     const int s = i % kStages;
     mbar_wait(&full[s], (i / kStages) & 1);
-    const int tok0 = (ch.page_begin + i) * kPageTokens + tb;
+    const int tok0 = (page0 + i) * kPageTokens + tb;
     if (tok0 < ch.ctx) {  // warp-uniform
       const uint32_t kbase = smem_u32(smem + s * kStageBytes);
       const uint32_t vbase = kbase + kHalf;
@@ -255,6 +268,53 @@ __global__ void __launch_bounds__(kDecThreads * WG, WG == 1 ? 2 : 1)
         make_float2(o[nt][2] * f1, o[nt][3] * f1);
   }
   __syncthreads();
+  if constexpr (CL > 1) {
+    // this CTA's normalised partial [G][HD] and its LSE (log2 units), then
+    // rank 0 merges the cluster's partials out of the peers' shared memory
+    float* s_o = so + kWarps * 16 * SO;
+    __shared__ float s_lse[16];
+    for (int idx = threadIdx.x; idx < G * HD; idx += kThreads) {
+      const int r = idx / HD, d = idx % HD;
+      float Mr = -CUDART_INF_F;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) Mr = fmaxf(Mr, sm_m[w][r]);
+      const float Mur = Mr == -CUDART_INF_F ? 0.f : Mr;
+      float L = 0.f, acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        L += sm_l[w][r] * exp2f(sm_m[w][r] - Mur);
+        acc += so[(w * 16 + r) * SO + d];
+      }
+      s_o[idx] = L > 0.f ? acc / L : 0.f;
+      if (d == 0) s_lse[r] = L > 0.f ? Mur + log2f(L) : -CUDART_INF_F;
+    }
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (crank == 0) {
+      for (int idx = threadIdx.x; idx < G * HD; idx += kThreads) {
+        const int r = idx / HD, d = idx % HD;
+        float lk[CL];
+        float mx = -CUDART_INF_F;
+#pragma unroll
+        for (int k = 0; k < CL; ++k) {
+          lk[k] = *cluster.map_shared_rank(&s_lse[r], k);
+          mx = fmaxf(mx, lk[k]);
+        }
+        const float mu = mx == -CUDART_INF_F ? 0.f : mx;
+        float ws = 0.f, acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < CL; ++k) {
+          const float w = exp2f(lk[k] - mu);
+          ws += w;
+          acc += w * *cluster.map_shared_rank(&s_o[idx], k);
+        }
+        out[static_cast<size_t>(ch.row) * out_row_stride + (kvh * G + r) * HD + d] =
+            __float2bfloat16(ws > 0.f ? acc / ws : 0.f);
+      }
+    }
+    cluster.sync();  // the peers' shared memory stays alive until rank 0 is done
+    return;
+  }
   const int base = (blockIdx.x * geom.n_kv + kvh) * G;
   const int c_lo = out ? row_chunk_begin[ch.row] : 0;
   const int n_row_chunks = out ? row_chunk_begin[ch.row + 1] - c_lo : 0;
@@ -387,7 +447,7 @@ __global__ void decode_combine_kernel(const float* __restrict__ o_part,
   if (lse_out && lane == 0) lse_out[pair] = wsum > 0.f ? mu + logf(wsum) : -CUDART_INF_F;
 }
 
-template <int HD, int WG>
+template <int HD, int WG, int CL = 1>
 static int launch_decode_wg(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
                             int q_row_stride, int n_q, const int* pt, int pt_stride,
                             const DecodeChunk* chunks, int n_chunks, float* o_part,
@@ -395,17 +455,22 @@ static int launch_decode_wg(const CUtensorMap& kv_map, const KvGeom& g, int laye
                             int* counters, bf16* out, int out_row_stride) {
   constexpr int kStageBytes = 2 * (HD / 64) * kPageTokens * 128;
   constexpr int kSmem = kDecStages * WG * kStageBytes + 1024;
-  static_assert(4 * WG * 16 * (HD + 8) * 4 <= kDecStages * WG * kStageBytes,
+  static_assert(4 * WG * 16 * (HD + 8) * 4 + 16 * HD * 4 <= kDecStages * WG * kStageBytes,
                 "merge scratch must fit");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(decode_attn_kernel<HD, WG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmem);
+    cudaFuncSetAttribute(decode_attn_kernel<HD, WG, CL>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
-  dim3 grid(n_chunks, g.n_kv);
-  return launch_pdl(decode_attn_kernel<HD, WG>, dim3(grid), dim3(kDecThreads * WG), kSmem, st,
+  dim3 grid(n_chunks * CL, g.n_kv);
+  if (CL > 1)
+    return launch_pdl_cluster(decode_attn_kernel<HD, WG, CL>, dim3(grid), dim3(kDecThreads * WG),
+                              kSmem, st, CL, kv_map, g, layer, q, q_row_stride, n_q, pt,
+                              pt_stride, chunks, o_part, lse_part, scale_log2, row_chunk_begin,
+                              counters, out, out_row_stride);
+  return launch_pdl(decode_attn_kernel<HD, WG, CL>, dim3(grid), dim3(kDecThreads * WG), kSmem, st,
                     kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, chunks, o_part,
                     lse_part, scale_log2, row_chunk_begin, counters, out, out_row_stride);
 }
@@ -418,12 +483,29 @@ static int launch_decode(const CUtensorMap& kv_map, const KvGeom& g, int layer, 
                          int q_row_stride, int n_q, const int* pt, int pt_stride,
                          const DecodeChunk* chunks, int n_chunks, float* o_part, float* lse_part,
                          cudaStream_t st, const int* row_chunk_begin = nullptr,
-                         int* counters = nullptr, bf16* out = nullptr, int out_row_stride = 0) {
+                         int* counters = nullptr, bf16* out = nullptr, int out_row_stride = 0,
+                         bool rows_whole = false) {
   static const int forced = [] {
     const char* e = getenv("HS_DEC_WG");
     return e ? atoi(e) : 0;
   }();
-  const bool two = forced ? forced == 2 : n_chunks * g.n_kv <= 148;
+  static const int cl_max = [] {
+    const char* e = getenv("HS_DEC_CLUSTER");
+    return e ? atoi(e) : 4;
+  }();
+  // whole rows of a launch that leaves SMs idle: a cluster per chunk
+  const int ctas = n_chunks * g.n_kv;
+  if (out && rows_whole && !forced) {
+    if (cl_max >= 4 && 4 * ctas <= 148)
+      return launch_decode_wg<HD, 2, 4>(kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride,
+                                        chunks, n_chunks, o_part, lse_part, st, row_chunk_begin,
+                                        counters, out, out_row_stride);
+    if (cl_max >= 2 && 2 * ctas <= 148)
+      return launch_decode_wg<HD, 2, 2>(kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride,
+                                        chunks, n_chunks, o_part, lse_part, st, row_chunk_begin,
+                                        counters, out, out_row_stride);
+  }
+  const bool two = forced ? forced == 2 : ctas <= 148;
   if (two)
     return launch_decode_wg<HD, 2>(kv_map, g, layer, q, q_row_stride, n_q, pt, pt_stride, chunks,
                                    n_chunks, o_part, lse_part, st, row_chunk_begin, counters, out,
@@ -452,17 +534,17 @@ int decode_attention_fused(const CUtensorMap& kv_map, const KvGeom& g, int layer
                            int q_row_stride, int n_q, const int* page_table, int pt_stride,
                            const DecodeChunk* chunks, int n_chunks, const int* row_chunk_begin,
                            float* o_part, float* lse_part, int* counters, bf16* out,
-                           int out_row_stride, cudaStream_t st) {
+                           int out_row_stride, cudaStream_t st, bool rows_whole) {
   if (n_chunks <= 0) return HS_OK;
   if (n_q % g.n_kv || n_q / g.n_kv > 16) return HS_E_CONFIG;
   if (g.head_dim == 128)
     return launch_decode<128>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride,
                               chunks, n_chunks, o_part, lse_part, st, row_chunk_begin, counters,
-                              out, out_row_stride);
+                              out, out_row_stride, rows_whole);
   if (g.head_dim == 64)
     return launch_decode<64>(kv_map, g, layer, q, q_row_stride, n_q, page_table, pt_stride, chunks,
                              n_chunks, o_part, lse_part, st, row_chunk_begin, counters, out,
-                             out_row_stride);
+                             out_row_stride, rows_whole);
   return HS_E_CONFIG;
 }
 

@@ -241,11 +241,14 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
           umma_commit(&o_full[t][i & 1]);
         }
         umma_commit(&kv_empty[s]);
+        // S_{i+2} first (its S buffer was read out, p_full_i; its page is
+        // resident), then the refill of page i's stage, which has to wait
+        // for P_i V_i to finish
+        if (i + 2 < npages) mma_s(i + 2);
         if (i + kTcStages < npages) {
           mbar_wait(&kv_empty[s], (i / kTcStages) & 1);  // K_i, V_i consumed
           issue(i + kTcStages);
         }
-        if (i + 2 < npages) mma_s(i + 2);  // S buffer i & 1 was read out (p_full_i)
       }
     }
   } else if (qt < n_tiles) {

@@ -145,7 +145,7 @@ int hs_op_decode_attention(const void* kv_pool, int layers, int pages, int n_kv,
 int hs_op_decode_attention_fused(const void* kv_pool, int layers, int pages, int n_kv,
                                  int head_dim, int layer, const void* q, int q_row_stride, int n_q,
                                  const int* page_table, int pt_stride, const int* chunks,
-                                 int n_chunks, const int* row_chunk_begin, float* o_part,
+                                 int n_chunks, int rows, const int* row_chunk_begin, float* o_part,
                                  float* lse_part, int* counters, void* out, int out_row_stride,
                                  void* stream) {
   KvGeom g{layers, pages, n_kv, head_dim};
@@ -156,7 +156,7 @@ int hs_op_decode_attention_fused(const void* kv_pool, int layers, int pages, int
       decode_attention_fused(m, g, layer, static_cast<const bf16*>(q), q_row_stride, n_q,
                              page_table, pt_stride, reinterpret_cast<const DecodeChunk*>(chunks),
                              n_chunks, row_chunk_begin, o_part, lse_part, counters,
-                             static_cast<bf16*>(out), out_row_stride, S(stream)),
+                             static_cast<bf16*>(out), out_row_stride, S(stream), n_chunks == rows),
       "decode_attention_fused");
 }
 

@@ -62,6 +62,29 @@ inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
   return launched();
 }
 
+// Same, as clusters of `cluster_x` CTAs along x (distributed shared memory).
+template <typename... KArgs, typename... Args>
+inline int launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cluster_x;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  HProf hp(HP_LAUNCH);
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  return launched();
+}
+
 // ---- KV pool geometry (used by GEMM epilogues and attention) ----
 struct KvGeom {
   int layers, pages, n_kv, head_dim;
@@ -185,12 +208,14 @@ int decode_attention(const CUtensorMap& kv_map, const KvGeom& g, int layer, cons
                      cudaStream_t st);
 // Fused variant: the last CTA of each (row, KV head) LSE-merges the row's
 // chunks (self-resetting counters [rows * n_kv], zero-initialised) and writes
-// the bf16 output; single-chunk rows are written directly.
+// the bf16 output; single-chunk rows are written directly.  rows_whole (every
+// row is one chunk): a small launch splits each chunk's pages over a cluster
+// of CTAs merged through distributed shared memory.
 int decode_attention_fused(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf16* q,
                            int q_row_stride, int n_q, const int* page_table, int pt_stride,
                            const DecodeChunk* chunks, int n_chunks, const int* row_chunk_begin,
                            float* o_part, float* lse_part, int* counters, bf16* out,
-                           int out_row_stride, cudaStream_t st);
+                           int out_row_stride, cudaStream_t st, bool rows_whole = false);
 int decode_combine(const float* o_part, const float* lse_part, const int* row_chunk_begin,
                    int rows, int n_q, int n_kv, int head_dim, bf16* out, int out_row_stride,
                    float* lse_out, cudaStream_t st);

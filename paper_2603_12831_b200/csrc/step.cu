@@ -1239,7 +1239,7 @@ int hs_layer(hs_ctx* c, const hs_layer_desc* d) {
   RC(decode_attention_fused(c->m_kv, c->geom, l, c->qbuf, nqh, m.n_q, c->page_table,
                             r.max_pages_per_req, reinterpret_cast<const DecodeChunk*>(c->it_chunks),
                             c->n_chunks, c->it_cbeg, c->o_part, c->lse_part, c->dec_counters,
-                            c->attn.p, nqh, st));
+                            c->attn.p, nqh, st, c->n_chunks == c->D));
   }
   {
   ProfScope pp(c, 2, c->pre_kv_tokens * 2.0 * m.n_kv * m.hd * 2.0, 4.0 * c->pre_units * nqh);

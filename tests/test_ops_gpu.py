@@ -338,7 +338,8 @@ def test_decode_attention_fused_combine(cuda, n_q, n_kv, hd, chunk_pages):
     for _ in range(2):
         out = torch.zeros(len(ctxs), n_q * hd, dtype=torch.bfloat16, device=cuda)
         _lib.call("hs_op_decode_attention_fused", _p(dpool), layers, pages, n_kv, hd, 0, _p(dq),
-                  n_q * hd, n_q, _p(dpt), max_pages, _p(dch), len(chunks), _p(dbeg), _p(opart),
+                  n_q * hd, n_q, _p(dpt), max_pages, _p(dch), len(chunks), len(ctxs), _p(dbeg),
+                  _p(opart),
                   _p(lpart), _p(cnt), _p(out), n_q * hd, None)
         torch.cuda.synchronize()
         got = out.float().cpu().numpy().reshape(len(ctxs), n_q, hd)
@@ -414,7 +415,8 @@ def test_decode_attention_long_context(cuda, ctxs):
     lpart = torch.zeros(len(chunks) * n_q, dtype=torch.float32, device=cuda)
     out = torch.zeros(len(ctxs), n_q * hd, dtype=torch.bfloat16, device=cuda)
     _lib.call("hs_op_decode_attention_fused", _p(dpool), 1, pages, n_kv, hd, 0, _p(dq),
-              n_q * hd, n_q, _p(dpt), max_pages, _p(dch), len(chunks), _p(dbeg), _p(opart),
+              n_q * hd, n_q, _p(dpt), max_pages, _p(dch), len(chunks), len(ctxs), _p(dbeg),
+              _p(opart),
               _p(lpart), _p(cnt), _p(out), n_q * hd, None)
     torch.cuda.synchronize()
     got = out.float().cpu().numpy().reshape(len(ctxs), n_q, hd)

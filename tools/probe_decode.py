@@ -69,7 +69,7 @@ for g, ctx in cases:
 
     def one(layer=0):
         _lib.call("hs_op_decode_attention_fused", p(pool), layers, pages, n_kv, hd, layer, p(q),
-                  n_q * hd, n_q, p(pt), npg, p(ch), len(chunks), p(beg), p(op), p(lp), p(cnt),
+                  n_q * hd, n_q, p(pt), npg, p(ch), len(chunks), g, p(beg), p(op), p(lp), p(cnt),
                   p(out), n_q * hd, st)
 
     def stream32():
