@@ -19,7 +19,9 @@
 //                      issued two pages ahead; A = Q K-major smem, B = the K
 //                      page K-major as TMA staged it)
 //   P_i = exp2(S_i*scale - m), one TMEM lane (row) per thread of the tile's
-//         four warps; bf16 P to smem (SWIZZLE_128B, K-major)
+//         four warps (one FFMA + one MUFU.EX2 per score; the row sum over
+//         the fp32 P); bf16 P to smem (SWIZZLE_128B, K-major), double-
+//         buffered so a page's softmax overlaps the previous page's P.V
 //   O_t += P_i V_i     tcgen05.mma M=128 N=hd K=64, accumulated in TMEM
 //                      (B = the V page, MN-major)
 //
@@ -270,18 +272,16 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
           for (int e = 0; e < 16; ++e) sv[c * 16 + e] = __uint_as_float(rr[c][e]);
       }
       const int kbase = i * kPageTokens;
-      if (valid && kbase + kPageTokens - 1 <= pos) {  // every key of the page visible
-#pragma unroll
-        for (int j = 0; j < kPageTokens; ++j) sv[j] *= scale_log2;
-      } else {
+      if (!(valid && kbase + kPageTokens - 1 <= pos)) {  // diagonal page / padding row
 #pragma unroll
         for (int j = 0; j < kPageTokens; ++j)
-          sv[j] = (valid && kbase + j <= pos) ? sv[j] * scale_log2 : -CUDART_INF_F;
+          if (!(valid && kbase + j <= pos)) sv[j] = -CUDART_INF_F;
       }
+      // row max of the raw scores (the scale is positive: it commutes)
       float mx4[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
 #pragma unroll
       for (int j = 0; j < kPageTokens; ++j) mx4[j & 3] = fmaxf(mx4[j & 3], sv[j]);
-      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
       // lazy rescale: move m only when the row max outgrows it by 2^8
       const bool grow = mx > m + kRescaleLog2;
       const float m_new = grow ? mx : m;
@@ -309,22 +309,24 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
         tc_fence_after();
       }
       uint8_t* sPt = sP + (qt * 2 + (i & 1)) * kPBytes;
-      float rs = 0.f;
+      // P = 2^(s * scale - m): one FFMA and one MUFU.EX2 per score; the row
+      // sum over the fp32 P (four chains)
+      const float nmu = -mu;
+      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int c = 0; c < kPageTokens / 8; ++c) {  // P row -> smem (K-major SW128)
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float a = ex2_ftz(sv[c * 8 + 2 * e] - mu), b = ex2_ftz(sv[c * 8 + 2 * e + 1] - mu);
-          const uint32_t pk = pack_bf16x2(a, b);
-          // the row sum is taken over the bf16-rounded P the MMA consumes
-          const __nv_bfloat162 r2 = *reinterpret_cast<const __nv_bfloat162*>(&pk);
-          rs += __bfloat162float(r2.x) + __bfloat162float(r2.y);
-          w[e] = pk;
+          const float a = ex2_ftz(fmaf(sv[c * 8 + 2 * e], scale_log2, nmu));
+          const float b = ex2_ftz(fmaf(sv[c * 8 + 2 * e + 1], scale_log2, nmu));
+          rs4[e] += a + b;
+          w[e] = pack_bf16x2(a, b);
         }
         *reinterpret_cast<uint4*>(sPt + r * 128 + ((c ^ (r & 7)) << 4)) =
             make_uint4(w[0], w[1], w[2], w[3]);
       }
+      const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
       l = l * alpha + rs;
       fence_proxy_async_smem();
       tc_fence_before();
