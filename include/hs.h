@@ -70,6 +70,11 @@ int hs_host_attention(const void* q, const void* k, const void* v, int n_keys, i
  * n_out % 128 == 0, k % 64 == 0.  *splits_used <= max_splits. */
 int hs_op_gemm_bf16(const void* x, int tokens, int ldx, const void* w, int n_out, int k,
                     float* out_partial, int max_splits, int* splits_used, void* stream);
+/* Same product on CTA pairs (tcgen05.mma.cta_group::2, 256 weight rows x
+ * 256 tokens per pair tile; the step uses it from 256 rows up).
+ * tokens >= 256, n_out % 256 == 0, k % 64 == 0. */
+int hs_op_gemm_bf16_pair(const void* x, int tokens, int ldx, const void* w, int n_out, int k,
+                         float* out_partial, int max_splits, int* splits_used, void* stream);
 /* Same product with the weights pre-tiled [n/128][k/64][128][64] (each
  * 16 KB TMA box contiguous in HBM); hs_op_relayout_blocked converts. */
 int hs_op_relayout_blocked(const void* w, void* w_blocked, int n, int k, void* stream);

@@ -27,6 +27,7 @@ _SIGNATURES: dict[str, list] = {
     "hs_device_ok": [],
     "hs_op_gemm_bf16": [_vp, _i, _i, _vp, _i, _i, _fp, _i, C.POINTER(C.c_int), _vp],
     "hs_op_splitk_reduce": [_fp, _i, _i, _i, _fp, _vp],
+    "hs_op_gemm_bf16_pair": [_vp, _i, _i, _vp, _i, _i, _fp, _i, C.POINTER(C.c_int), _vp],
     "hs_op_relayout_blocked": [_vp, _vp, _i, _i, _vp],
     "hs_op_gemm_bf16_blocked": [_vp, _i, _i, _vp, _i, _i, _fp, _i, C.POINTER(C.c_int), _vp],
     "hs_op_decode_attention": [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _ip, _i, _ip, _i, _fp, _fp,

@@ -95,6 +95,22 @@ int hs_op_gemm_bf16(const void* x, int tokens, int ldx, const void* w, int n_out
   return cuda_status(rc, "gemm");
 }
 
+int hs_op_gemm_bf16_pair(const void* x, int tokens, int ldx, const void* w, int n_out, int k,
+                         float* out_partial, int max_splits, int* splits_used, void* stream) {
+  if (tokens < 256 || n_out % 256 || k % 64 || ldx < k || max_splits < 1)
+    return set_error(HS_E_CONFIG, "gemm_pair: bad shape tokens=%d n=%d k=%d ldx=%d", tokens,
+                     n_out, k, ldx);
+  CUtensorMap mw, mx;
+  if (make_weight_map(&mw, static_cast<const bf16*>(w), n_out, k) != HS_OK ||
+      make_act_map(&mx, static_cast<const bf16*>(x), tokens, k, ldx, 128) != HS_OK)
+    return set_error(HS_E_CUDA, "gemm_pair: cuTensorMapEncodeTiled failed");
+  Planes planes;
+  const int rc = gemm_launch_pair(mw, mx, out_partial, n_out, tokens, k, max_splits, true,
+                                  S(stream), &planes);
+  if (splits_used) *splits_used = planes.n;
+  return cuda_status(rc, "gemm_pair");
+}
+
 int hs_op_relayout_blocked(const void* w, void* w_blocked, int n, int k, void* stream) {
   return cuda_status(relayout_blocked(static_cast<const bf16*>(w), static_cast<bf16*>(w_blocked),
                                       n, k, S(stream)),

@@ -128,11 +128,12 @@ struct Planes {
   int n = 1;
   StreamK sk{0, 0, 0, 0};
   int n_tiles = 0, bn = 0;
+  int tile_m = 128;  // features per tile (256: the CTA-pair kernel, gemm_2sm.cu)
   Planes() = default;
   Planes(int uniform) : n(uniform) {}  // NOLINT(runtime/explicit)
   __host__ __device__ int count(int row, int feat) const {
     if (sk.G <= 0) return n;
-    const int t = (row / bn) * n_tiles + feat / 128;
+    const int t = (row / bn) * n_tiles + feat / tile_m;
     const long long a = static_cast<long long>(t) * sk.kb;
     return sk.owner(a + sk.kb - 1) - sk.owner(a) + 1;
   }
@@ -182,6 +183,12 @@ int gemm_pick_splits(int n_out, int k, int tokens, int bn, int max_splits);
 // Persistent stream-K GEMM; writes `*planes` (<= max_planes) fp32 partial
 // planes [planes][tokens][n_out] whose sum is the product.
 // step-level launch: per-tile planes, no zero fill (consumers take `Planes`)
+// CTA-pair GEMM (gemm_2sm.cu) for >= 256 token rows: same partial-plane
+// output; mx_half is the activation map with 128-token boxes.
+bool gemm_pair_ok(int n_out, int k, int tokens);
+int gemm_launch_pair(const CUtensorMap& mw, const CUtensorMap& mx_half, float* out, int n_out,
+                     int tokens, int k, int max_planes, bool uniform_planes, cudaStream_t st,
+                     Planes* planes);
 int gemm_launch_planes(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,
                        int tokens, int k, int max_planes, cudaStream_t st, Planes* planes);
 int gemm_launch(const CUtensorMap& mw, const CUtensorMap& mx, int bn, float* out, int n_out,

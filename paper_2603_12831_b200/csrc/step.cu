@@ -181,6 +181,9 @@ int gemm(hs_ctx* c, const CUtensorMap& mw, const ActBuf& x, int tokens, int n_ou
   const size_t per_split = static_cast<size_t>(tokens) * n_out;
   const int cap = static_cast<int>(std::min<size_t>(16, c->part_floats / per_split));
   if (cap < 1) return set_error(HS_E_CAPACITY, "split-K buffer too small for %d x %d", tokens, n_out);
+  if (gemm_pair_ok(n_out, k, tokens))  // prefill-sized batches: CTA pairs
+    return gemm_launch_pair(mw, x.maps[bn_index(128)], c->part, n_out, tokens, k, cap, false,
+                            c->st, planes_out);
   return gemm_launch_planes(mw, x.maps[bn_index(bn)], bn, c->part, n_out, tokens, k, cap, c->st,
                             planes_out);
 }

@@ -72,6 +72,31 @@ def test_gemm_tcgen05(cuda, tokens, n, k):
     assert _rel(out.cpu().numpy().reshape(tokens, n), ref) < 1e-4
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("tokens,n,k", [(256, 256, 256), (300, 512, 512), (512, 768, 1024),
+                                        (1024, 1024, 4096), (700, 6144, 4096)])
+def test_gemm_cta_pair(cuda, tokens, n, k):
+    """K3 on CTA pairs (tcgen05.mma.cta_group::2) against the oracle; the
+    partial planes sum to the product."""
+    import torch
+    from paper_2603_12831_b200 import _lib
+
+    rng = np.random.default_rng(tokens * 5 + n + k)
+    x = _bf16_np(rng, (tokens, k))
+    w = _bf16_np(rng, (n, k), 0.05)
+    xd, wd = _t(x, cuda, torch.bfloat16), _t(w, cuda, torch.bfloat16)
+    max_splits = 16
+    part = torch.full((max_splits * tokens * n,), float("nan"), dtype=torch.float32, device=cuda)
+    out = torch.zeros(tokens * n, dtype=torch.float32, device=cuda)
+    used = C.c_int(0)
+    _lib.call("hs_op_gemm_bf16_pair", _p(xd), tokens, k, _p(wd), n, k, _p(part), max_splits,
+              C.byref(used), None)
+    _lib.call("hs_op_splitk_reduce", _p(part), used.value, tokens, n, _p(out), None)
+    torch.cuda.synchronize()
+    ref = O.gemm(x, w)
+    assert _rel(out.cpu().numpy().reshape(tokens, n), ref) < 1e-4, used.value
+
+
 def _make_pool(rng, layers, pages, n_kv, hd):
     pool = _bf16_np(rng, (layers, pages, 2, n_kv, 64, hd))
     return pool
