@@ -12,6 +12,10 @@ echo "== longctx"; timeout 1200 python bench.py --workload longctx --steps 20 --
 echo "== launch list (whole iterations, 8 LS decodes x 700 + 2 merges/layer)"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_8x700_m2.csv python tools/probe_step.py 8 700 2 6 > $O/ncu_launch.log 2>&1
 python tools/ncu_summary.py $O/launches_8x700_m2.csv > $O/launches_8x700_m2.txt; head -16 $O/launches_8x700_m2.txt
+echo "== kernel probes"
+timeout 300 python tools/probe_prefill.py > $O/probe_prefill.jsonl 2>&1; tail -1 $O/probe_prefill.jsonl
+timeout 300 python tools/probe_decode.py > $O/probe_decode.jsonl 2>&1; grep '"g": 8, "ctx": 700' $O/probe_decode.jsonl | head -1
+timeout 300 python tools/probe_gemm_pair.py 256 512 1024 > $O/probe_gemm_pair.jsonl 2>&1; tail -2 $O/probe_gemm_pair.jsonl
 echo "== K6 capture (1024-token chunk after 31744)"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:prefill_attn_tc -s 74 -c 1 -o $O/ncu_prefill_tc_32k python tools/probe_prefill.py > $O/ncu_prefill.log 2>&1; tail -1 $O/ncu_prefill.log
 ls $O
