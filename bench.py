@@ -653,11 +653,16 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    import torch
+
+    # ranks beyond the box's GPUs time-share them (a functional multi-rank
+    # run on a smaller box; gpus_active reports the distinct devices)
+    n_dev = max(1, torch.cuda.device_count())
+    dev = local % n_dev
     if world > 1:
-        import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
+        torch.cuda.set_device(dev)
         dist.init_process_group("gloo")
         if world != args.gpus:
             raise SystemExit(f"bench: WORLD_SIZE {world} != --gpus {args.gpus}")
@@ -666,13 +671,13 @@ def run_ours(args) -> None:
 
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
     t_setup = time.perf_counter()
-    rep = Replica(args, world, rank, local, local_world)
+    rep = Replica(args, world, rank, local, local_world, device=dev)
     model, step = rep.model, rep.step
     L = model.n_layers
     rep.start(args.ls_rate)
     setup_s = time.perf_counter() - t_setup
     warm_iters = rep.warm(args.warmup * L, args.warmup_s, max(args.warmup, 40) * L)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev) as clocks:
         m = timed_window(rep, args.steps * L, dist)
     eng = rep.engine
     iters = m["iters"]
@@ -734,7 +739,8 @@ def run_ours(args) -> None:
         "data": "synthetic (random-init weights, synthetic KV, Poisson LS trace)",
         "config": bench_config(args, model, rep.rt.cpu_threads, world),
         "iterations_timed": len(iters), "warmup_iterations": warm_iters,
-        "gpus_active": int(tot[6]),
+        "gpus_active": int(min(tot[6], n_dev * (world // max(1, local_world)))),
+        "gpus_time_shared": bool(local_world > n_dev),
         "be_prefill_tok_s": (sum(i.get("be_chunk_tokens", 0) for i in iters) * world
                              / device_max) if device_max > 0 else 0.0,
         "ls_tpot_attainment": attain, "ls_tpot_p99_ms": float(mx[2]),
