@@ -41,6 +41,20 @@
 
 namespace hs {
 
+#ifdef HS_K6_TRACE
+// diagnostic build only (HS_NVCC_DEFS=-DHS_K6_TRACE): SM clock stamps of the
+// page handoffs of CTA (0, 0), read back with hs_debug_k6_trace
+__device__ long long g_k6_trace[8][128];
+#define K6T(ev, i)                                                              \
+  do {                                                                          \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (i) < 128) g_k6_trace[ev][i] = clock64(); \
+  } while (0)
+#else
+#define K6T(ev, i) \
+  do {             \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int kTcStages = 3;
@@ -235,6 +249,7 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
           // P_i in smem, S_i read out, O rescaled if needed
           mbar_wait(&p_full[t][i & 1], (i >> 1) & 1);
           tc_fence_after();
+          K6T(2 + t, i);
           const uint32_t p_base = smem_u32(sP + (t * 2 + (i & 1)) * kPBytes);
 #pragma unroll
           for (int j = 0; j < kPageTokens / 16; ++j)  // O += P_i V_i (16 keys per step)
@@ -243,14 +258,17 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
           umma_commit(&o_full[t][i & 1]);
         }
         umma_commit(&kv_empty[s]);
+        K6T(4, i);
         // S_{i+2} first (its S buffer was read out, p_full_i; its page is
         // resident), then the refill of page i's stage, which has to wait
         // for P_i V_i to finish
         if (i + 2 < npages) mma_s(i + 2);
+        K6T(5, i);
         if (i + kTcStages < npages) {
           mbar_wait(&kv_empty[s], (i / kTcStages) & 1);  // K_i, V_i consumed
           issue(i + kTcStages);
         }
+        K6T(6, i);
       }
     }
   } else if (qt < n_tiles) {
@@ -260,6 +278,7 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
     for (int i = 0; i < npages; ++i) {
       mbar_wait(&s_full[qt][i & 1], (i >> 1) & 1);
       tc_fence_after();
+      if (threadIdx.x == 0) K6T(0, i);
       float sv[kPageTokens];
       {
         uint32_t rr[4][16];
@@ -330,6 +349,8 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
       l = l * alpha + rs;
       fence_proxy_async_smem();
       tc_fence_before();
+      if (threadIdx.x == 0) K6T(1, i);
+      if (threadIdx.x == kRows) K6T(7, i);
       mbar_arrive(&p_full[qt][i & 1]);
     }
     // MMAs complete in issue order: the last page's commit covers them all
@@ -427,3 +448,9 @@ int prefill_attention_tc(const CUtensorMap& kv_map, const KvGeom& g, int layer, 
 }
 
 }  // namespace hs
+
+#ifdef HS_K6_TRACE
+extern "C" __attribute__((visibility("default"))) int hs_debug_k6_trace(long long* host) {
+  return cudaMemcpyFromSymbol(host, hs::g_k6_trace, sizeof(hs::g_k6_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
