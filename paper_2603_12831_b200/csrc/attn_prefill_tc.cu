@@ -57,7 +57,7 @@ __device__ long long g_k6_trace[8][128];
 
 namespace {
 
-constexpr int kTcStages = 3;
+constexpr int kTcStages = 4;
 constexpr int kMaxTiles = 2;            // Q tiles of 128 rows sharing each KV page
 constexpr int kTcSoftmaxThreads = 128;  // per tile: warps 4t..4t+3, one TMEM lane (row) each
 constexpr int kRows = 128;              // MMA M
@@ -118,6 +118,19 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[15])
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem]: the A operand (M = 128 lanes x K = 16,
+// bf16 pairs in 8 consecutive 32-bit columns) read from tensor memory
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -133,15 +146,13 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
   constexpr int kKvBytes = (HD / 64) * kBox;    // K or V of one page
   constexpr int kStageBytes = 2 * kKvBytes;
   constexpr int kQBytes = (HD / 64) * kRows * 128;  // one Q tile
-  constexpr int kPBytes = kRows * 128;          // one P tile: 128 rows x 64 keys bf16
   constexpr int kKSteps = HD / 16;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                       // [tile][kQBytes]
-  uint8_t* sP = sQ + NT * kQBytes;      // [tile][buffer][kPBytes]
-  uint8_t* sKV = sP + NT * 2 * kPBytes;
+  uint8_t* sKV = sQ + NT * kQBytes;
   __shared__ uint64_t kv_full[kTcStages], kv_empty[kTcStages];
   // S, P and the P.V commit are double-buffered by page parity: a page's
   // softmax writes its P while the previous page's P.V is still running
@@ -250,11 +261,12 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
           mbar_wait(&p_full[t][i & 1], (i >> 1) & 1);
           tc_fence_after();
           K6T(2 + t, i);
-          const uint32_t p_base = smem_u32(sP + (t * 2 + (i & 1)) * kPBytes);
+          // P_i sits in the first 32 columns of its S buffer (bf16 pairs)
+          const uint32_t p_tmem = tmem + s_col<NT>(i & 1, t);
 #pragma unroll
           for (int j = 0; j < kPageTokens / 16; ++j)  // O += P_i V_i (16 keys per step)
-            umma_bf16(tmem + o_col<NT>(t), umma_desc_k128(p_base + j * 32),
-                      umma_desc_mn128(v_base + j * 2048, kBox), id_o, (i | j) != 0);
+            umma_bf16_ts(tmem + o_col<NT>(t), p_tmem + j * 8,
+                         umma_desc_mn128(v_base + j * 2048, kBox), id_o, (i | j) != 0);
           umma_commit(&o_full[t][i & 1]);
         }
         umma_commit(&kv_empty[s]);
@@ -323,31 +335,24 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
         }
         tmem_wait_st();
       }
-      if (i >= 2) {
-        mbar_wait(&o_full[qt][i & 1], ((i - 2) >> 1) & 1);
-        tc_fence_after();
-      }
-      uint8_t* sPt = sP + (qt * 2 + (i & 1)) * kPBytes;
-      // P = 2^(s * scale - m): one FFMA and one MUFU.EX2 per score; the row
-      // sum over the fp32 P (four chains)
+      // P_i -> the first 32 columns of S buffer i & 1 (this thread's lane),
+      // the A operand of P_i V_i.  The buffer's previous P (page i - 2) was
+      // consumed before S_i was written there (the MMAs run in issue order).
       const float nmu = -mu;
       float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pw[2][16];
 #pragma unroll
-      for (int c = 0; c < kPageTokens / 8; ++c) {  // P row -> smem (K-major SW128)
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float a = ex2_ftz(fmaf(sv[c * 8 + 2 * e], scale_log2, nmu));
-          const float b = ex2_ftz(fmaf(sv[c * 8 + 2 * e + 1], scale_log2, nmu));
-          rs4[e] += a + b;
-          w[e] = pack_bf16x2(a, b);
-        }
-        *reinterpret_cast<uint4*>(sPt + r * 128 + ((c ^ (r & 7)) << 4)) =
-            make_uint4(w[0], w[1], w[2], w[3]);
+      for (int j = 0; j < kPageTokens / 2; ++j) {
+        const float a = ex2_ftz(fmaf(sv[2 * j], scale_log2, nmu));
+        const float b = ex2_ftz(fmaf(sv[2 * j + 1], scale_log2, nmu));
+        rs4[j & 3] += a + b;
+        pw[j >> 4][j & 15] = pack_bf16x2(a, b);
       }
+      tmem_st16(t_row + s_col<NT>(i & 1, qt), pw[0]);
+      tmem_st16(t_row + s_col<NT>(i & 1, qt) + 16, pw[1]);
+      tmem_wait_st();
       const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
       l = l * alpha + rs;
-      fence_proxy_async_smem();
       tc_fence_before();
       if (threadIdx.x == 0) K6T(1, i);
       if (threadIdx.x == kRows) K6T(7, i);
@@ -392,7 +397,7 @@ int launch_tc_nt(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf
                  int q_row_stride, int n_q, const int* pt, int pt_stride,
                  const PrefillTile* tiles, int n_tiles, bf16* out, int out_row_stride,
                  cudaStream_t st) {
-  constexpr int kSmem = NT * ((HD / 64) * kRows * 128 + 2 * kRows * 128) +
+  constexpr int kSmem = NT * (HD / 64) * kRows * 128 +
                         kTcStages * 2 * (HD / 64) * kPageTokens * 128 + 1024;
   static bool attr = false;
   if (!attr) {
