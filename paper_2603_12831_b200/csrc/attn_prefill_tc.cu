@@ -13,25 +13,28 @@
 // + g (G = n_q / n_kv), so each KV page is read once per group instead of
 // once per query head; a CTA holds NT = 1 or 2 Q tiles of 128 rows (2 when
 // the launch still fills every SM: two tiles share each staged page, half
-// the KV traffic per flop).  Per 64-key page i and Q tile t:
+// the KV traffic per flop).  Keys go in blocks of 128 (two KV pages staged
+// side by side by TMA).  Per key block j and Q tile t:
 //
-//   S_i = Q_t K_i^T    tcgen05.mma M=128 N=64 K=hd into TMEM (double-buffered,
-//                      issued two pages ahead; A = Q K-major smem, B = the K
-//                      page K-major as TMA staged it)
-//   P_i = exp2(S_i*scale - m), one TMEM lane (row) per thread of the tile's
-//         four warps (one FFMA + one MUFU.EX2 per score; the row sum over
-//         the fp32 P); bf16 P to smem (SWIZZLE_128B, K-major), double-
-//         buffered so a page's softmax overlaps the previous page's P.V
-//   O_t += P_i V_i     tcgen05.mma M=128 N=hd K=64, accumulated in TMEM
-//                      (B = the V page, MN-major)
+//   S_j = Q_t K_j^T    tcgen05.mma M=128 N=128 K=hd into the tile's 128 TMEM
+//                      columns (A = Q K-major smem, B = the two K pages)
+//   P_j = exp2(S_j*scale - m), one TMEM lane (row) per thread of the tile's
+//         four warps (one FFMA + one MUFU.EX2 per score, the row sum over
+//         the fp32 P), written back as bf16 pairs into the first 64 of those
+//         columns (tcgen05.st)
+//   O_t += P_j V_j     tcgen05.mma M=128 N=hd K=128 with A = P read from
+//                      TMEM and B = the V pages (MN-major), accumulated in
+//                      TMEM; then S_{j+1} of the same tile is issued into the
+//                      same columns (MMAs run in issue order)
 //
-// The running max m only moves when a row's max grows by more than 2^8
-// (lazy rescaling): P <= 256 stays exact enough in bf16 and O in TMEM is
-// rescaled (tcgen05.ld / st) only on those rare pages, so the per-page work
-// on the CUDA cores is the S read-out, 64 exp2 and the P store.  The last
-// warp issues the TMA page loads (4-stage ring: the KV stream is latency-
-// bound with fewer bytes in flight) and, from one thread, every MMA.  One
-// CTA per SM (up to 225 KB of shared memory, 512 TMEM columns).
+// The two tiles alternate on the tensor pipe: while one tile's warps run
+// the softmax of block j, the other tile's P.V and next S execute (N = 128
+// S tiles run the tensor pipe at full rate; N = 64 ran at half).  The
+// running max m only moves when a row's max grows by more than 2^8 (lazy
+// rescaling): P <= 256 stays exact enough in bf16 and O in TMEM is rescaled
+// (tcgen05.ld / st) only on those rare blocks.  The last warp issues the TMA
+// loads (2-stage ring of 128-key blocks) and, from one thread, every MMA.
+// One CTA per SM (192 KB of shared memory, 512 TMEM columns).
 #include <math_constants.h>
 
 #include <algorithm>
@@ -57,15 +60,17 @@ __device__ long long g_k6_trace[8][128];
 
 namespace {
 
-constexpr int kTcStages = 4;
+constexpr int kTcStages = 2;   // 128-key blocks of K and V in flight (64 KB each at hd 128)
+constexpr int kBlkKeys = 128;  // keys per S tile (two KV pages): N = 128 per S MMA
 constexpr int kMaxTiles = 2;            // Q tiles of 128 rows sharing each KV page
 constexpr int kTcSoftmaxThreads = 128;  // per tile: warps 4t..4t+3, one TMEM lane (row) each
 constexpr int kRows = 128;              // MMA M
 constexpr float kRescaleLog2 = 8.0f;    // lazy-rescale threshold (P <= 2^8)
 
-// TMEM columns with NT tiles: S (2 buffers x NT x 64), then O (NT x 128)
+// TMEM columns with NT tiles: S of tile t (128 fp32 columns, later P_j as 64
+// columns of bf16 pairs), then O (NT x 128)
 template <int NT>
-__host__ __device__ constexpr int s_col(int buf, int t) { return (buf * NT + t) * 64; }
+__host__ __device__ constexpr int s_col(int t) { return t * kBlkKeys; }
 template <int NT>
 __host__ __device__ constexpr int o_col(int t) { return NT * 128 + t * 128; }
 template <int NT>
@@ -142,8 +147,9 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
                            const int* __restrict__ page_table, int pt_stride,
                            const PrefillTile* __restrict__ tiles, int blocks_per_tile,
                            bf16* __restrict__ out, int out_row_stride, float scale_log2) {
-  constexpr int kBox = kPageTokens * 128;       // one [64 keys][64 el] SW128 box
-  constexpr int kKvBytes = (HD / 64) * kBox;    // K or V of one page
+  constexpr int kBox = kPageTokens * 128;          // one [64 keys][64 el] SW128 box
+  constexpr int kChunk = kBlkKeys * 128;           // [128 keys][64 el]: two pages of a chunk
+  constexpr int kKvBytes = (HD / 64) * kChunk;     // K or V of one key block
   constexpr int kStageBytes = 2 * kKvBytes;
   constexpr int kQBytes = (HD / 64) * kRows * 128;  // one Q tile
   constexpr int kKSteps = HD / 16;
@@ -151,12 +157,10 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                       // [tile][kQBytes]
-  uint8_t* sKV = sQ + NT * kQBytes;
+  uint8_t* sQ = smem;                   // [tile][kQBytes]
+  uint8_t* sKV = sQ + NT * kQBytes;     // [stage][K | V][chunk][128 keys][128 B]
   __shared__ uint64_t kv_full[kTcStages], kv_empty[kTcStages];
-  // S, P and the P.V commit are double-buffered by page parity: a page's
-  // softmax writes its P while the previous page's P.V is still running
-  __shared__ uint64_t s_full[NT][2], p_full[NT][2], o_full[NT][2];
+  __shared__ uint64_t s_full[NT], p_full[NT], o_full[NT];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
   const int n_tiles = (nt * G + kRows - 1) / kRows;       // Q tiles with rows (1 or 2)
   const int last_pos = tile.pos0 + t0 + nt - 1;
   const int npages = last_pos / kPageTokens + 1;
+  const int nblk = (npages + 1) / 2;                      // 128-key blocks
   const int* pt = page_table + static_cast<size_t>(tile.slot) * pt_stride;
   const int mma_warp = NT * 4;
 
@@ -180,11 +185,9 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
       mbar_init(&kv_empty[s], 1);
     }
     for (int t = 0; t < NT; ++t) {
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&s_full[t][b], 1);
-        mbar_init(&p_full[t][b], kTcSoftmaxThreads);
-        mbar_init(&o_full[t][b], 1);
-      }
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], kTcSoftmaxThreads);
+      mbar_init(&o_full[t], 1);
     }
     fence_mbar_init();
   }
@@ -218,112 +221,108 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
 
   if (warp == mma_warp) {
     if (lane == 0) {
-      auto issue = [&](int i) {
-        const int s = i % kTcStages;
-        const int phys = pt[i];
+      // key block j = pages 2j and 2j+1 (an odd tail repeats its last page:
+      // those keys are masked, the data only has to be finite)
+      auto issue = [&](int j) {
+        const int s = j % kTcStages;
         uint8_t* dst = sKV + s * kStageBytes;
         mbar_expect_tx(&kv_full[s], kStageBytes);
-        const int rk = static_cast<int>(kv_row(geom, layer, phys, 0, kvh));
-        const int rv = static_cast<int>(kv_row(geom, layer, phys, 1, kvh));
 #pragma unroll
-        for (int b = 0; b < HD / 64; ++b) {
-          tma_load_2d(dst + b * kBox, &kv_map, &kv_full[s], b * 64, rk);
-          tma_load_2d(dst + kKvBytes + b * kBox, &kv_map, &kv_full[s], b * 64, rv);
+        for (int h = 0; h < 2; ++h) {
+          const int phys = pt[min(2 * j + h, npages - 1)];
+          const int rk = static_cast<int>(kv_row(geom, layer, phys, 0, kvh));
+          const int rv = static_cast<int>(kv_row(geom, layer, phys, 1, kvh));
+#pragma unroll
+          for (int b = 0; b < HD / 64; ++b) {
+            tma_load_2d(dst + b * kChunk + h * kBox, &kv_map, &kv_full[s], b * 64, rk);
+            tma_load_2d(dst + kKvBytes + b * kChunk + h * kBox, &kv_map, &kv_full[s], b * 64, rv);
+          }
         }
       };
-      for (int i = 0; i < min(kTcStages, npages); ++i) issue(i);
-      const uint32_t id_s = umma_idesc_bf16(kRows, kPageTokens);
+      for (int j = 0; j < min(kTcStages, nblk); ++j) issue(j);
+      const uint32_t id_s = umma_idesc_bf16(kRows, kBlkKeys);
       const uint32_t id_o = umma_idesc_bf16(kRows, HD) | (1u << 16);  // B (V) MN-major
-      auto mma_s = [&](int i) {  // S_i = Q K_i^T of every tile into S buffer i & 1
-        const int s = i % kTcStages;
-        mbar_wait(&kv_full[s], (i / kTcStages) & 1);
+      // S_j = Q_t K_j^T (M=128, N=128 keys) into tile t's S columns; the
+      // previous block's P.V (reading P from those columns) was issued first
+      auto mma_s = [&](int j, int t) {
+        const int s = j % kTcStages;
+        mbar_wait(&kv_full[s], (j / kTcStages) & 1);
         tc_fence_after();
         const uint32_t k_base = smem_u32(sKV + s * kStageBytes);
-        for (int t = 0; t < n_tiles; ++t) {
-          const uint32_t q_base = smem_u32(sQ + t * kQBytes);
+        const uint32_t q_base = smem_u32(sQ + t * kQBytes);
 #pragma unroll
-          for (int j = 0; j < kKSteps; ++j) {
-            const uint32_t off_a = (j >> 2) * (kRows * 128) + (j & 3) * 32;
-            const uint32_t off_b = (j >> 2) * kBox + (j & 3) * 32;
-            umma_bf16(tmem + s_col<NT>(i & 1, t), umma_desc_k128(q_base + off_a),
-                      umma_desc_k128(k_base + off_b), id_s, j > 0);
-          }
-          umma_commit(&s_full[t][i & 1]);
+        for (int kk = 0; kk < kKSteps; ++kk) {
+          const uint32_t off_a = (kk >> 2) * (kRows * 128) + (kk & 3) * 32;
+          const uint32_t off_b = (kk >> 2) * kChunk + (kk & 3) * 32;
+          umma_bf16(tmem + s_col<NT>(t), umma_desc_k128(q_base + off_a),
+                    umma_desc_k128(k_base + off_b), id_s, kk > 0);
         }
+        umma_commit(&s_full[t]);
       };
-      mma_s(0);
-      if (npages > 1) mma_s(1);
-      for (int i = 0; i < npages; ++i) {
-        const int s = i % kTcStages;
+      for (int t = 0; t < n_tiles; ++t) mma_s(0, t);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kTcStages;
         const uint32_t v_base = smem_u32(sKV + s * kStageBytes + kKvBytes);
         for (int t = 0; t < n_tiles; ++t) {
-          // P_i in smem, S_i read out, O rescaled if needed
-          mbar_wait(&p_full[t][i & 1], (i >> 1) & 1);
+          mbar_wait(&p_full[t], j & 1);  // P_j in TMEM, O rescaled if needed
           tc_fence_after();
-          K6T(2 + t, i);
-          // P_i sits in the first 32 columns of its S buffer (bf16 pairs)
-          const uint32_t p_tmem = tmem + s_col<NT>(i & 1, t);
+          K6T(2 + t, j);
+          const uint32_t p_tmem = tmem + s_col<NT>(t);  // P_j: bf16 pairs, 64 columns
 #pragma unroll
-          for (int j = 0; j < kPageTokens / 16; ++j)  // O += P_i V_i (16 keys per step)
-            umma_bf16_ts(tmem + o_col<NT>(t), p_tmem + j * 8,
-                         umma_desc_mn128(v_base + j * 2048, kBox), id_o, (i | j) != 0);
-          umma_commit(&o_full[t][i & 1]);
+          for (int kk = 0; kk < kBlkKeys / 16; ++kk)  // O += P_j V_j (16 keys per step)
+            umma_bf16_ts(tmem + o_col<NT>(t), p_tmem + kk * 8,
+                         umma_desc_mn128(v_base + kk * 2048, kChunk), id_o, (j | kk) != 0);
+          if (j + 1 == nblk) umma_commit(&o_full[t]);
+          if (t == n_tiles - 1) umma_commit(&kv_empty[s]);  // after every P_j V_j
+          // this tile's next S (the other tile's softmax runs meanwhile)
+          if (j + 1 < nblk) mma_s(j + 1, t);
         }
-        umma_commit(&kv_empty[s]);
-        K6T(4, i);
-        // S_{i+2} first (its S buffer was read out, p_full_i; its page is
-        // resident), then the refill of page i's stage, which has to wait
-        // for P_i V_i to finish
-        if (i + 2 < npages) mma_s(i + 2);
-        K6T(5, i);
-        if (i + kTcStages < npages) {
-          mbar_wait(&kv_empty[s], (i / kTcStages) & 1);  // K_i, V_i consumed
-          issue(i + kTcStages);
+        K6T(4, j);
+        if (j + kTcStages < nblk) {
+          mbar_wait(&kv_empty[s], (j / kTcStages) & 1);  // K_j, V_j consumed
+          issue(j + kTcStages);
         }
-        K6T(6, i);
+        K6T(6, j);
       }
     }
   } else if (qt < n_tiles) {
     // softmax: thread = TMEM lane = MMA row of tile qt
     const uint32_t t_row = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     float m = -CUDART_INF_F, l = 0.f;
-    for (int i = 0; i < npages; ++i) {
-      mbar_wait(&s_full[qt][i & 1], (i >> 1) & 1);
+    for (int j = 0; j < nblk; ++j) {
+      // S_j done implies the previous P.V is done too (MMAs complete in order)
+      mbar_wait(&s_full[qt], j & 1);
       tc_fence_after();
-      if (threadIdx.x == 0) K6T(0, i);
-      float sv[kPageTokens];
+      if (threadIdx.x == 0) K6T(0, j);
+      float sv[kBlkKeys];
       {
-        uint32_t rr[4][16];
+        uint32_t rr[8][16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld16_nw(t_row + s_col<NT>(i & 1, qt) + c * 16, rr[c]);
+        for (int c = 0; c < 8; ++c) tmem_ld16_nw(t_row + s_col<NT>(qt) + c * 16, rr[c]);
         tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 8; ++c)
 #pragma unroll
           for (int e = 0; e < 16; ++e) sv[c * 16 + e] = __uint_as_float(rr[c][e]);
       }
-      const int kbase = i * kPageTokens;
-      if (!(valid && kbase + kPageTokens - 1 <= pos)) {  // diagonal page / padding row
+      const int kbase = j * kBlkKeys;
+      if (!(valid && kbase + kBlkKeys - 1 <= pos)) {  // diagonal block / padding row
 #pragma unroll
-        for (int j = 0; j < kPageTokens; ++j)
-          if (!(valid && kbase + j <= pos)) sv[j] = -CUDART_INF_F;
+        for (int k = 0; k < kBlkKeys; ++k)
+          if (!(valid && kbase + k <= pos)) sv[k] = -CUDART_INF_F;
       }
       // row max of the raw scores (the scale is positive: it commutes)
       float mx4[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
 #pragma unroll
-      for (int j = 0; j < kPageTokens; ++j) mx4[j & 3] = fmaxf(mx4[j & 3], sv[j]);
+      for (int k = 0; k < kBlkKeys; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], sv[k]);
       const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
       // lazy rescale: move m only when the row max outgrows it by 2^8
       const bool grow = mx > m + kRescaleLog2;
       const float m_new = grow ? mx : m;
-      const float alpha = grow ? exp2f(m - m_new) : 1.f;  // 0 on the first page
+      const float alpha = grow ? exp2f(m - m_new) : 1.f;  // 0 on the first block
       m = m_new;
       const float mu = m == -CUDART_INF_F ? 0.f : m;
-      // O is rescaled only once the previous page's P.V is done; this
-      // page's P buffer is free once the P.V of page i - 2 is done
-      if (i > 0 && __any_sync(0xffffffffu, grow)) {  // O *= alpha (warp-collective)
-        mbar_wait(&o_full[qt][(i - 1) & 1], ((i - 1) >> 1) & 1);
-        tc_fence_after();
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {  // O *= alpha (warp-collective)
 #pragma unroll
         for (int c = 0; c < HD / 16; ++c) {
           uint32_t rr[16];
@@ -333,33 +332,32 @@ __global__ void __launch_bounds__(NT * kTcSoftmaxThreads + 32, 1)
           for (int e = 0; e < 16; ++e) rr[e] = __float_as_uint(__uint_as_float(rr[e]) * alpha);
           tmem_st16(t_row + o_col<NT>(qt) + c * 16, rr);
         }
-        tmem_wait_st();
       }
-      // P_i -> the first 32 columns of S buffer i & 1 (this thread's lane),
-      // the A operand of P_i V_i.  The buffer's previous P (page i - 2) was
-      // consumed before S_i was written there (the MMAs run in issue order).
+      // P_j = 2^(s * scale - m) as bf16 pairs into the first 64 S columns:
+      // one FFMA and one MUFU.EX2 per score, the row sum over the fp32 P
       const float nmu = -mu;
       float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t pw[2][16];
 #pragma unroll
-      for (int j = 0; j < kPageTokens / 2; ++j) {
-        const float a = ex2_ftz(fmaf(sv[2 * j], scale_log2, nmu));
-        const float b = ex2_ftz(fmaf(sv[2 * j + 1], scale_log2, nmu));
-        rs4[j & 3] += a + b;
-        pw[j >> 4][j & 15] = pack_bf16x2(a, b);
+      for (int c = 0; c < kBlkKeys / 32; ++c) {
+        uint32_t pw[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float a = ex2_ftz(fmaf(sv[c * 32 + 2 * e], scale_log2, nmu));
+          const float b = ex2_ftz(fmaf(sv[c * 32 + 2 * e + 1], scale_log2, nmu));
+          rs4[e & 3] += a + b;
+          pw[e] = pack_bf16x2(a, b);
+        }
+        tmem_st16(t_row + s_col<NT>(qt) + c * 16, pw);
       }
-      tmem_st16(t_row + s_col<NT>(i & 1, qt), pw[0]);
-      tmem_st16(t_row + s_col<NT>(i & 1, qt) + 16, pw[1]);
       tmem_wait_st();
       const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
       l = l * alpha + rs;
       tc_fence_before();
-      if (threadIdx.x == 0) K6T(1, i);
-      if (threadIdx.x == kRows) K6T(7, i);
-      mbar_arrive(&p_full[qt][i & 1]);
+      if (threadIdx.x == 0) K6T(1, j);
+      if (threadIdx.x == kRows) K6T(7, j);
+      mbar_arrive(&p_full[qt]);
     }
-    // MMAs complete in issue order: the last page's commit covers them all
-    mbar_wait(&o_full[qt][(npages - 1) & 1], ((npages - 1) >> 1) & 1);
+    mbar_wait(&o_full[qt], 0);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     bf16* dst = out + static_cast<size_t>(tile.q_row + t0 + tok) * out_row_stride +
@@ -398,7 +396,7 @@ int launch_tc_nt(const CUtensorMap& kv_map, const KvGeom& g, int layer, const bf
                  const PrefillTile* tiles, int n_tiles, bf16* out, int out_row_stride,
                  cudaStream_t st) {
   constexpr int kSmem = NT * (HD / 64) * kRows * 128 +
-                        kTcStages * 2 * (HD / 64) * kPageTokens * 128 + 1024;
+                        kTcStages * 2 * (HD / 64) * kBlkKeys * 128 + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(prefill_attn_tc_kernel<HD, NT>,
