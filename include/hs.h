@@ -294,6 +294,35 @@ int hs_swap_out_async(hs_ctx* ctx, int slot, int tokens, int* ticket);
 int hs_swap_in_async(hs_ctx* ctx, int slot, int tokens, int* ticket);
 /* 1 = done, 0 = in flight */
 int hs_swap_done(hs_ctx* ctx, int ticket);
+
+/* ------------------------------------------------------- remote CPU hosts
+ * The reference's cluster has `cpu_hosts` CPU hosts: host 0 is the GPU's
+ * own (PCIe), hosts 1.. are remote (network link, engine.py:329-331); a
+ * request is offloaded to the local host while its memory lasts, else to
+ * the least loaded remote host (_distribute_offload, engine.py:402-419),
+ * and its work items are serviced there (engine.py:529-560).
+ *
+ * hs_cpu_host_serve runs a remote host: a blocking TCP server that owns the
+ * KV of the requests placed on it and runs the host attention kernel for
+ * every client replica (one slot namespace per connection).  It prints
+ * "HS_CPU_HOST_READY port=<p>" once listening (port 0: any free port) and
+ * returns after a client's shutdown request.  No GPU is needed.
+ *
+ * A replica connects each remote host id once (hs_cpu_host_connect) and
+ * places a slot's KV on it after the swap-out landed in the slot's host
+ * region (hs_cpu_place(slot, host, ctx tokens): the context is streamed to
+ * the remote host, and from then on the slot's work items -- hs_cpu_attend
+ * and hs_cpu_submit alike, device-polled ones included -- are relayed there
+ * in FIFO order and their results written into the slot's result mailbox
+ * with the same completion tag as a local item).  hs_cpu_place(slot, 0,
+ * tokens) fetches the KV back into the region (before a swap-in); releasing
+ * the region frees the remote copy.  bf16 datapath only. */
+int hs_cpu_host_serve(const hs_model_cfg* model, const char* bind_addr, int port, int threads,
+                      int max_slots);
+int hs_cpu_host_connect(hs_ctx* ctx, int host, const char* addr, int port);
+int hs_cpu_place(hs_ctx* ctx, int slot, int host, int tokens);
+/* [4]: work items relayed, KV bytes placed, KV bytes fetched back, result bytes */
+int hs_cpu_remote_stats(hs_ctx* ctx, int host, int64_t* stats);
 /* Pipelined iterations: hs_iter_end_async queues the token readback and an
  * event and returns at once (the host plans the next iteration while this
  * one runs); hs_iter_poll returns 1 with the tokens and the completion time

@@ -46,6 +46,8 @@ _SIGNATURES: dict[str, list] = {
     "hs_op_argmax": [_fp, _i, _i, _i, _ip, _fp, _vp],
     "hs_op_lse_merge": [_vp, _fp, _i, _i, _i, _i, _i, _i, _vp, _i, _vp],
     "hs_host_attention": [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _fp, _i],
+    # a remote CPU host process (cpu_host.py): model cfg, bind address, port, threads, max slots
+    "hs_cpu_host_serve": [_vp, C.c_char_p, _i, _i, _i],
 }
 
 _lib = None

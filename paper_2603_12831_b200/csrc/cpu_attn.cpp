@@ -51,6 +51,10 @@ void ThreadPool::loop(int) {
       cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
       if (stop_) return;
       seen = gen_;
+      // a call the caller finished alone before this worker woke: body_ is
+      // already cleared (the caller clears it under the lock before it
+      // returns).  Joining it would race the next call's reset of next_.
+      if (!body_) continue;
       body = body_;
       n = n_;
       ++active_;

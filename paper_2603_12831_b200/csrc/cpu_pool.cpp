@@ -65,6 +65,11 @@ class CpuService {
   std::function<void(int slot, int ctx, int layer)> publish;
   std::function<void(int slot)> retract;  // the slot's previous completion tag is void
   std::function<int(int slot)> host_cap;
+  // remote CPU hosts (cpu_remote.cpp): hands the item to the relay of the
+  // slot's remote host and returns true, or returns false for a local slot.
+  // `done` completes the item from the relay's receiver thread.
+  std::function<bool(int slot, int layer, int ctx, cudaEvent_t ev, std::function<void()> done)>
+      route;
 
   int submit(cudaStream_t st, const int* slots, const int* layers, const int* ctxs, int n) {
     if (n <= 0) return HS_OK;
@@ -93,11 +98,12 @@ class CpuService {
     {
       std::lock_guard<std::mutex> g(mu_);
       for (int i = 0; i < n; ++i) {
+        in_flight_ += 1;
+        if (to_remote(slots[i], layers[i], ctxs[i], ev)) continue;
         const int idx = static_cast<int>(items_.size());
         items_.push_back(CpuItem{slots[i], layers[i], ctxs[i], ev, m_.n_kv, now});
         for (int h = 0; h < m_.n_kv; ++h) tasks_.push_back(CpuTask{idx, h});
       }
-      in_flight_ += n;
     }
     cv_.notify_all();
     return HS_OK;
@@ -143,6 +149,18 @@ class CpuService {
   }
 
  private:
+  // called with mu_ held; the relay's completion takes mu_ from its own thread
+  bool to_remote(int slot, int layer, int ctx, int ev) {
+    if (!route) return false;
+    return route(slot, layer, ctx, ev >= 0 ? events_[ev] : nullptr, [this, slot, layer, ctx, ev] {
+      std::lock_guard<std::mutex> g(mu_);
+      publish(slot, ctx, layer);
+      done_.emplace_back(slot, layer, wall());
+      if (ev >= 0) --ev_refs_[ev];
+      --in_flight_;
+    });
+  }
+
   void dispatch() {
     int idle = 0;
     for (;;) {
@@ -165,10 +183,11 @@ class CpuService {
         std::lock_guard<std::mutex> g(mu_);
         for (int i = ring_next_; i != tail; ++i) {
           const int* e = ring_ + static_cast<size_t>(i % ring_q_) * 4;
+          ++in_flight_;
+          if (to_remote(e[0], e[1], e[2], -1)) continue;
           const int idx = static_cast<int>(items_.size());
           items_.push_back(CpuItem{e[0], e[1], e[2], -1, m_.n_kv, now});
           for (int h = 0; h < m_.n_kv; ++h) tasks_.push_back(CpuTask{idx, h});
-          ++in_flight_;
         }
       }
       ring_next_ = tail;
@@ -249,6 +268,11 @@ void cpu_service_bind(CpuService* s, std::function<bf16*(int)> ship, std::functi
   s->host_cap = std::move(cap);
   s->publish = std::move(publish);
   s->retract = std::move(retract);
+}
+void cpu_service_route(
+    CpuService* s,
+    std::function<bool(int, int, int, cudaEvent_t, std::function<void()>)> route) {
+  s->route = std::move(route);
 }
 int cpu_service_submit(CpuService* s, cudaStream_t st, const int* slots, const int* layers,
                        const int* ctxs, int n) {

@@ -2,7 +2,9 @@
 // (step.cu) and the fp32 validation datapath (step_f32.cu).
 #pragma once
 
+#include <atomic>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -158,6 +160,10 @@ struct hs_ctx {
   ThreadPool* pool = nullptr;
   std::vector<int> cpus;  // the replica's CPU-attention core set (empty: unpinned)
   CpuService* cpu = nullptr;
+  // remote CPU hosts (cpu_remote.cpp): relay per host id (index 0 = this
+  // replica's own host, unused) and the host each slot's KV lives on
+  std::vector<RemoteHost*> remotes;
+  std::unique_ptr<std::atomic<int>[]> slot_host;
   // swaps: copy stream + contiguous staging for pack/unpack around one 2D DMA
   cudaStream_t copy_st = nullptr;
   bf16* swap_stage = nullptr;

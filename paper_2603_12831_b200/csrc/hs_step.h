@@ -84,6 +84,23 @@ int cpu_service_poll(CpuService* s, int* slots, int* layers, double* t_done, int
 // publishes into (mapped host memory: [Q][4] slot, layer, ctx, seq + tail)
 void cpu_service_attach_ring(CpuService* s, const int* ring, const int* tail, int Q);
 int cpu_service_in_flight(CpuService* s);
+void cpu_service_route(
+    CpuService* s,
+    std::function<bool(int, int, int, cudaEvent_t, std::function<void()>)> route);
+
+// remote CPU hosts (cpu_remote.cpp): one TCP relay per remote host; every
+// op is sent in FIFO order by the relay's sender thread
+class RemoteHost;
+RemoteHost* remote_connect(const ModelCfg& m, const char* addr, int port);
+void remote_destroy(RemoteHost* r);
+// the slot's context (first ctx tokens of a [layers][2][n_kv][cap][hd] region) moves to the host
+void remote_put(RemoteHost* r, int slot, int ctx, const bf16* region, int cap);
+void remote_attend(RemoteHost* r, int slot, int layer, int ctx, cudaEvent_t ev, const bf16* ship,
+                   bf16* result, std::function<void()> before_send, std::function<void()> done);
+void remote_get(RemoteHost* r, int slot, int ctx, bf16* region, int cap);
+void remote_free(RemoteHost* r, int slot);
+bool remote_quiesce(RemoteHost* r);  // false once the connection failed
+const int64_t* remote_stats(RemoteHost* r);
 double cpu_service_busy(CpuService* s);
 double wall_seconds();
 

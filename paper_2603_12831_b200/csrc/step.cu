@@ -382,6 +382,10 @@ int build_maps(hs_ctx* c) {
 void free_all(hs_ctx* c) {
   // stop and join the CPU-attention workers first: an in-flight work item
   // reads the ship mailbox and host KV and writes the result mailbox / tags
+  // the remote relays complete items into the CPU service: stop them first
+  for (auto* r : c->remotes)
+    if (r) remote_destroy(r);
+  c->remotes.clear();
   if (c->cpu) destroy_cpu_service(c->cpu);
   c->cpu = nullptr;
   pg_free(c);
@@ -687,6 +691,11 @@ int check_device_faults(hs_ctx* c) {
                    "(completion tag 0x%x)", slot, layer, seen);
 }
 
+// the CPU host a slot's KV lives on (0 = this replica's own host)
+int slot_host_of(hs_ctx* c, int slot) {
+  return c->slot_host ? c->slot_host[slot].load(std::memory_order_acquire) : 0;
+}
+
 int ensure_cpu_service(hs_ctx* c) {
   if (c->cpu) return HS_OK;
   if (c->r.cpu_threads <= 0) return set_error(HS_E_CONFIG, "no CPU attention threads configured");
@@ -696,6 +705,14 @@ int ensure_cpu_service(hs_ctx* c) {
       [c](int s) { return host_region(c, s); }, [c](int s) { return c->regions[s].cap; },
       [c](int s, int ctx, int layer) { publish_tag(c, s, ctx, layer); },
       [c](int s) { retract_tag(c, s); });
+  cpu_service_route(c->cpu, [c](int s, int layer, int ctx, cudaEvent_t ev,
+                                std::function<void()> done) {
+    const int h = slot_host_of(c, s);
+    if (h <= 0) return false;
+    remote_attend(c->remotes[h], s, layer, ctx, ev, ship_row(c, s), result_row(c, s),
+                  [c, s] { retract_tag(c, s); }, std::move(done));
+    return true;
+  });
   return HS_OK;
 }
 
@@ -1003,6 +1020,13 @@ int hs_host_kv_release(hs_ctx* c, int slot) {
   if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
   HostRegion& hr = c->regions[slot];
   if (!hr.used) return HS_OK;
+  if (const int h = slot_host_of(c, slot); h > 0) {
+    // the relay may still read the region (a queued PUT): drain it first
+    remote_free(c->remotes[h], slot);
+    c->slot_host[slot].store(0, std::memory_order_release);
+    if (!remote_quiesce(c->remotes[h]))
+      return set_error(HS_E_CUDA, "remote CPU host %d: connection failed", h);
+  }
   // the slot's last completion tag stands for nothing any more: a later
   // occupant's item with the same (ctx, layer) must not read as complete
   retract_tag(c, slot);
@@ -1500,12 +1524,30 @@ int hs_cpu_attend(hs_ctx* c, const int* slots, const int* layers, const int* ctx
       return set_error(HS_E_CONFIG, "work item ctx %d outside [0, max_pos)", ctxs[i]);
   }
   for (int i = 0; i < n; ++i) retract_tag(c, slots[i]);
-  c->pool->parallel_for(n * m.n_kv, [&](int task) {
-    const int i = task / m.n_kv, h = task % m.n_kv;
+  // items of slots placed on remote hosts go to their relays first and are
+  // serviced there while the local pool runs
+  std::vector<int> local;
+  std::vector<char> used_host(c->remotes.size(), 0);
+  for (int i = 0; i < n; ++i) {
+    const int h = slot_host_of(c, slots[i]);
+    if (h <= 0) {
+      local.push_back(i);
+      continue;
+    }
+    used_host[h] = 1;
+    remote_attend(c->remotes[h], slots[i], layers[i], ctxs[i], nullptr, ship_row(c, slots[i]),
+                  result_row(c, slots[i]), nullptr, nullptr);
+  }
+  const int nl = static_cast<int>(local.size());
+  c->pool->parallel_for(nl * m.n_kv, [&](int task) {
+    const int i = local[task / m.n_kv], h = task % m.n_kv;
     const int s = slots[i];
     cpu_attend_head(m, ship_row(c, s), host_region(c, s), c->regions[s].cap, layers[i] - 1,
                     ctxs[i], h, result_row(c, s), nullptr);
   });
+  for (size_t h = 1; h < used_host.size(); ++h)
+    if (used_host[h] && !remote_quiesce(c->remotes[h]))
+      return set_error(HS_E_CUDA, "remote CPU host %zu: connection failed", h);
   for (int i = 0; i < n; ++i) publish_tag(c, slots[i], ctxs[i], layers[i]);
   return HS_OK;
 }
@@ -1796,6 +1838,52 @@ int hs_cpu_in_flight(hs_ctx* c) { return c->cpu ? cpu_service_in_flight(c->cpu) 
 double hs_cpu_busy_seconds(hs_ctx* c) { return c->cpu ? cpu_service_busy(c->cpu) : 0.0; }
 
 double hs_wall_seconds(void) { return wall_seconds(); }
+
+int hs_cpu_host_connect(hs_ctx* c, int host, const char* addr, int port) {
+  if (host < 1 || host > 4096 || !addr) return set_error(HS_E_CONFIG, "remote host id %d", host);
+  if (static_cast<int>(c->remotes.size()) <= host) c->remotes.resize(host + 1, nullptr);
+  if (c->remotes[host]) return set_error(HS_E_CONFIG, "remote host %d already connected", host);
+  if (!c->slot_host) {
+    c->slot_host.reset(new std::atomic<int>[c->r.max_slots]);
+    for (int s = 0; s < c->r.max_slots; ++s) c->slot_host[s].store(0);
+  }
+  RC(ensure_cpu_service(c));
+  RemoteHost* r = remote_connect(c->m, addr, port);
+  if (!r) return HS_E_CONFIG;  // remote_connect set the message
+  c->remotes[host] = r;
+  return HS_OK;
+}
+
+int hs_cpu_place(hs_ctx* c, int slot, int host, int tokens) {
+  if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
+  if (host < 0 || (host > 0 && (host >= static_cast<int>(c->remotes.size()) || !c->remotes[host])))
+    return set_error(HS_E_CONFIG, "CPU host %d is not connected to this replica", host);
+  HostRegion& hr = c->regions[slot];
+  if (!hr.used) return set_error(HS_E_INTEGRITY, "slot %d has no host KV region", slot);
+  if (tokens < 0 || tokens > hr.cap)
+    return set_error(HS_E_CAPACITY, "placement of %d tokens exceeds the region", tokens);
+  const int cur = slot_host_of(c, slot);
+  if (cur == host) return HS_OK;
+  if (cur > 0) {  // back from a remote host: its KV (with every appended token) into the region
+    remote_get(c->remotes[cur], slot, tokens, host_region(c, slot), hr.cap);
+    remote_free(c->remotes[cur], slot);
+    c->slot_host[slot].store(0, std::memory_order_release);
+    if (!remote_quiesce(c->remotes[cur]))
+      return set_error(HS_E_CUDA, "remote CPU host %d: connection failed", cur);
+  }
+  if (host > 0) {
+    remote_put(c->remotes[host], slot, tokens, host_region(c, slot), hr.cap);
+    c->slot_host[slot].store(host, std::memory_order_release);
+  }
+  return HS_OK;
+}
+
+int hs_cpu_remote_stats(hs_ctx* c, int host, int64_t* out) {
+  if (host < 1 || host >= static_cast<int>(c->remotes.size()) || !c->remotes[host])
+    return set_error(HS_E_CONFIG, "CPU host %d is not connected", host);
+  std::memcpy(out, remote_stats(c->remotes[host]), 4 * sizeof(int64_t));
+  return HS_OK;
+}
 
 int hs_sync(hs_ctx* c) {
   CK(cudaStreamSynchronize(c->st));

@@ -244,8 +244,8 @@ class Engine(PlannerMixin):
 
     def _finish_swap_out(self, req: SimRequest) -> None:
         host = req.swap_dest
+        self.step.swap_out_done(req)  # copies the pages to host `swap_dest`, then frees them
         req.swap_dest = None
-        self.step.swap_out_done(req)  # copies the pages to the host, then frees them
         self.kv.free_gpu(req.kv_held)
         req.kv_place = host
         req.swap_state = "none"

@@ -122,6 +122,10 @@ _CTX_SIGS = {
     "hs_pg_iter": [C.c_void_p, C.c_int, _IP, C.c_int],
     "hs_pg_log": [C.c_void_p, C.c_int, _IP, C.c_int],
     "hs_pg_share_tags": [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int],
+    # remote CPU hosts (cpu_host.py)
+    "hs_cpu_host_connect": [C.c_void_p, C.c_int, C.c_char_p, C.c_int],
+    "hs_cpu_place": [C.c_void_p, C.c_int, C.c_int, C.c_int],
+    "hs_cpu_remote_stats": [C.c_void_p, C.c_int, C.POINTER(C.c_int64)],
 }
 _NONNEG_RETURNS = {"hs_iter_end", "hs_cpu_poll", "hs_cpu_in_flight", "hs_swap_done", "hs_mark",
                    "hs_timer", "hs_iter_poll", "hs_iter_ntokens", "hs_pg_log"}
@@ -151,6 +155,9 @@ class RuntimeConfig:
     # "bf16" serving datapath, or "fp32" validation datapath (fp32 weights,
     # activations, KV, piggyback mailboxes and host attention; SIMT kernels)
     precision: str = "bf16"
+    # remote CPU hosts 1..n of the scenario's cluster: (addr, port) of each
+    # running `cpu_host` server, connected at context creation
+    remote_hosts: tuple = ()
 
 
 class HsContext:
@@ -193,6 +200,9 @@ class HsContext:
         _lib.check(lib.hs_create(C.byref(mc), C.byref(rc), C.byref(h)), "hs_create")
         self.h = h
         self._tok = np.zeros(2 * rt.max_rows, np.int32)
+        self.remote_host_ids: set[int] = set()
+        for i, (addr, port) in enumerate(getattr(rt, "remote_hosts", ()) or (), start=1):
+            self.cpu_host_connect(i, addr, port)
 
     def close(self) -> None:
         if self.h:
@@ -298,6 +308,20 @@ class HsContext:
         l = np.zeros(max_items, np.int32)
         n = self._call("hs_cpu_poll", _ip(s), _ip(l), None, max_items)
         return s[:n], l[:n]
+
+    def cpu_host_connect(self, host: int, addr: str, port: int) -> None:
+        self._call("hs_cpu_host_connect", host, addr.encode(), int(port))
+        self.remote_host_ids.add(host)
+
+    def cpu_place(self, slot: int, host: int, tokens: int) -> None:
+        """Moves the slot's host KV (its first `tokens` tokens) to CPU host
+        `host` (0 = this replica's own host)."""
+        self._call("hs_cpu_place", slot, host, tokens)
+
+    def remote_stats(self, host: int) -> dict:
+        out = (C.c_int64 * 4)()
+        self._call("hs_cpu_remote_stats", host, out)
+        return dict(zip(("items", "put_bytes", "get_bytes", "result_bytes"), list(out)))
 
     def cpu_busy_seconds(self) -> float:
         return self.lib.hs_cpu_busy_seconds(self.h)
@@ -487,6 +511,8 @@ class CudaStep(LayerStep):
         self.iterations = 0
         self._pending_release: list[str] = []
         self._tags: dict[str, int] = {}  # completion tag of each request's outstanding result
+        self.remote_slots: dict[int, int] = {}  # slot -> remote CPU host holding its KV
+        self.remote_colocated = 0  # offloads to a remote host id with no server connected
         # host<->device bytes moved by the step (metadata, tokens, piggyback rows)
         self.h2d_bytes = 0
         self.d2h_bytes = 0
@@ -633,11 +659,36 @@ class CudaStep(LayerStep):
         self.ctx.swap_out(s, req.kv_held)
         self.pages.release(s)
         self._dirty.add(s)
+        self._place(req, s, req.kv_held)
+
+    def _place(self, req, slot: int, tokens: int) -> None:
+        """The engine offloaded `req` to CPU host `req.swap_dest`
+        (_distribute_offload, reference engine.py:402-419): a remote host
+        (>= 1) receives the context that just landed in the slot's host
+        region and services the request's work items from now on."""
+        # the hook runs inside _finish_swap_out before kv_place takes the host
+        dest = getattr(req, "swap_dest", None)
+        host = dest if isinstance(dest, int) else (
+            req.kv_place if isinstance(req.kv_place, int) else 0)
+        if host <= 0:
+            return
+        if host in getattr(self.ctx, "remote_host_ids", ()):
+            self.ctx.cpu_place(slot, host, tokens)
+            self.remote_slots[slot] = host
+        else:  # no server runs for that host: it is co-located with host 0
+            self.remote_colocated += 1
+
+    def _unplace(self, slot: int, tokens: int) -> None:
+        """Swap-in from a remote host: its KV comes back into the slot's
+        host region first."""
+        if self.remote_slots.pop(slot, 0):
+            self.ctx.cpu_place(slot, 0, tokens)
 
     def resumed_on_gpu(self, req) -> None:
         s = self.slot_of(req.id)
         self._ensure(s, req.ctx)
         self._flush_pages()
+        self._unplace(s, req.ctx)
         self.ctx.swap_in(s, req.ctx)
         self.ctx.host_kv_release(s)
 
@@ -659,6 +710,7 @@ class CudaStep(LayerStep):
             if s is None:
                 continue
             self.pages.release(s)
+            self.remote_slots.pop(s, None)
             self.ctx.host_kv_release(s)
             self._dirty.discard(s)
             self.free_slots.append(s)
@@ -767,6 +819,7 @@ class LiveCudaStep(CudaStep):
             self._dirty.add(s)
         self._flush_pages()
         self.slots.clear()
+        self.remote_slots.clear()
         self.free_slots = list(range(self.rt.max_slots - 1, -1, -1))
         for d in (self.generated, self.prompts, self._tags):
             d.clear()
@@ -853,6 +906,7 @@ class LiveCudaStep(CudaStep):
         s = self.slot_of(req.id)
         self._ensure(s, req.ctx)
         self._flush_pages()
+        self._unplace(s, req.ctx)
         return self.ctx.swap_async(s, req.ctx, out=False)
 
     def swap_done(self, ticket: int) -> bool:
@@ -862,9 +916,12 @@ class LiveCudaStep(CudaStep):
         s = self.slot_of(req.id)
         self.pages.release(s)
         self._dirty.add(s)
+        self._place(req, s, req.kv_held)
 
     def resumed_on_gpu(self, req) -> None:
-        self.ctx.host_kv_release(self.slot_of(req.id))
+        s = self.slot_of(req.id)
+        self.remote_slots.pop(s, None)
+        self.ctx.host_kv_release(s)
 
     def cpu_service(self, host_id: int, items) -> None:
         raise AssertionError("live mode submits work items asynchronously")
