@@ -125,7 +125,8 @@ def scenario_doc(args, cores: int, ls_rate: float = None) -> dict:
         "model": "34B", "policy": "omniserve", "horizon_s": 3600.0, "seed": args.seed,
         "transformer": args.config,
         "profiles": {"cluster": {
-            "layers": get_transformer(args.config).n_layers, "gpu_count": 1, "tp_degree": 1, "cpu_hosts": 1,
+            "layers": get_transformer(args.config).n_layers, "gpu_count": 1, "tp_degree": 1,
+            "cpu_hosts": 1 + getattr(args, "remote_hosts", 0),
             "gpu_kv_capacity": args.gpu_kv_tokens, "cpu_mem_tokens": 10_000_000,
             "cpu_cores_per_host": cores, "max_piggyback_per_layer": args.max_piggyback,
             "merge_cost_per_result": 0.5}},
@@ -180,13 +181,20 @@ def prepopulate_be(engine, step, n: int, seed: int, start: int = 0, fixed=None) 
         r.token_times = [engine.now]
         r.first_token_time = engine.now
         need = r.prompt_len + r.output_len - r.tokens_out + 1
-        engine.kv.alloc_host(0, need)
+        # --remote-hosts N: the backlog is spread evenly over the local host
+        # and the N remote hosts (as if the local host's memory held 1/(N+1)
+        # of it; _distribute_offload, reference engine.py:402-419)
+        host = i % engine.cluster.cpu_hosts
+        engine.kv.alloc_host(host, need)
         r.swap_reserved = need
-        r.kv_place = 0
+        r.kv_place = host
         r.kv_held = r.ctx
-        r.placement_log = [(engine.now, "cpu0")]
+        r.placement_log = [(engine.now, f"cpu{host}")]
         slot = step.slot_of(r.id)
         step.ctx.host_kv_reserve(slot, r.prompt_len + r.output_len + 1)
+        if host > 0:  # the host process receives the request's context
+            step.ctx.cpu_place(slot, host, r.ctx)
+            step.remote_slots[slot] = host
         engine._inject(r)
         out.append(r)
     return out
@@ -346,7 +354,8 @@ def bench_config(args, model, cpu_threads: int, world: int) -> dict:
             "gpu_kv_tokens": args.gpu_kv_tokens, "max_piggyback_per_layer": args.max_piggyback,
             "merge_decision": args.merges, "be_arrivals_per_s": args.be_rate,
             "cpu_threads_per_replica": cpu_threads, "parallelism": f"replicas x{world}",
-            "l2": "working set (16 GB weights/iteration) > 126 MB L2"}
+            "l2": "working set (16 GB weights/iteration) > 126 MB L2",
+            **({"cpu_hosts": 1 + args.remote_hosts} if getattr(args, "remote_hosts", 0) else {})}
 
 
 def replica_workers(cpus: list) -> list:
@@ -439,6 +448,23 @@ class Replica:
         self.be_fixed = (32768, 136) if args.workload == "longctx" else None
         fit_be_chains(args, model, local_world, verbose=rank == 0)
         rt = self.rt = _replica_rt(args, model, local, local_world, device)
+        self.remote = None
+        if args.remote_hosts:
+            # remote CPU hosts: separate processes on the cores
+            # outside this replica's set (the other NUMA node), reached over TCP
+            from paper_2603_12831_b200 import cpu_host
+
+            others = sorted(set(os.sched_getaffinity(0)) - set(cpus))
+            k = args.remote_hosts
+            per = len(others) // k
+            sets = [others[i * per:(i + 1) * per] for i in range(k)] if per else None
+            self.remote = cpu_host.RemoteHosts(model, k, threads=max(1, per or 2),
+                                               max_slots=rt.max_slots, cpu_sets=sets)
+            import atexit
+
+            atexit.register(self.remote.close)
+            rt.remote_hosts = tuple((h.addr, h.port) for h in self.remote.hosts)
+            self.remote_threads = [max(1, per or 2)] * k
         # make_ctx (a TP group's rank 0): the caller builds the context -- the
         # shard, the group's exchange and shared tags -- and mirrors it
         self.step = LiveCudaStep(model, rt, weight_seed=args.seed,
@@ -739,6 +765,10 @@ def run_ours(args) -> None:
         "data": "synthetic (random-init weights, synthetic KV, Poisson LS trace)",
         "config": bench_config(args, model, rep.rt.cpu_threads, world),
         "iterations_timed": len(iters), "warmup_iterations": warm_iters,
+        **({"remote_hosts": {"n": args.remote_hosts, "threads": rep.remote_threads,
+                             "per_host": [step.ctx.remote_stats(h)
+                                          for h in range(1, args.remote_hosts + 1)]}}
+           if rep.remote else {}),
         "gpus_active": int(min(tot[6], n_dev * (world // max(1, local_world)))),
         "gpus_time_shared": bool(local_world > n_dev),
         "be_prefill_tok_s": (sum(i.get("be_chunk_tokens", 0) for i in iters) * world
@@ -927,6 +957,9 @@ def main() -> None:
     ap.add_argument("--route", default="seeded", choices=["seeded", "round_robin"],
                     help="N>1: per-replica seeded traces, or one global trace routed")
     ap.add_argument("--pin", type=int, default=1, help="pin CPU-attention workers")
+    ap.add_argument("--remote-hosts", type=int, default=0,
+                    help="remote CPU hosts (cpu_host processes on the other cores, over TCP); "
+                         "the BE backlog is spread over the local and remote hosts")
     ap.add_argument("--profile-steps", type=int, default=160,
                     help="profiled iterations after the timed region (device breakdown)")
     args = ap.parse_args()

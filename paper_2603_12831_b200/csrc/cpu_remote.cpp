@@ -157,9 +157,24 @@ class RemoteHost {
   void push(RemoteOp op) {
     {
       std::lock_guard<std::mutex> g(mu_);
+      if (op.op == RM_PUT) ++puts_pending_;
       q_.push_back(std::move(op));
     }
     cv_.notify_all();
+  }
+
+  // waits until no queued PUT still has to read a local host region
+  bool flush_puts() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return failed_ || puts_pending_ == 0; });
+    return !failed_;
+  }
+
+  // waits for the reply of the op whose `done` flag is `flag`
+  bool wait_flag(const std::atomic<bool>& flag) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return failed_ || flag.load(); });
+    return !failed_;
   }
 
   // waits until every queued op has been sent (and every reply received)
@@ -216,6 +231,7 @@ class RemoteHost {
       {
         std::lock_guard<std::mutex> g(mu_);
         sending_ = false;
+        if (op.op == RM_PUT) --puts_pending_;
         if (!ok) failed_ = true;
       }
       cv_.notify_all();
@@ -281,6 +297,7 @@ class RemoteHost {
   std::condition_variable cv_;
   std::deque<RemoteOp> q_, replies_;
   bool sending_ = false, stop_ = false, failed_ = false;
+  int puts_pending_ = 0;
   std::thread sender_, receiver_;
 };
 
@@ -337,12 +354,17 @@ void remote_attend(RemoteHost* r, int slot, int layer, int ctx, cudaEvent_t ev, 
   r->push(std::move(op));
 }
 
-void remote_get(RemoteHost* r, int slot, int ctx, bf16* region, int cap) {
+bool remote_get(RemoteHost* r, int slot, int ctx, bf16* region, int cap) {
   RemoteOp op{RM_GET, slot, ctx, 0};
   op.dst = region;
   op.dst_cap = cap;
+  auto flag = std::make_shared<std::atomic<bool>>(false);
+  op.done = [flag] { flag->store(true); };
   r->push(std::move(op));
+  return r->wait_flag(*flag);  // the receiver notifies after done()
 }
+
+bool remote_flush_puts(RemoteHost* r) { return r->flush_puts(); }
 
 void remote_free(RemoteHost* r, int slot) { r->push(RemoteOp{RM_FREE, slot, 0, 0}); }
 

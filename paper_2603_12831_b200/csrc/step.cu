@@ -1024,7 +1024,7 @@ int hs_host_kv_release(hs_ctx* c, int slot) {
     // the relay may still read the region (a queued PUT): drain it first
     remote_free(c->remotes[h], slot);
     c->slot_host[slot].store(0, std::memory_order_release);
-    if (!remote_quiesce(c->remotes[h]))
+    if (!remote_flush_puts(c->remotes[h]))
       return set_error(HS_E_CUDA, "remote CPU host %d: connection failed", h);
   }
   // the slot's last completion tag stands for nothing any more: a later
@@ -1865,11 +1865,10 @@ int hs_cpu_place(hs_ctx* c, int slot, int host, int tokens) {
   const int cur = slot_host_of(c, slot);
   if (cur == host) return HS_OK;
   if (cur > 0) {  // back from a remote host: its KV (with every appended token) into the region
-    remote_get(c->remotes[cur], slot, tokens, host_region(c, slot), hr.cap);
+    const bool ok = remote_get(c->remotes[cur], slot, tokens, host_region(c, slot), hr.cap);
     remote_free(c->remotes[cur], slot);
     c->slot_host[slot].store(0, std::memory_order_release);
-    if (!remote_quiesce(c->remotes[cur]))
-      return set_error(HS_E_CUDA, "remote CPU host %d: connection failed", cur);
+    if (!ok) return set_error(HS_E_CUDA, "remote CPU host %d: connection failed", cur);
   }
   if (host > 0) {
     remote_put(c->remotes[host], slot, tokens, host_region(c, slot), hr.cap);
