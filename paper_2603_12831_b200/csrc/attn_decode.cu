@@ -119,8 +119,7 @@ __global__ void __launch_bounds__(kDecThreads * WG, WG == 1 ? 2 : 1)
   const int first = min(kStages, npages);
   if (threadIdx.x == 0)
     for (int i = 0; i < min(first, safe); ++i) issue(i);
-  pdl_wait();  // q and the new token's K/V are visible from here on
-  pdl_trigger();
+  pdl_enter();  // q and the new token's K/V are visible from here on
   if (threadIdx.x == 0)
     for (int i = min(first, safe); i < first; ++i) issue(i);
 
@@ -415,8 +414,7 @@ __global__ void decode_combine_kernel(const float* __restrict__ o_part,
                                       const int* __restrict__ row_chunk_begin, int rows, int n_q,
                                       int n_kv, bf16* __restrict__ out, int out_row_stride,
                                       float* __restrict__ lse_out) {
-  pdl_wait();  // dependent data of the previous kernel is visible
-  pdl_trigger();
+  pdl_enter();  // dependent data of the previous kernel is visible
   const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (pair >= rows * n_q) return;

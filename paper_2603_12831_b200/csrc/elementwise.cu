@@ -120,8 +120,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // ---------------------------------------------------------------- embedding
 __global__ void embed_kernel(const int* __restrict__ tokens, const bf16* __restrict__ emb, int d,
                              float* __restrict__ h) {
-  pdl_wait();  // dependent data of the previous kernel is visible
-  pdl_trigger();
+  pdl_enter();  // dependent data of the previous kernel is visible
   const int r = blockIdx.x;
   const bf16* src = emb + static_cast<size_t>(tokens[r]) * d;
   float* dst = h + static_cast<size_t>(r) * d;
@@ -143,8 +142,7 @@ int rmsnorm_rows(const float* h, int rows, int d, const float* w, float eps, bf1
 // ---------------------------------------------------------------- split-K
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, size_t total,
                                      float* __restrict__ out) {
-  pdl_wait();  // dependent data of the previous kernel is visible
-  pdl_trigger();
+  pdl_enter();  // dependent data of the previous kernel is visible
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     float s = 0.f;
@@ -170,8 +168,7 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
     residual_add_norm_kernel(const float* __restrict__ part, Planes splits, int rows, int d,
                              float* __restrict__ h, const float* __restrict__ w, float eps,
                              bf16* __restrict__ out, int ld_out, RowIo io) {
-  pdl_wait();  // dependent data of the previous kernel is visible
-  pdl_trigger();
+  pdl_enter();  // dependent data of the previous kernel is visible
   __shared__ float red[32];
   __shared__ float ssq_all[kNormCluster];
   cg::cluster_group cluster = cg::this_cluster();
@@ -339,8 +336,7 @@ __global__ void __launch_bounds__(256)
     residual_add_norm_rows_kernel(const float* __restrict__ part, Planes splits, int rows, int d,
                                   float* __restrict__ h, const float* __restrict__ w, float eps,
                                   bf16* __restrict__ out, int ld_out, RowIo io) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter();
   __shared__ float red[32];
   const int r = blockIdx.x;
   float* x = h + static_cast<size_t>(r) * d;
@@ -447,8 +443,7 @@ __global__ void __launch_bounds__(256)
                             int q_row_stride, bf16* __restrict__ kv_pool, KvGeom geom, int layer,
                             const int* __restrict__ page_table, int pt_stride,
                             bf16* __restrict__ ship, int ship_stride, int permuted, RowCopy rc) {
-  pdl_wait();  // dependent data of the previous kernel is visible
-  pdl_trigger();
+  pdl_enter();  // dependent data of the previous kernel is visible
   const int r = blockIdx.y;
   if (r >= rows) {  // merged rows: host attention result -> attention buffer
     const int i = r - rows;
@@ -557,8 +552,7 @@ int qkv_rope_scatter(const float* part, const Planes& splits, int rows, int n_q,
 __global__ void __launch_bounds__(256)
     silu_mul_kernel(const float* __restrict__ part, Planes splits, int rows, int ffn,
                     bf16* __restrict__ act, int ld_act, int permuted) {
-  pdl_wait();  // dependent data of the previous kernel is visible
-  pdl_trigger();
+  pdl_enter();  // dependent data of the previous kernel is visible
   const int r = blockIdx.y;
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= ffn) return;
@@ -600,8 +594,7 @@ __device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
 __global__ void __cluster_dims__(kArgCluster, 1, 1) __launch_bounds__(512)
     argmax_kernel(const float* __restrict__ part, Planes splits, int rows, int vocab,
                   int* __restrict__ tokens, float* __restrict__ logits_out) {
-  pdl_wait();  // dependent data of the previous kernel is visible
-  pdl_trigger();
+  pdl_enter();  // dependent data of the previous kernel is visible
   __shared__ float sv[32];
   __shared__ int si[32];
   __shared__ float cta_v;
@@ -705,8 +698,7 @@ __global__ void lse_merge_kernel(const bf16* __restrict__ parts, const float* __
                                  int n_parts, int rows, int n_q, int part_stride,
                                  int row_stride_parts, bf16* __restrict__ out,
                                  int out_row_stride) {
-  pdl_wait();  // dependent data of the previous kernel is visible
-  pdl_trigger();
+  pdl_enter();  // dependent data of the previous kernel is visible
   const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (pair >= rows * n_q) return;

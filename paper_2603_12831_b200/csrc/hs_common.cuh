@@ -55,6 +55,25 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 // Blocks until every prerequisite grid has completed and its writes are visible.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Entry of a kernel whose every dependent read and write follows the wait.
+// HS_PDL_EARLY: release the dependents first, so the next GEMM is scheduled
+// while this kernel still waits on / runs behind its own predecessor and its
+// weight prefetch (issued before its own wait) fills the gap.  Safe because
+// every PDL-launched kernel of the library waits before touching dependent
+// data, and a dependent is launched only once all of this grid's CTAs are
+// resident (no residency deadlock).
+#ifndef HS_PDL_EARLY
+#define HS_PDL_EARLY 1
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if HS_PDL_EARLY
+  pdl_trigger();
+  pdl_wait();
+#else
+  pdl_wait();
+  pdl_trigger();
+#endif
+}
 
 // ----------------------------------------------------------------------------
 // mbarrier
