@@ -19,7 +19,10 @@
 // local worker would (completion tag, then the output FIFO).
 //
 // Wire format: a 16-byte header {op, slot, a, b} followed by the payload.
-//   PUT    slot, a=ctx tokens, b=cap   + KV rows: [layers][2][n_kv] x ctx*hd
+//   PUT    slot, a=ctx tokens, b=cap     (allocates the slot's KV)
+//   PUT_ROWS slot, a=first row, b=rows  + that many of the [layers][2][n_kv]
+//          rows, ctx*hd each (a placement streams in chunks, so other
+//          slots' items and fetches are not stuck behind a 1 GB context)
 //   ATTEND slot, a=layer (1-based), b=ctx  + one q|k|v row ((n_q+2n_kv)*hd)
 //   GET    slot, a=ctx                      -> KV reply (rows as PUT)
 //   FREE   slot
@@ -38,7 +41,9 @@
 #include <cerrno>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <deque>
+#include <map>
 #include <memory>
 
 #include "hs_step.h"
@@ -49,7 +54,7 @@ namespace {
 
 enum : int32_t {
   RM_HELLO = 1, RM_PUT = 2, RM_ATTEND = 3, RM_GET = 4, RM_FREE = 5, RM_BYE = 6,
-  RM_RESULT = 7, RM_KV = 8, RM_ERR = 9
+  RM_RESULT = 7, RM_KV = 8, RM_ERR = 9, RM_PUT_ROWS = 10
 };
 
 struct RmHdr {
@@ -157,16 +162,19 @@ class RemoteHost {
   void push(RemoteOp op) {
     {
       std::lock_guard<std::mutex> g(mu_);
-      if (op.op == RM_PUT) ++puts_pending_;
+      if (op.op == RM_PUT) ++puts_of_slot_[op.slot];
       q_.push_back(std::move(op));
     }
     cv_.notify_all();
   }
 
-  // waits until no queued PUT still has to read a local host region
-  bool flush_puts() {
+  // waits until no queued or streaming PUT of `slot` still reads its local region
+  bool flush_puts(int slot) {
     std::unique_lock<std::mutex> lk(mu_);
-    cv_.wait(lk, [&] { return failed_ || puts_pending_ == 0; });
+    cv_.wait(lk, [&] {
+      auto it = puts_of_slot_.find(slot);
+      return failed_ || it == puts_of_slot_.end() || it->second == 0;
+    });
     return !failed_;
   }
 
@@ -180,7 +188,9 @@ class RemoteHost {
   // waits until every queued op has been sent (and every reply received)
   bool quiesce() {
     std::unique_lock<std::mutex> lk(mu_);
-    cv_.wait(lk, [&] { return failed_ || (q_.empty() && replies_.empty() && !sending_); });
+    cv_.wait(lk, [&] {
+      return failed_ || (q_.empty() && replies_.empty() && !sending_ && !put_active_);
+    });
     return !failed_;
   }
 
@@ -198,46 +208,103 @@ class RemoteHost {
     cv_.notify_all();
   }
 
+  // Sender: ops leave in FIFO order per slot, but a placement (PUT) streams
+  // in chunks and the other slots' ops overtake it between chunks.  An op of
+  // a slot with a PUT in flight or queued ahead of it waits.
   void send_loop() {
+    const size_t rows_total = kv_row_elems(m_);
+    RemoteOp put;  // the placement being streamed (put_active_)
+    size_t put_row = 0;
+    bool alternate = false;  // a chunk goes next (control ops cannot starve a placement)
     for (;;) {
       RemoteOp op;
+      bool chunk = false;
+      size_t r0 = 0, nr = 0;
       {
         std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
-        if (q_.empty()) {  // stop_ with nothing left to send
+        cv_.wait(lk, [&] { return stop_ || !q_.empty() || put_active_; });
+        if (q_.empty() && !put_active_) {  // stop_ with nothing left to send
           send_hdr(fd_, RM_BYE, 0, 0, 0);
           return;
         }
-        op = std::move(q_.front());
-        q_.pop_front();
+        int pick = -1;
+        blocked_.clear();
+        if (put_active_ && alternate) goto stream_chunk;
+        if (put_active_) blocked_.push_back(put.slot);
+        for (size_t i = 0; i < q_.size(); ++i) {
+          const bool b = std::find(blocked_.begin(), blocked_.end(), q_[i].slot) != blocked_.end();
+          if (q_[i].op == RM_PUT) {
+            if (!b && !put_active_ && pick < 0) {  // start the oldest startable placement
+              pick = static_cast<int>(i);
+              break;
+            }
+            blocked_.push_back(q_[i].slot);
+            continue;
+          }
+          if (!b) {
+            pick = static_cast<int>(i);
+            break;
+          }
+        }
+        if (pick >= 0) {
+          op = std::move(q_[pick]);
+          q_.erase(q_.begin() + pick);
+          if (op.op == RM_PUT) {
+            put = op;
+            put_row = 0;
+            put_active_ = true;
+          }
+        } else {  // every queued op waits for the placement in flight: stream its next chunk
+        stream_chunk:
+          chunk = true;
+          const size_t row_bytes = static_cast<size_t>(put.a) * m_.hd * sizeof(bf16);
+          nr = std::max<size_t>(1, (size_t(4) << 20) / std::max<size_t>(row_bytes, 1));
+          r0 = put_row;
+          nr = std::min(nr, rows_total - r0);
+          put_row += nr;
+        }
         sending_ = true;
+        alternate = put_active_ && !chunk;
       }
       bool ok = true;
-      if (op.ev) cudaEventSynchronize(op.ev);
-      if (op.before_send) op.before_send();
-      const bool reply = op.op == RM_ATTEND || op.op == RM_GET;
-      if (reply) {  // registered before the request leaves: the receiver may see it at once
-        std::lock_guard<std::mutex> g(mu_);
-        replies_.push_back(op);
-      }
-      ok = send_hdr(fd_, op.op, op.slot, op.a, op.b);
-      if (ok && op.op == RM_PUT) {
-        ok = send_kv(fd_, m_, op.src, op.src_cap, op.a);
-        stats[1] += static_cast<int64_t>(op.a) * kv_row_elems(m_) * m_.hd * sizeof(bf16);
-      } else if (ok && op.op == RM_ATTEND) {
-        ok = send_all(fd_, op.src, static_cast<size_t>(m_.qkv_n()) * sizeof(bf16));
-        stats[0] += 1;
+      if (chunk) {
+        ok = send_hdr(fd_, RM_PUT_ROWS, put.slot, static_cast<int32_t>(r0),
+                      static_cast<int32_t>(nr));
+        const size_t row = static_cast<size_t>(put.a) * m_.hd;
+        for (size_t r = r0; ok && r < r0 + nr; ++r)
+          if (row) ok = send_all(fd_, put.src + r * put.src_cap * m_.hd, row * sizeof(bf16));
+        stats[1] += static_cast<int64_t>(nr * row * sizeof(bf16));
+      } else {
+        if (op.ev) cudaEventSynchronize(op.ev);
+        if (op.before_send) op.before_send();
+        const bool reply = op.op == RM_ATTEND || op.op == RM_GET;
+        if (reply) {  // registered before the request leaves: the receiver may see it at once
+          std::lock_guard<std::mutex> g(mu_);
+          replies_.push_back(op);
+        }
+        ok = send_hdr(fd_, op.op, op.slot, op.a, op.b);
+        if (ok && op.op == RM_ATTEND) {
+          ok = send_all(fd_, op.src, static_cast<size_t>(m_.qkv_n()) * sizeof(bf16));
+          stats[0] += 1;
+        }
       }
       {
         std::lock_guard<std::mutex> g(mu_);
         sending_ = false;
-        if (op.op == RM_PUT) --puts_pending_;
+        if (chunk && put_row >= rows_total) {  // placement complete
+          put_active_ = false;
+          --puts_of_slot_[put.slot];
+        } else if (!chunk && op.op == RM_PUT && rows_total == 0) {
+          put_active_ = false;
+          --puts_of_slot_[op.slot];
+        }
         if (!ok) failed_ = true;
       }
       cv_.notify_all();
       if (!ok) {
-        std::fprintf(stderr, "hs remote host: send of op %d (slot %d, %d, %d) failed (%s)\n",
-                     op.op, op.slot, op.a, op.b, std::strerror(errno));
+        std::fprintf(stderr, "hs remote host: send of op %d (slot %d) failed (%s)\n",
+                     chunk ? RM_PUT_ROWS : op.op, chunk ? put.slot : op.slot,
+                     std::strerror(errno));
         return;
       }
     }
@@ -296,8 +363,9 @@ class RemoteHost {
   std::mutex mu_;
   std::condition_variable cv_;
   std::deque<RemoteOp> q_, replies_;
-  bool sending_ = false, stop_ = false, failed_ = false;
-  int puts_pending_ = 0;
+  bool sending_ = false, stop_ = false, failed_ = false, put_active_ = false;
+  std::map<int, int> puts_of_slot_;  // queued or streaming placements per slot
+  std::vector<int> blocked_;         // send_loop scratch
   std::thread sender_, receiver_;
 };
 
@@ -364,7 +432,7 @@ bool remote_get(RemoteHost* r, int slot, int ctx, bf16* region, int cap) {
   return r->wait_flag(*flag);  // the receiver notifies after done()
 }
 
-bool remote_flush_puts(RemoteHost* r) { return r->flush_puts(); }
+bool remote_flush_puts(RemoteHost* r, int slot) { return r->flush_puts(slot); }
 
 void remote_free(RemoteHost* r, int slot) { r->push(RemoteOp{RM_FREE, slot, 0, 0}); }
 
@@ -379,6 +447,7 @@ namespace {
 struct ServerSlot {
   std::vector<bf16> kv;
   int cap = 0;
+  int put_ctx = 0;  // tokens per row of the placement being received
 };
 
 // a crashing host process says where before it dies (it runs unattended)
@@ -428,8 +497,20 @@ bool serve_client(int fd, const ModelCfg& m, ThreadPool& pool, std::mutex& pool_
         if (!slot_ok || h.a < 0 || h.b < h.a) return err(HS_E_CONFIG, "bad PUT");
         ServerSlot& s = slots[h.slot];
         s.cap = h.b;
+        s.put_ctx = h.a;
         s.kv.assign(kv_row_elems(m) * static_cast<size_t>(s.cap) * m.hd, bf16{});
-        if (!recv_kv(fd, m, s.kv.data(), s.cap, h.a)) return false;
+        break;
+      }
+      case RM_PUT_ROWS: {
+        if (!slot_ok || slots[h.slot].cap == 0 || h.a < 0 || h.b < 0 ||
+            static_cast<size_t>(h.a) + h.b > kv_row_elems(m))
+          return err(HS_E_CONFIG, "bad PUT_ROWS");
+        ServerSlot& s = slots[h.slot];
+        const size_t row = static_cast<size_t>(s.put_ctx) * m.hd;
+        for (int r = h.a; r < h.a + h.b; ++r)
+          if (row && !recv_all(fd, s.kv.data() + static_cast<size_t>(r) * s.cap * m.hd,
+                               row * sizeof(bf16)))
+            return false;
         break;
       }
       case RM_ATTEND: {

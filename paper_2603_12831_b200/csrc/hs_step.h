@@ -99,7 +99,7 @@ void remote_attend(RemoteHost* r, int slot, int layer, int ctx, cudaEvent_t ev, 
                    bf16* result, std::function<void()> before_send, std::function<void()> done);
 // blocking: the host's copy (with every appended token) lands in the region
 bool remote_get(RemoteHost* r, int slot, int ctx, bf16* region, int cap);
-bool remote_flush_puts(RemoteHost* r);  // no queued PUT reads a local region any more
+bool remote_flush_puts(RemoteHost* r, int slot);  // no PUT of the slot reads its region any more
 void remote_free(RemoteHost* r, int slot);
 bool remote_quiesce(RemoteHost* r);  // false once the connection failed
 const int64_t* remote_stats(RemoteHost* r);

@@ -1024,7 +1024,7 @@ int hs_host_kv_release(hs_ctx* c, int slot) {
     // the relay may still read the region (a queued PUT): drain it first
     remote_free(c->remotes[h], slot);
     c->slot_host[slot].store(0, std::memory_order_release);
-    if (!remote_flush_puts(c->remotes[h]))
+    if (!remote_flush_puts(c->remotes[h], slot))
       return set_error(HS_E_CUDA, "remote CPU host %d: connection failed", h);
   }
   // the slot's last completion tag stands for nothing any more: a later

@@ -19,7 +19,7 @@ import pytest
 from oracle import llama_ops as O
 from paper_2603_12831_b200.models import TRANSFORMERS
 
-HELLO, PUT, ATTEND, GET, FREE, BYE, RESULT, KV, ERR = range(1, 10)
+HELLO, PUT, ATTEND, GET, FREE, BYE, RESULT, KV, ERR, PUT_ROWS = range(1, 11)
 
 
 def _hdr(op, slot=0, a=0, b=0):
@@ -62,7 +62,10 @@ def test_remote_host_attends_like_the_oracle(host):
     region = O.to_bf16(rng.standard_normal((L, 2, nkv, cap, hd)).astype(np.float32))
     with socket.create_connection((host.addr, host.port)) as s:
         assert _hello(s, cfg)[0] == HELLO
-        s.sendall(_hdr(PUT, slot, ctx, cap) + O.bf16_bits(region[:, :, :, :ctx]).tobytes())
+        # a placement: the header, then the rows in two chunks
+        rows = O.bf16_bits(region[:, :, :, :ctx]).reshape(L * 2 * nkv, ctx * hd)
+        s.sendall(_hdr(PUT, slot, ctx, cap) + _hdr(PUT_ROWS, slot, 0, 3) + rows[:3].tobytes()
+                  + _hdr(PUT_ROWS, slot, 3, len(rows) - 3) + rows[3:].tobytes())
         kv = region.copy()
         for step, layer in enumerate((2, 1, 2)):  # two tokens at layer 2, one at layer 1
             c = ctx + (1 if step == 2 else 0)
