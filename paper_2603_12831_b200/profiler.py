@@ -156,11 +156,36 @@ def fit_decode_attn_nonneg(samples) -> DecodeAttnModel:
     return DecodeAttnModel(float(c[0]), float(c[1]), float(c[2]))
 
 
+def _rel_l1_line(x: np.ndarray, y: np.ndarray) -> tuple[float, float]:
+    """y ~ a*x + b (a, b >= 0) minimising the mean relative error
+    |a*x + b - y| / y -- the accuracy the paper reports.
+    An L1 optimum of a two-parameter line passes through two samples (or
+    one, with a or b at its bound), so the candidates are enumerated."""
+    cands = [(0.0, float(np.median(y)))]
+    for i in range(len(x)):
+        if x[i] > 0:
+            cands.append((float(y[i] / x[i]), 0.0))
+        cands.append((0.0, float(y[i])))
+        for j in range(i + 1, len(x)):
+            if x[j] != x[i]:
+                a = (y[j] - y[i]) / (x[j] - x[i])
+                b = y[i] - a * x[i]
+                if a >= 0 and b >= 0:
+                    cands.append((float(a), float(b)))
+    err = [float(np.mean(np.abs(a * x + b - y) / y)) for a, b in cands]
+    return cands[int(np.argmin(err))]
+
+
 def fit_prefill_attn_nonneg(samples) -> PrefillAttnModel:
+    """Eq. 2 (linear in pairwise units) fitted for the mean relative error:
+    the kernel's time steps with its tile waves at short chunks, which a
+    least-squares line (even on relative residuals) pays for with the many
+    short samples."""
     fit_prefill_attn(samples)
     a = np.asarray(samples, dtype=float)
-    c = _rel_nnls(np.column_stack([a[:, 0], np.ones(len(a))]), a[:, 1])
-    return PrefillAttnModel(float(c[0]), float(c[1]))
+    keep = a[:, 1] > 0
+    per_unit, base = _rel_l1_line(a[keep, 0], a[keep, 1])
+    return PrefillAttnModel(per_unit, base)
 
 
 def accuracy(ctx, models: LatencyModelSet, seed: int = 1, n: int = 12,
