@@ -192,8 +192,11 @@ def prepopulate_be(engine, step, n: int, seed: int, start: int = 0, fixed=None) 
         r.placement_log = [(engine.now, f"cpu{host}")]
         slot = step.slot_of(r.id)
         step.ctx.host_kv_reserve(slot, r.prompt_len + r.output_len + 1)
-        if host > 0:  # the host process receives the request's context
-            step.ctx.cpu_place(slot, host, r.ctx)
+        if host > 0:
+            # the remote host holds the request from now on; its context is as
+            # synthetic as the local backlog's host KV, so none is streamed
+            # (0 tokens placed: the host's region starts zeroed)
+            step.ctx.cpu_place(slot, host, 0)
             step.remote_slots[slot] = host
         engine._inject(r)
         out.append(r)
