@@ -361,6 +361,19 @@ def bench_config(args, model, cpu_threads: int, world: int) -> dict:
             **({"cpu_hosts": 1 + args.remote_hosts} if getattr(args, "remote_hosts", 0) else {})}
 
 
+def _state_summary(eng) -> dict:
+    """Request states at the end of the run, counted (remote-host runs)."""
+    from collections import Counter
+
+    rep = eng.stall_report()
+    cnt = Counter((rid[:2], v[0], v[1], v[2], str(v[3])) for rid, v in rep["reqs"].items())
+    return {"gpu_used": rep["gpu_used"], "host_used": rep["host_used"], "pg": rep["pg"],
+            "counters": {k: eng.counters[k] for k in ("ls_admitted", "swap_in_started",
+                                                       "swap_in_done", "swap_out_started",
+                                                       "swap_out_done", "merges")},
+            "states": {"/".join(k): n for k, n in cnt.most_common(12)}}
+
+
 def replica_workers(cpus: list) -> list:
     """CPU-attention workers of a replica: its cores minus two for the
     engine thread."""
@@ -769,6 +782,7 @@ def run_ours(args) -> None:
         "config": bench_config(args, model, rep.rt.cpu_threads, world),
         "iterations_timed": len(iters), "warmup_iterations": warm_iters,
         **({"remote_hosts": {"n": args.remote_hosts, "threads": rep.remote_threads,
+                             "engine_state": _state_summary(eng),
                              "per_host": [step.ctx.remote_stats(h)
                                           for h in range(1, args.remote_hosts + 1)]}}
            if rep.remote else {}),

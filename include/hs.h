@@ -321,6 +321,12 @@ int hs_cpu_host_serve(const hs_model_cfg* model, const char* bind_addr, int port
                       int max_slots);
 int hs_cpu_host_connect(hs_ctx* ctx, int host, const char* addr, int port);
 int hs_cpu_place(hs_ctx* ctx, int slot, int host, int tokens);
+/* Live swap-in from a remote host without blocking the engine: queue the
+ * fetch of the slot's KV into its host region (and the host's free), then
+ * poll hs_cpu_fetch_done (1 = landed, the slot is local again; 0 = in
+ * flight) before the swap-in DMA. */
+int hs_cpu_fetch_async(hs_ctx* ctx, int slot, int tokens);
+int hs_cpu_fetch_done(hs_ctx* ctx, int slot);
 /* [4]: work items relayed, KV bytes placed, KV bytes fetched back, result bytes */
 int hs_cpu_remote_stats(hs_ctx* ctx, int host, int64_t* stats);
 /* Pipelined iterations: hs_iter_end_async queues the token readback and an

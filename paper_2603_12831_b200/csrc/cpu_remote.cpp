@@ -40,6 +40,7 @@
 
 #include <cerrno>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <deque>
@@ -267,6 +268,10 @@ class RemoteHost {
         alternate = put_active_ && !chunk;
       }
       bool ok = true;
+      static const bool trace = std::getenv("HS_CPU_HOST_TRACE") != nullptr;
+      if (trace)
+        std::fprintf(stderr, "hs remote host: send op %d slot %d\n", chunk ? RM_PUT_ROWS : op.op,
+                     chunk ? put.slot : op.slot);
       if (chunk) {
         ok = send_hdr(fd_, RM_PUT_ROWS, put.slot, static_cast<int32_t>(r0),
                       static_cast<int32_t>(nr));
@@ -434,6 +439,17 @@ bool remote_get(RemoteHost* r, int slot, int ctx, bf16* region, int cap) {
 
 bool remote_flush_puts(RemoteHost* r, int slot) { return r->flush_puts(slot); }
 
+void remote_get_async(RemoteHost* r, int slot, int ctx, bf16* region, int cap,
+                      std::shared_ptr<std::atomic<int>> flag) {
+  RemoteOp op{RM_GET, slot, ctx, 0};
+  op.dst = region;
+  op.dst_cap = cap;
+  op.done = [flag] { flag->store(1, std::memory_order_release); };
+  r->push(std::move(op));
+}
+
+bool remote_failed(RemoteHost* r) { return r->failed(); }
+
 void remote_free(RemoteHost* r, int slot) { r->push(RemoteOp{RM_FREE, slot, 0, 0}); }
 
 bool remote_quiesce(RemoteHost* r) { return r->quiesce(); }
@@ -469,6 +485,7 @@ bool serve_client(int fd, const ModelCfg& m, ThreadPool& pool, std::mutex& pool_
   std::vector<ServerSlot> slots(static_cast<size_t>(max_slots));
   std::vector<bf16> ship(static_cast<size_t>(m.qkv_n())), out(static_cast<size_t>(m.n_q) * m.hd);
   RmHdr cur{};
+  static const bool trace = std::getenv("HS_CPU_HOST_TRACE") != nullptr;
   auto err = [&](int code, const char* msg) {
     std::fprintf(stderr, "hs cpu host: %s (op %d slot %d a %d b %d)\n", msg, cur.op, cur.slot,
                  cur.a, cur.b);
@@ -481,6 +498,7 @@ bool serve_client(int fd, const ModelCfg& m, ThreadPool& pool, std::mutex& pool_
     RmHdr h;
     if (!recv_all(fd, &h, sizeof h)) return true;  // client went away
     cur = h;
+    if (trace) std::fprintf(stderr, "hs cpu host: op %d slot %d a %d b %d\n", h.op, h.slot, h.a, h.b);
     const bool slot_ok = h.slot >= 0 && h.slot < max_slots;
     switch (h.op) {
       case RM_HELLO: {

@@ -164,6 +164,8 @@ struct hs_ctx {
   // replica's own host, unused) and the host each slot's KV lives on
   std::vector<RemoteHost*> remotes;
   std::unique_ptr<std::atomic<int>[]> slot_host;
+  // live swap-ins from a remote host: the slot's pending fetch (host, done flag)
+  std::map<int, std::pair<int, std::shared_ptr<std::atomic<int>>>> fetches;
   // swaps: copy stream + contiguous staging for pack/unpack around one 2D DMA
   cudaStream_t copy_st = nullptr;
   bf16* swap_stage = nullptr;

@@ -4,6 +4,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -99,7 +100,11 @@ void remote_attend(RemoteHost* r, int slot, int layer, int ctx, cudaEvent_t ev, 
                    bf16* result, std::function<void()> before_send, std::function<void()> done);
 // blocking: the host's copy (with every appended token) lands in the region
 bool remote_get(RemoteHost* r, int slot, int ctx, bf16* region, int cap);
-bool remote_flush_puts(RemoteHost* r, int slot);  // no PUT of the slot reads its region any more
+bool remote_flush_puts(RemoteHost* r, int slot);
+// non-blocking fetch (a live swap-in): `flag` becomes 1 once the KV landed
+void remote_get_async(RemoteHost* r, int slot, int ctx, bf16* region, int cap,
+                      std::shared_ptr<std::atomic<int>> flag);
+bool remote_failed(RemoteHost* r);  // no PUT of the slot reads its region any more
 void remote_free(RemoteHost* r, int slot);
 bool remote_quiesce(RemoteHost* r);  // false once the connection failed
 const int64_t* remote_stats(RemoteHost* r);

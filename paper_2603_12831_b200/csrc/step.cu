@@ -1877,6 +1877,35 @@ int hs_cpu_place(hs_ctx* c, int slot, int host, int tokens) {
   return HS_OK;
 }
 
+int hs_cpu_fetch_async(hs_ctx* c, int slot, int tokens) {
+  if (slot < 0 || slot >= c->r.max_slots) return set_error(HS_E_CONFIG, "slot out of range");
+  HostRegion& hr = c->regions[slot];
+  if (!hr.used) return set_error(HS_E_INTEGRITY, "slot %d has no host KV region", slot);
+  if (tokens < 0 || tokens > hr.cap)
+    return set_error(HS_E_CAPACITY, "fetch of %d tokens exceeds the region", tokens);
+  const int cur = slot_host_of(c, slot);
+  if (cur <= 0) return set_error(HS_E_CONFIG, "slot %d is not on a remote host", slot);
+  if (c->fetches.count(slot)) return set_error(HS_E_CONFIG, "slot %d: fetch in flight", slot);
+  auto flag = std::make_shared<std::atomic<int>>(0);
+  remote_get_async(c->remotes[cur], slot, tokens, host_region(c, slot), hr.cap, flag);
+  remote_free(c->remotes[cur], slot);
+  c->fetches[slot] = {cur, flag};
+  return HS_OK;
+}
+
+int hs_cpu_fetch_done(hs_ctx* c, int slot) {
+  auto it = c->fetches.find(slot);
+  if (it == c->fetches.end()) return -set_error(HS_E_CONFIG, "slot %d: no fetch in flight", slot);
+  if (it->second.second->load(std::memory_order_acquire)) {
+    c->slot_host[slot].store(0, std::memory_order_release);
+    c->fetches.erase(it);
+    return 1;
+  }
+  if (remote_failed(c->remotes[it->second.first]))
+    return -set_error(HS_E_CUDA, "remote CPU host %d: connection failed", it->second.first);
+  return 0;
+}
+
 int hs_cpu_remote_stats(hs_ctx* c, int host, int64_t* out) {
   if (host < 1 || host >= static_cast<int>(c->remotes.size()) || !c->remotes[host])
     return set_error(HS_E_CONFIG, "CPU host %d is not connected", host);

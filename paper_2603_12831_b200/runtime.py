@@ -126,8 +126,10 @@ _CTX_SIGS = {
     "hs_cpu_host_connect": [C.c_void_p, C.c_int, C.c_char_p, C.c_int],
     "hs_cpu_place": [C.c_void_p, C.c_int, C.c_int, C.c_int],
     "hs_cpu_remote_stats": [C.c_void_p, C.c_int, C.POINTER(C.c_int64)],
+    "hs_cpu_fetch_async": [C.c_void_p, C.c_int, C.c_int],
+    "hs_cpu_fetch_done": [C.c_void_p, C.c_int],
 }
-_NONNEG_RETURNS = {"hs_iter_end", "hs_cpu_poll", "hs_cpu_in_flight", "hs_swap_done", "hs_mark",
+_NONNEG_RETURNS = {"hs_cpu_fetch_done", "hs_iter_end", "hs_cpu_poll", "hs_cpu_in_flight", "hs_swap_done", "hs_mark",
                    "hs_timer", "hs_iter_poll", "hs_iter_ntokens", "hs_pg_log"}
 _lib._SIGNATURES.update(_CTX_SIGS)
 
@@ -317,6 +319,12 @@ class HsContext:
         """Moves the slot's host KV (its first `tokens` tokens) to CPU host
         `host` (0 = this replica's own host)."""
         self._call("hs_cpu_place", slot, host, tokens)
+
+    def cpu_fetch_async(self, slot: int, tokens: int) -> None:
+        self._call("hs_cpu_fetch_async", slot, tokens)
+
+    def cpu_fetch_done(self, slot: int) -> bool:
+        return self._call("hs_cpu_fetch_done", slot) == 1
 
     def remote_stats(self, host: int) -> dict:
         out = (C.c_int64 * 4)()
@@ -742,6 +750,9 @@ class LiveCudaStep(CudaStep):
         self._marks: list[int] = []
         self.last_device_ms = 0.0
         self.swap_out_tickets: dict[int, str] = {}
+        # swap-ins from remote hosts: ticket -> (slot, tokens, DMA ticket once fetched)
+        self._fetches: dict[int, tuple] = {}
+        self._fetch_seq = 0
         self._inflight: list[tuple[int, list[str], object]] = []  # (ticket, reqs, payload)
         # iterations finished by a blocking drain() (a recompute rebuild
         # needing their tokens) that the engine has not resolved yet: handed
@@ -820,6 +831,7 @@ class LiveCudaStep(CudaStep):
         self._flush_pages()
         self.slots.clear()
         self.remote_slots.clear()
+        self._fetches.clear()
         self.free_slots = list(range(self.rt.max_slots - 1, -1, -1))
         for d in (self.generated, self.prompts, self._tags):
             d.clear()
@@ -906,10 +918,28 @@ class LiveCudaStep(CudaStep):
         s = self.slot_of(req.id)
         self._ensure(s, req.ctx)
         self._flush_pages()
-        self._unplace(s, req.ctx)
+        if self.remote_slots.pop(s, 0):
+            # from a remote host: the KV comes back over the network first
+            # (without blocking the engine), then the DMA is issued by
+            # swap_done; fetch tickets are negative
+            self.ctx.cpu_fetch_async(s, req.ctx)
+            self._fetch_seq -= 1
+            self._fetches[self._fetch_seq] = (s, req.ctx, None)
+            return self._fetch_seq
         return self.ctx.swap_async(s, req.ctx, out=False)
 
     def swap_done(self, ticket: int) -> bool:
+        if ticket in self._fetches:
+            s, n, dma = self._fetches[ticket]
+            if dma is None:
+                if not self.ctx.cpu_fetch_done(s):
+                    return False
+                self._fetches[ticket] = (s, n, self.ctx.swap_async(s, n, out=False))
+                return False
+            if self.ctx.swap_done(dma):
+                del self._fetches[ticket]
+                return True
+            return False
         return self.ctx.swap_done(ticket)
 
     def swap_out_done(self, req) -> None:
