@@ -24,7 +24,8 @@
 //          rows, ctx*hd each (a placement streams in chunks, so other
 //          slots' items and fetches are not stuck behind a 1 GB context)
 //   ATTEND slot, a=layer (1-based), b=ctx  + one q|k|v row ((n_q+2n_kv)*hd)
-//   GET    slot, a=ctx                      -> KV reply (rows as PUT)
+//   GET    slot, a=ctx  -> KV_ROWS replies (slot, a=first row, b=rows + the
+//          rows), streamed in chunks between the RESULTs of later items
 //   FREE   slot
 //   HELLO  a=byte width of an element, + hs_model_cfg ints -> HELLO reply
 //   BYE    a=1: also stop the server
@@ -35,6 +36,7 @@
 #include <signal.h>
 #include <netinet/in.h>
 #include <netinet/tcp.h>
+#include <poll.h>
 #include <sys/socket.h>
 #include <unistd.h>
 
@@ -55,7 +57,7 @@ namespace {
 
 enum : int32_t {
   RM_HELLO = 1, RM_PUT = 2, RM_ATTEND = 3, RM_GET = 4, RM_FREE = 5, RM_BYE = 6,
-  RM_RESULT = 7, RM_KV = 8, RM_ERR = 9, RM_PUT_ROWS = 10
+  RM_RESULT = 7, RM_ERR = 9, RM_PUT_ROWS = 10, RM_KV_ROWS = 11  // 8: retired
 };
 
 struct RmHdr {
@@ -98,22 +100,6 @@ void set_nodelay(int fd) {
 }
 
 size_t kv_row_elems(const ModelCfg& m) { return static_cast<size_t>(2) * m.layers * m.n_kv; }
-
-// KV region [layers][2][n_kv][cap][hd]: the first `ctx` tokens of every
-// (layer, k|v, head) row, sent row by row
-bool send_kv(int fd, const ModelCfg& m, const bf16* region, int cap, int ctx) {
-  const size_t row = static_cast<size_t>(ctx) * m.hd * sizeof(bf16);
-  for (size_t r = 0; r < kv_row_elems(m); ++r)
-    if (row && !send_all(fd, region + r * cap * m.hd, row)) return false;
-  return true;
-}
-
-bool recv_kv(int fd, const ModelCfg& m, bf16* region, int cap, int ctx) {
-  const size_t row = static_cast<size_t>(ctx) * m.hd * sizeof(bf16);
-  for (size_t r = 0; r < kv_row_elems(m); ++r)
-    if (row && !recv_all(fd, region + r * cap * m.hd, row)) return false;
-  return true;
-}
 
 int model_ints(const ModelCfg& m, int32_t* out) {
   out[0] = m.d;
@@ -190,7 +176,8 @@ class RemoteHost {
   bool quiesce() {
     std::unique_lock<std::mutex> lk(mu_);
     cv_.wait(lk, [&] {
-      return failed_ || (q_.empty() && replies_.empty() && !sending_ && !put_active_);
+      return failed_ || (q_.empty() && attends_.empty() && gets_.empty() && !sending_ &&
+                         !put_active_);
     });
     return !failed_;
   }
@@ -285,7 +272,7 @@ class RemoteHost {
         const bool reply = op.op == RM_ATTEND || op.op == RM_GET;
         if (reply) {  // registered before the request leaves: the receiver may see it at once
           std::lock_guard<std::mutex> g(mu_);
-          replies_.push_back(op);
+          (op.op == RM_ATTEND ? attends_ : gets_).push_back(op);
         }
         ok = send_hdr(fd_, op.op, op.slot, op.a, op.b);
         if (ok && op.op == RM_ATTEND) {
@@ -315,49 +302,63 @@ class RemoteHost {
     }
   }
 
+  // Receiver: RESULTs arrive in the order of the ATTENDs, KV_ROWS chunks in
+  // the order of the GETs (one streaming at a time), the two interleaved.
   void recv_loop() {
+    const size_t rows_total = kv_row_elems(m_);
     for (;;) {
       RmHdr h;
       if (!recv_all(fd_, &h, sizeof h)) {
         std::lock_guard<std::mutex> g(mu_);
-        if (!replies_.empty() || !q_.empty()) failed_ = true;
+        if (!attends_.empty() || !gets_.empty() || !q_.empty()) failed_ = true;
         cv_.notify_all();
         return;
       }
+      const bool result = h.op == RM_RESULT;
       RemoteOp op;
       {
         std::lock_guard<std::mutex> g(mu_);
-        if (replies_.empty()) {
-          std::fprintf(stderr, "hs remote host: unexpected message %d (slot %d, %d, %d)\n", h.op,
-                       h.slot, h.a, h.b);
+        std::deque<RemoteOp>& fifo = result ? attends_ : gets_;
+        if ((h.op != RM_RESULT && h.op != RM_KV_ROWS) || fifo.empty()) {
+          if (h.op == RM_ERR) {
+            std::vector<char> msg(static_cast<size_t>(std::max(0, h.b)) + 1, 0);
+            recv_all(fd_, msg.data(), static_cast<size_t>(std::max(0, h.b)));
+            std::fprintf(stderr, "hs remote host: error %d: %s\n", h.a, msg.data());
+          } else {
+            std::fprintf(stderr, "hs remote host: unexpected message %d (slot %d, %d, %d)\n",
+                         h.op, h.slot, h.a, h.b);
+          }
           failed_ = true;
           cv_.notify_all();
           return;
         }
-        op = replies_.front();  // popped once handled: quiesce() waits for it
+        op = fifo.front();  // popped once handled: quiesce() waits for it
       }
-      bool ok = false;
-      if (h.op == RM_RESULT && op.op == RM_ATTEND && h.slot == op.slot && h.a == op.a &&
-          h.b == op.b) {
+      bool ok = false, finished = false;
+      if (result && h.slot == op.slot && h.a == op.a && h.b == op.b) {
         const size_t bytes = static_cast<size_t>(m_.n_q) * m_.hd * sizeof(bf16);
         ok = recv_all(fd_, op.dst, bytes);
         stats[3] += static_cast<int64_t>(bytes);
-      } else if (h.op == RM_KV && op.op == RM_GET && h.slot == op.slot && h.a == op.a) {
-        ok = recv_kv(fd_, m_, op.dst, op.dst_cap, op.a);
-        stats[2] += static_cast<int64_t>(op.a) * kv_row_elems(m_) * m_.hd * sizeof(bf16);
-      } else if (h.op == RM_ERR) {
-        std::vector<char> msg(static_cast<size_t>(std::max(0, h.b)) + 1, 0);
-        recv_all(fd_, msg.data(), static_cast<size_t>(std::max(0, h.b)));
-        std::fprintf(stderr, "hs remote host: error %d: %s\n", h.a, msg.data());
+        finished = true;
+      } else if (!result && h.slot == op.slot && h.a >= 0 && h.b >= 0 &&
+                 static_cast<size_t>(h.a) + h.b <= rows_total) {
+        const size_t row = static_cast<size_t>(op.a) * m_.hd;
+        ok = true;
+        for (int r = h.a; ok && r < h.a + h.b; ++r)
+          if (row) ok = recv_all(fd_, op.dst + static_cast<size_t>(r) * op.dst_cap * m_.hd,
+                                 row * sizeof(bf16));
+        stats[2] += static_cast<int64_t>(h.b * row * sizeof(bf16));
+        finished = static_cast<size_t>(h.a) + h.b == rows_total;
       }
       if (!ok) {
         fail();
         return;
       }
+      if (!finished) continue;
       if (op.done) op.done();
       {
         std::lock_guard<std::mutex> g(mu_);
-        replies_.pop_front();
+        (result ? attends_ : gets_).pop_front();
       }
       cv_.notify_all();
     }
@@ -367,7 +368,7 @@ class RemoteHost {
   int fd_;
   std::mutex mu_;
   std::condition_variable cv_;
-  std::deque<RemoteOp> q_, replies_;
+  std::deque<RemoteOp> q_, attends_, gets_;  // sent ops awaiting their reply
   bool sending_ = false, stop_ = false, failed_ = false, put_active_ = false;
   std::map<int, int> puts_of_slot_;  // queued or streaming placements per slot
   std::vector<int> blocked_;         // send_loop scratch
@@ -494,10 +495,50 @@ bool serve_client(int fd, const ModelCfg& m, ThreadPool& pool, std::mutex& pool_
     send_all(fd, msg, n);
     return false;
   };
+  // the fetch being streamed back (one at a time, in GET order): its rows go
+  // out in ~4 MB chunks whenever no request is waiting on the socket, so the
+  // RESULTs of later items are not held behind a multi-GB context
+  std::deque<RmHdr> gets;  // slot, a = ctx
+  size_t get_row = 0;
+  const size_t rows_total = kv_row_elems(m);
+  auto stream_chunk = [&]() -> bool {
+    const RmHdr g = gets.front();
+    const ServerSlot& sl = slots[g.slot];
+    const size_t row = static_cast<size_t>(g.a) * m.hd;
+    size_t nr = std::max<size_t>(1, (size_t(4) << 20) / std::max<size_t>(row * sizeof(bf16), 1));
+    nr = std::min(nr, rows_total - get_row);
+    if (!send_hdr(fd, RM_KV_ROWS, g.slot, static_cast<int32_t>(get_row), static_cast<int32_t>(nr)))
+      return false;
+    for (size_t r = get_row; r < get_row + nr; ++r)
+      if (row && !send_all(fd, sl.kv.data() + r * sl.cap * m.hd, row * sizeof(bf16))) return false;
+    get_row += nr;
+    if (get_row == rows_total) {
+      gets.pop_front();
+      get_row = 0;
+    }
+    return true;
+  };
+  // a request touching a slot whose fetch is still streaming: finish it first
+  auto drain_gets_of = [&](int slot) -> bool {
+    for (;;) {
+      bool pending = false;
+      for (const RmHdr& g : gets) pending |= g.slot == slot;
+      if (!pending) return true;
+      if (!stream_chunk()) return false;
+    }
+  };
   for (;;) {
+    while (!gets.empty()) {  // stream while no request is waiting
+      pollfd pf{fd, POLLIN, 0};
+      if (::poll(&pf, 1, 0) > 0) break;
+      if (!stream_chunk()) return false;
+    }
     RmHdr h;
     if (!recv_all(fd, &h, sizeof h)) return true;  // client went away
     cur = h;
+    if (h.op != RM_HELLO && h.op != RM_BYE && h.slot >= 0 && h.slot < max_slots &&
+        !drain_gets_of(h.slot))
+      return false;
     if (trace) std::fprintf(stderr, "hs cpu host: op %d slot %d a %d b %d\n", h.op, h.slot, h.a, h.b);
     const bool slot_ok = h.slot >= 0 && h.slot < max_slots;
     switch (h.op) {
@@ -551,15 +592,15 @@ bool serve_client(int fd, const ModelCfg& m, ThreadPool& pool, std::mutex& pool_
       }
       case RM_GET: {
         if (!slot_ok || slots[h.slot].cap < h.a || h.a < 0) return err(HS_E_CONFIG, "bad GET");
-        if (!send_hdr(fd, RM_KV, h.slot, h.a, 0) ||
-            !send_kv(fd, m, slots[h.slot].kv.data(), slots[h.slot].cap, h.a))
-          return false;
+        gets.push_back(h);
         break;
       }
       case RM_FREE:
         if (slot_ok) slots[h.slot] = ServerSlot{};
         break;
       case RM_BYE:
+        while (!gets.empty())
+          if (!stream_chunk()) return false;
         *shutdown = h.a == 1;
         return true;
       default:

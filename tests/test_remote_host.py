@@ -19,7 +19,7 @@ import pytest
 from oracle import llama_ops as O
 from paper_2603_12831_b200.models import TRANSFORMERS
 
-HELLO, PUT, ATTEND, GET, FREE, BYE, RESULT, KV, ERR, PUT_ROWS = range(1, 11)
+HELLO, PUT, ATTEND, GET, FREE, BYE, RESULT, KV, ERR, PUT_ROWS, KV_ROWS = range(1, 12)
 
 
 def _hdr(op, slot=0, a=0, b=0):
@@ -86,9 +86,13 @@ def test_remote_host_attends_like_the_oracle(host):
             assert err < 1.5e-2, (step, err)
         # GET returns the context with the appended tokens (swap-in from the host)
         s.sendall(_hdr(GET, slot, ctx + 2))
-        assert struct.unpack("<4i", _recv(s, 16))[:3] == (KV, slot, ctx + 2)
-        back = np.frombuffer(_recv(s, L * 2 * nkv * (ctx + 2) * hd * 2), np.uint16)
-        back = back.reshape(L, 2, nkv, ctx + 2, hd)
+        rows, n_rows = {}, L * 2 * nkv
+        while len(rows) < n_rows:  # KV_ROWS chunks (slot, first row, rows)
+            op, sl, r0, nr = struct.unpack("<4i", _recv(s, 16))
+            assert op == KV_ROWS and sl == slot and r0 == len(rows), (op, sl, r0, nr)
+            for r in range(r0, r0 + nr):
+                rows[r] = np.frombuffer(_recv(s, (ctx + 2) * hd * 2), np.uint16)
+        back = np.stack([rows[r] for r in range(n_rows)]).reshape(L, 2, nkv, ctx + 2, hd)
         want = O.bf16_bits(kv[:, :, :, :ctx + 2])
         # layer 1 got one appended token (position ctx); its position ctx+1 is unwritten
         assert np.array_equal(back[:, :, :, :ctx], want[:, :, :, :ctx])
@@ -229,3 +233,37 @@ def test_live_engine_with_remote_hosts_matches_oracle_replay(cuda, device_merges
     assert not st.bad, st.bad[:5]
     assert st.max_rel < 2e-2, st.max_rel
     print(f"live remote: iterations={n} tokens={st.compared} merges={st.merges} {stats}")
+
+
+def test_remote_host_streams_fetches_between_results(host):
+    """A fetch (GET) of a long context streams in chunks; an item of another
+    slot sent right behind it is answered between the chunks instead of
+    after the whole context."""
+    cfg = TRANSFORMERS["tiny"]
+    L, nkv, nq, hd = cfg.n_layers, cfg.n_kv, cfg.n_q, cfg.head_dim
+    rng = np.random.default_rng(1)
+    big, small, ctx, cap = 7, 8, 40000, 40100  # 5 MB per row: one row per chunk
+    n_rows = L * 2 * nkv
+    with socket.create_connection((host.addr, host.port)) as s:
+        assert _hello(s, cfg)[0] == HELLO
+        region = rng.integers(0, 1 << 14, (n_rows, ctx * hd)).astype(np.uint16)
+        s.sendall(_hdr(PUT, big, ctx, cap) + _hdr(PUT_ROWS, big, 0, n_rows) + region.tobytes())
+        s.sendall(_hdr(PUT, small, 10, 64) + _hdr(PUT_ROWS, small, 0, n_rows)
+                  + np.zeros((n_rows, 10 * hd), np.uint16).tobytes())
+        ship = np.zeros(cfg.qkv_dim, np.uint16)
+        s.sendall(_hdr(GET, big, ctx) + _hdr(ATTEND, small, 1, 10) + ship.tobytes())
+        got, order = {}, []
+        while len(got) < n_rows or "result" not in order:
+            op, sl, a, b = struct.unpack("<4i", _recv(s, 16))
+            if op == RESULT:
+                assert (sl, a, b) == (small, 1, 10)
+                _recv(s, nq * hd * 2)
+                order.append("result")
+                continue
+            assert op == KV_ROWS and sl == big
+            for r in range(a, a + b):
+                got[r] = np.frombuffer(_recv(s, ctx * hd * 2), np.uint16)
+            order.append("rows")
+        assert all(np.array_equal(got[r], region[r]) for r in range(n_rows))
+        assert order.index("result") < len(order) - 1, order  # not behind the whole context
+        s.sendall(_hdr(FREE, big) + _hdr(FREE, small) + _hdr(BYE, 0, 0))
