@@ -1028,8 +1028,11 @@ int hs_host_kv_release(hs_ctx* c, int slot) {
       return set_error(HS_E_CUDA, "remote CPU host %d: connection failed", h);
   }
   // the slot's last completion tag stands for nothing any more: a later
-  // occupant's item with the same (ctx, layer) must not read as complete
-  retract_tag(c, slot);
+  // occupant's item with the same (ctx, layer) must not read as complete.
+  // Retracted in stream order: a merge of the slot's last result that the
+  // host already launched (pipelined iterations) still checks its tag first.
+  if (cudaMemsetAsync(c->tag_d + slot, 0xff, sizeof(unsigned), c->st) != cudaSuccess)
+    return set_error(HS_E_CUDA, "host_kv_release: tag retract");
   const size_t bytes = region_bytes(c, hr.cap);
   c->free_list.push_back({hr.offset, bytes});
   std::sort(c->free_list.begin(), c->free_list.end());
