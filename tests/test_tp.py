@@ -292,6 +292,9 @@ def _mirror_rank(rank, world, port, q):
             eng.run_live(horizon_s=30.0)
             step.finish()
             mirror.flush(stop=True)
+            if eng.stalled:  # the reference policy's wall-clock wedge (test_live_host.py)
+                q.put((0, "error", "policy wedge", None, None))
+                return
             q.put((0, dict(fake.calls), sorted(fake.pages.items()), len(fake.iters),
                    eng.counters["tokens_total"]))
         else:
@@ -343,9 +346,12 @@ def test_live_tp_mirror_replays_every_call():
         return out, err
 
     # a wall-clock run of two spawned ranks (gloo rendezvous on a fresh port):
-    # one retry for an environmental failure, with its reason printed
+    # retried, with the reason printed, on an environmental failure or the
+    # reference policy's wall-clock wedge (a policy property, not the mirror)
     out, err = attempt()
-    if err is not None:
+    for _ in range(2):
+        if err is None:
+            break
         print("mirror run failed, retrying:", err)
         out, err = attempt()
     assert err is None, err
