@@ -499,6 +499,7 @@ bool serve_client(int fd, const ModelCfg& m, ThreadPool& pool, std::mutex& pool_
   // out in ~4 MB chunks whenever no request is waiting on the socket, so the
   // RESULTs of later items are not held behind a multi-GB context
   std::deque<RmHdr> gets;  // slot, a = ctx
+  std::vector<int> freeing;  // FREEs waiting for their slot's fetch to go out
   size_t get_row = 0;
   const size_t rows_total = kv_row_elems(m);
   auto stream_chunk = [&]() -> bool {
@@ -515,6 +516,17 @@ bool serve_client(int fd, const ModelCfg& m, ThreadPool& pool, std::mutex& pool_
     if (get_row == rows_total) {
       gets.pop_front();
       get_row = 0;
+      // deferred FREEs of slots with no fetch left
+      for (size_t i = 0; i < freeing.size();) {
+        bool pending = false;
+        for (const RmHdr& q : gets) pending |= q.slot == freeing[i];
+        if (pending) {
+          ++i;
+          continue;
+        }
+        slots[freeing[i]] = ServerSlot{};
+        freeing.erase(freeing.begin() + i);
+      }
     }
     return true;
   };
@@ -536,6 +548,16 @@ bool serve_client(int fd, const ModelCfg& m, ThreadPool& pool, std::mutex& pool_
     RmHdr h;
     if (!recv_all(fd, &h, sizeof h)) return true;  // client went away
     cur = h;
+    // a FREE right behind its slot's fetch (the usual swap-in) is deferred
+    // until the stream is out; any other request on that slot drains it
+    if (h.op == RM_FREE && h.slot >= 0 && h.slot < max_slots) {
+      bool streaming = false;
+      for (const RmHdr& g : gets) streaming |= g.slot == h.slot;
+      if (streaming) {
+        freeing.push_back(h.slot);
+        continue;
+      }
+    }
     if (h.op != RM_HELLO && h.op != RM_BYE && h.slot >= 0 && h.slot < max_slots &&
         !drain_gets_of(h.slot))
       return false;

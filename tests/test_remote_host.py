@@ -251,7 +251,9 @@ def test_remote_host_streams_fetches_between_results(host):
         s.sendall(_hdr(PUT, small, 10, 64) + _hdr(PUT_ROWS, small, 0, n_rows)
                   + np.zeros((n_rows, 10 * hd), np.uint16).tobytes())
         ship = np.zeros(cfg.qkv_dim, np.uint16)
-        s.sendall(_hdr(GET, big, ctx) + _hdr(ATTEND, small, 1, 10) + ship.tobytes())
+        # the swap-in pattern: the fetch, its FREE right behind it, then an item
+        s.sendall(_hdr(GET, big, ctx) + _hdr(FREE, big) + _hdr(ATTEND, small, 1, 10)
+                  + ship.tobytes())
         got, order = {}, []
         while len(got) < n_rows or "result" not in order:
             op, sl, a, b = struct.unpack("<4i", _recv(s, 16))
@@ -266,4 +268,4 @@ def test_remote_host_streams_fetches_between_results(host):
             order.append("rows")
         assert all(np.array_equal(got[r], region[r]) for r in range(n_rows))
         assert order.index("result") < len(order) - 1, order  # not behind the whole context
-        s.sendall(_hdr(FREE, big) + _hdr(FREE, small) + _hdr(BYE, 0, 0))
+        s.sendall(_hdr(FREE, small) + _hdr(BYE, 0, 0))
