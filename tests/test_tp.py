@@ -287,7 +287,11 @@ def _mirror_rank(rank, world, port, q):
             mirror = tp.MirrorContext(fake)
             step = LiveCudaStep(sc, rt, ctx=mirror)
             doc = copy.deepcopy(APPENDIX_B)
-            doc["profiles"]["cluster"]["gpu_kv_capacity"] = 1600
+            # 2400 GPU KV tokens: BE requests still swap out (13 swap-outs in
+            # tests/test_live_host.py's run of this budget) but the LS load alone
+            # cannot fill it -- with 1600 the mirrored run, slower per
+            # iteration under a loaded host, hit the policy's wall-clock wedge
+            doc["profiles"]["cluster"]["gpu_kv_capacity"] = 2400
             eng = LiveEngine(scenario_from_dict(doc, "mirror"), step=step, pace_layers=1)
             eng.run_live(horizon_s=30.0)
             step.finish()
